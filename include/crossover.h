@@ -1,0 +1,139 @@
+/*
+ * crossover.h -- C-ABI of libcrossover.so, the B200-native crossover step.
+ *
+ * The reference (colosim, /root/reference/pkg/src/colosim) is pure Python and
+ * has no FFI.  These entry points are the calls its Python API would bind
+ * (ctypes) to execute the crossover step on the device instead of pricing it:
+ *
+ *   cs_pack            replaces  workload.fuse_gradients     (workload.py:94-101)
+ *                                the payload sum becomes a real gather of every
+ *                                gradient tensor into one contiguous bucket.
+ *   cs_unpack_sgd      replaces  equivalence.average_gradients (equivalence.py:150-160)
+ *                           +    equivalence.sgd_step          (equivalence.py:163-168)
+ *                                fixed left-to-right sum over sources, divide by
+ *                                the worker count, SGD(-momentum) update, in place.
+ *   cs_nccl_*          replaces  comm.comm_time_allreduce       (comm.py:87-99)
+ *                                the alpha-beta price becomes a measured NCCL
+ *                                all-reduce on the caller's comm stream.
+ *   cs_gradient_stats  new       warp-reduced sum of squares / non-finite count
+ *                                over a bucket (gradient health, checksums).
+ *
+ * Conventions
+ *   - Ownership: every device buffer (gradients, buckets, parameters, momentum
+ *     buffers, snapshots) is allocated and owned by the caller.  The library
+ *     never allocates on the step path and never frees caller memory.
+ *   - Streams: `stream` is a cudaStream_t passed as void*; NULL = legacy default.
+ *     Every call is an asynchronous enqueue; nothing blocks the host.
+ *   - Descriptor arrays are HOST memory; they are copied into kernel parameters
+ *     at launch (no device-side tables, no per-step H2D copies).
+ *   - Errors: 0 on success; CS_ERR_ARG (<0) for invalid arguments; otherwise a
+ *     cudaError_t value or CS_ERR_NCCL_BASE + ncclResult_t.  cs_last_error()
+ *     returns a thread-local message for the last failure on this thread.
+ *   - Threading: one host thread per process (one process per GPU).  Calls on
+ *     distinct streams are reentrant.
+ */
+#ifndef CROSSOVER_H_
+#define CROSSOVER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CS_API __attribute__((visibility("default")))
+#else
+#define CS_API
+#endif
+
+#define CS_ABI_VERSION 1
+#define CS_ERR_ARG (-1)
+#define CS_ERR_NCCL_BASE 10000
+#define CS_NCCL_UNIQUE_ID_BYTES 128
+#define CS_MAX_SOURCES 8
+
+/* One gradient tensor to gather: src[0:numel) -> dst[0:numel). */
+typedef struct cs_pack_desc {
+  const float* src;   /* device pointer of the gradient tensor (contiguous fp32) */
+  float* dst;         /* device pointer inside the bucket (bucket + offset)      */
+  int64_t numel;      /* elements; 0 is allowed (skipped)                         */
+} cs_pack_desc;
+
+/* One parameter tensor to update from the reduced gradient. */
+typedef struct cs_update_desc {
+  float* param;          /* device pointer, updated in place                      */
+  float* momentum_buf;   /* device pointer or NULL when momentum == 0             */
+  uint64_t grad_offset;  /* byte offset added to every source base (see below)    */
+  uint64_t snap_offset;  /* byte offset into `snapshot` (ignored if snapshot NULL) */
+  int64_t numel;
+} cs_update_desc;
+
+/* Update rule.  rounding = CS_ROUND_REFERENCE reproduces equivalence.sgd_step's
+ * `p - lr * avg` (two roundings, no FMA; momentum/weight_decay must be 0).
+ * rounding = CS_ROUND_TORCH reproduces torch.optim.SGD's single-tensor update
+ * (weight decay, momentum/dampening/nesterov, `p.add_(d, alpha=-lr)` as FMA). */
+enum { CS_ROUND_REFERENCE = 0, CS_ROUND_TORCH = 1 };
+
+typedef struct cs_sgd_hyper {
+  float lr;
+  float momentum;
+  float dampening_complement;  /* 1 - dampening, rounded once from double (ATen's alpha) */
+  float weight_decay;
+  int32_t nesterov;
+  int32_t first_step;  /* momentum buffer is initialised to the gradient      */
+  int32_t divisor;     /* worker count W: the summed gradient is divided by W */
+  int32_t rounding;    /* CS_ROUND_REFERENCE or CS_ROUND_TORCH                */
+} cs_sgd_hyper;
+
+CS_API int cs_abi_version(void);
+CS_API const char* cs_last_error(void);
+
+/* K1: gather n tensors into the bucket (128-bit vector path when src and dst
+ * are 16-byte aligned, scalar otherwise).  Bit-exact copy. */
+CS_API int cs_pack(const cs_pack_desc* descs, int n, void* stream);
+
+/* K2: for every tensor i and element k
+ *     acc  = 0 + g_0 + g_1 + ... + g_{S-1}   (left to right over sources)
+ *     avg  = acc / divisor                      (IEEE division, == equivalence.py:160)
+ *     param, momentum_buf <- SGD(param, avg)   (see cs_sgd_hyper)
+ * where g_s = *(const float*)(sources[s] + descs[i].grad_offset + 4k).
+ * `sources` is a HOST array of n_sources (1..CS_MAX_SOURCES) device byte
+ * addresses: a reduced bucket (after all-reduce), the rows of a simulated-worker
+ * staging buffer, or {0} with grad_offset = raw gradient pointer (W = 1, no bucket).
+ * If snapshot != NULL the updated parameter is also written to
+ * snapshot + snap_offset (per-iteration weight capture for parity). */
+CS_API int cs_unpack_sgd(const cs_update_desc* descs, int n, const uint64_t* sources,
+                  int n_sources, float* snapshot, const cs_sgd_hyper* hyper,
+                  void* stream);
+
+/* Gradient health over a contiguous fp32 range: out[0] += sum of squares
+ * (fp64), out[1] += count of non-finite values.  Deterministic: per-CTA
+ * partials are reduced in a fixed order by the last CTA.  `workspace` must hold
+ * cs_gradient_stats_workspace_bytes(numel) bytes (device, caller-owned, zeroed
+ * once before first use; the kernel leaves it zeroed again). */
+CS_API size_t cs_gradient_stats_workspace_bytes(int64_t numel);
+CS_API int cs_gradient_stats(const float* data, int64_t numel, double* out,
+                      void* workspace, void* stream);
+
+/* NCCL communicator over NVLink / NVSwitch (one per process, one per job set).
+ * min_ctas / max_ctas <= 0 leave NCCL's defaults. */
+CS_API int cs_nccl_version(void);
+CS_API int cs_nccl_get_unique_id(uint8_t* out /* CS_NCCL_UNIQUE_ID_BYTES */);
+CS_API int cs_nccl_init(void** comm, int nranks, int rank, const uint8_t* id,
+                 int min_ctas, int max_ctas);
+CS_API int cs_nccl_allreduce_sum_f32(void* comm, const float* send, float* recv,
+                              size_t count, void* stream);
+CS_API int cs_nccl_reduce_scatter_sum_f32(void* comm, const float* send, float* recv,
+                                   size_t recv_count, void* stream);
+CS_API int cs_nccl_all_gather_f32(void* comm, const float* send, float* recv,
+                           size_t send_count, void* stream);
+CS_API int cs_nccl_async_error(void* comm);
+CS_API int cs_nccl_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CROSSOVER_H_ */

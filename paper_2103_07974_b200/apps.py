@@ -1,0 +1,314 @@
+"""Co-located training apps for the configs of BASELINE.json.
+
+* linear problems   -- the reference's own numeric workload (equivalence.py:42-147):
+                       least squares / logistic regression, dim 8, seeded datasets.
+* MLP 784-256-10    -- config 1 (cross-entropy, batch 64 per worker).
+* ResNet-50, VGG-16, BERT-base -- configs 2/3/5 (bf16 autocast, fp32 master
+                       parameters and gradients, synthetic data).
+
+Host-side data generation uses the reference's seeding scheme verbatim in
+meaning (equivalence.py:84-132): dataset ``default_rng(dataset_seed)``, initial
+parameters ``default_rng([seed, 0])``, mini-batch indices
+``default_rng([seed, 1, t, worker]).integers(0, size, batch)``.  That is
+*input* generation only: all index arrays and datasets are uploaded once and
+every gather, forward, backward and update runs on the device.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from .fusion import SgdSettings
+from .scheduler import App
+
+__all__ = [
+    "LossKind",
+    "SgdConfig",
+    "make_dataset",
+    "initial_parameters",
+    "batch_indices",
+    "LinearModel",
+    "linear_app",
+    "MlpConfig",
+    "make_mlp_dataset",
+    "mlp_initial_parameters",
+    "mlp_app",
+    "resnet50_app",
+    "vgg16_app",
+    "bert_app",
+    "synthetic_image_batches",
+]
+
+
+# ---------------------------------------------------------------------------
+# the reference's linear problems
+# ---------------------------------------------------------------------------
+class LossKind(Enum):
+    LEAST_SQUARES = "least_squares"
+    LOGISTIC = "logistic_regression"
+
+
+@dataclass(frozen=True)
+class SgdConfig:
+    """Synchronous-SGD setup of one linear job (equivalence.py:47-65)."""
+
+    learning_rate: float
+    workers: int
+    loss: LossKind
+    dataset_seed: int
+    dim: int = 8
+    dataset_size: int = 128
+    batch_size: int = 16
+
+    def __post_init__(self):
+        if self.learning_rate <= 0:
+            raise ValueError("learning_rate must be > 0")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if min(self.dim, self.dataset_size, self.batch_size) < 1:
+            raise ValueError("dim, dataset_size and batch_size must be >= 1")
+
+
+def make_dataset(config: SgdConfig) -> tuple[np.ndarray, np.ndarray]:
+    """Seeded synthetic dataset (equivalence.py:84-95 seeding)."""
+    rng = np.random.default_rng(config.dataset_seed)
+    x = rng.standard_normal((config.dataset_size, config.dim))
+    z = x @ rng.standard_normal(config.dim)
+    y = z if config.loss is LossKind.LEAST_SQUARES else (z > 0).astype(np.float64)
+    return x, y
+
+
+def initial_parameters(dim: int, rng_seed: int) -> np.ndarray:
+    """equivalence.py:98-100 seeding: default_rng([seed, 0]).standard_normal(dim)."""
+    return np.random.default_rng([rng_seed, 0]).standard_normal(dim)
+
+
+def batch_indices(rng_seed: int, iteration: int, worker: int, dataset_size: int,
+                  batch_size: int) -> np.ndarray:
+    """equivalence.py:129-132 seeding for the mini-batch of (iteration, worker)."""
+    rng = np.random.default_rng([rng_seed, 1, iteration, worker])
+    return rng.integers(0, dataset_size, size=batch_size)
+
+
+def _index_table(rng_seed: int, iterations: int, workers: int, size: int, batch: int) -> np.ndarray:
+    out = np.empty((iterations, workers, batch), dtype=np.int64)
+    for t in range(iterations):
+        for w in range(workers):
+            out[t, w] = batch_indices(rng_seed, t + 1, w, size, batch)
+    return out
+
+
+class LinearModel(torch.nn.Module):
+    def __init__(self, init: np.ndarray):
+        super().__init__()
+        self.weight = torch.nn.Parameter(torch.as_tensor(init, dtype=torch.float32).clone())
+
+
+def _linear_loss(kind: LossKind):
+    def loss_fn(model: LinearModel, batch):
+        x, y = batch
+        z = x @ model.weight
+        if kind is LossKind.LEAST_SQUARES:
+            r = z - y
+            return 0.5 * torch.mean(r * r)
+        return torch.mean(F.softplus(z) - y * z)   # logaddexp(0, z) - y z
+    return loss_fn
+
+
+class _GatherData:
+    """data(t, worker) -> (x[idx], y[idx]) gathered on the device."""
+
+    def __init__(self, x: torch.Tensor, y: torch.Tensor, idx: torch.Tensor):
+        self.x, self.y, self.idx = x, y, idx
+
+    def __call__(self, t: int, worker: int):
+        sel = self.idx[t - 1, worker]
+        return self.x.index_select(0, sel), self.y.index_select(0, sel)
+
+
+def linear_app(config: SgdConfig, job_id: str, rng_seed: int, iterations: int,
+               device: torch.device, local_workers: int | None = None) -> App:
+    """One of the reference's synthetic SGD jobs as a device app."""
+    x, y = make_dataset(config)
+    idx = _index_table(rng_seed, iterations, config.workers, config.dataset_size, config.batch_size)
+    model = LinearModel(initial_parameters(config.dim, rng_seed)).to(device)
+    data = _GatherData(torch.as_tensor(x, dtype=torch.float32, device=device),
+                       torch.as_tensor(y, dtype=torch.float32, device=device),
+                       torch.as_tensor(idx, device=device))
+    return App(job_id, model, _linear_loss(config.loss), data,
+               SgdSettings(config.learning_rate), iterations,
+               local_workers=config.workers if local_workers is None else local_workers,
+               samples_per_batch=config.batch_size)
+
+
+# ---------------------------------------------------------------------------
+# config 1: MLP 784-256-10
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class MlpConfig:
+    learning_rate: float = 0.05
+    workers: int = 2
+    dataset_seed: int = 0
+    in_dim: int = 784
+    hidden: int = 256
+    classes: int = 10
+    dataset_size: int = 4096
+    batch_size: int = 64
+    momentum: float = 0.0
+
+
+def make_mlp_dataset(config: MlpConfig) -> tuple[np.ndarray, np.ndarray]:
+    rng = np.random.default_rng(config.dataset_seed)
+    x = rng.standard_normal((config.dataset_size, config.in_dim))
+    y = rng.integers(0, config.classes, size=config.dataset_size)
+    return x, y
+
+
+def mlp_initial_parameters(config: MlpConfig, rng_seed: int) -> list[np.ndarray]:
+    """[W1 (h, in), b1 (h), W2 (c, h), b2 (c)], N(0,1)/sqrt(fan_in), drawn in that order."""
+    rng = np.random.default_rng([rng_seed, 0])
+    s1, s2 = 1.0 / math.sqrt(config.in_dim), 1.0 / math.sqrt(config.hidden)
+    w1 = rng.standard_normal((config.hidden, config.in_dim)) * s1
+    b1 = rng.standard_normal(config.hidden) * s1
+    w2 = rng.standard_normal((config.classes, config.hidden)) * s2
+    b2 = rng.standard_normal(config.classes) * s2
+    return [w1, b1, w2, b2]
+
+
+def _mlp_module(config: MlpConfig, init: list[np.ndarray]) -> torch.nn.Module:
+    m = torch.nn.Sequential(torch.nn.Linear(config.in_dim, config.hidden), torch.nn.ReLU(),
+                            torch.nn.Linear(config.hidden, config.classes))
+    with torch.no_grad():
+        for p, v in zip(m.parameters(), init):
+            p.copy_(torch.as_tensor(v, dtype=torch.float32))
+    return m
+
+
+def _ce_loss(model, batch):
+    x, y = batch
+    return F.cross_entropy(model(x), y)
+
+
+def mlp_app(config: MlpConfig, job_id: str, rng_seed: int, iterations: int,
+            device: torch.device, local_workers: int | None = None,
+            worker_count: int | None = None) -> App:
+    """Config 1 app: two of these co-located, W = 2, batch 64 per worker."""
+    x, y = make_mlp_dataset(config)
+    workers = config.workers if worker_count is None else worker_count
+    idx = _index_table(rng_seed, iterations, workers, config.dataset_size, config.batch_size)
+    model = _mlp_module(config, mlp_initial_parameters(config, rng_seed)).to(device)
+    data = _GatherData(torch.as_tensor(x, dtype=torch.float32, device=device),
+                       torch.as_tensor(y, dtype=torch.int64, device=device),
+                       torch.as_tensor(idx, device=device))
+    return App(job_id, model, _ce_loss, data,
+               SgdSettings(config.learning_rate, momentum=config.momentum), iterations,
+               local_workers=config.workers if local_workers is None else local_workers,
+               samples_per_batch=config.batch_size)
+
+
+# ---------------------------------------------------------------------------
+# configs 2/3/5: image / text models with synthetic data
+# ---------------------------------------------------------------------------
+class _CycleData:
+    """Cycles through pre-built batches (device-resident or pinned host)."""
+
+    def __init__(self, batches: list[tuple]):
+        self.batches = batches
+
+    def __call__(self, t: int, worker: int):
+        return self.batches[(t - 1) % len(self.batches)]
+
+
+def synthetic_image_batches(batch: int, n_batches: int, seed: int, device: torch.device,
+                            host_uint8: bool = False, classes: int = 1000, size: int = 224):
+    """Synthetic ImageNet-shaped batches.
+
+    device mode: bf16 N(0,1) images [B,3,H,W] in channels_last + int64 labels on the GPU.
+    host mode:   pinned uint8 NHWC images + labels (the e2e path copies them every step
+                 and normalises on the device).
+    """
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    out = []
+    for _ in range(n_batches):
+        labels = torch.randint(0, classes, (batch,), generator=g)
+        if host_uint8:
+            img = torch.randint(0, 256, (batch, size, size, 3), dtype=torch.uint8, generator=g)
+            out.append((img.pin_memory(), labels.pin_memory()))
+        else:
+            gd = torch.Generator(device=device).manual_seed(seed + len(out))
+            img = torch.randn((batch, 3, size, size), generator=gd, device=device,
+                              dtype=torch.bfloat16).contiguous(memory_format=torch.channels_last)
+            out.append((img, labels.to(device)))
+    return out
+
+
+def _image_loss(model, batch):
+    x, y = batch
+    if x.dtype == torch.uint8:   # e2e path: NHWC bytes -> normalised bf16 channels_last
+        x = x.permute(0, 3, 1, 2).to(torch.bfloat16).sub_(127.5).mul_(1.0 / 64.0)
+    return F.cross_entropy(model(x), y)
+
+
+def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
+               device: torch.device, seed: int, host_data: bool, sgd: SgdSettings,
+               n_batches: int = 2) -> App:
+    model = model.to(device).to(memory_format=torch.channels_last)
+    data = _CycleData(synthetic_image_batches(batch, n_batches, seed, device, host_uint8=host_data))
+    return App(job_id, model, _image_loss, data, sgd, iterations,
+               autocast_dtype=torch.bfloat16, samples_per_batch=batch)
+
+
+DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
+
+
+def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
+                 host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD) -> App:
+    import torchvision
+
+    torch.manual_seed(seed)
+    return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device, seed,
+                      host_data, sgd)
+
+
+def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
+              host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD) -> App:
+    import torchvision
+
+    torch.manual_seed(seed)
+    return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device, seed,
+                      host_data, sgd)
+
+
+def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,
+             seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-4, momentum=0.9)) -> App:
+    """BERT-base encoder (transformers BertModel defaults) with a masked-token-style loss."""
+    from transformers import BertConfig, BertModel
+
+    torch.manual_seed(seed)
+    cfg = BertConfig()
+    model = BertModel(cfg, add_pooling_layer=True).to(device)
+    head = torch.nn.Linear(cfg.hidden_size, cfg.vocab_size, bias=False).to(device)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    ids = torch.randint(0, cfg.vocab_size, (batch, seq_len), generator=g).to(device)
+    labels = torch.randint(0, cfg.vocab_size, (batch, seq_len), generator=g).to(device)
+
+    class _Wrap(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.bert, self.head = model, head
+
+    wrap = _Wrap()
+
+    def loss_fn(m, b):
+        i, lab = b
+        h = m.bert(input_ids=i).last_hidden_state
+        return F.cross_entropy(m.head(h).float().view(-1, cfg.vocab_size), lab.view(-1))
+
+    return App(job_id, wrap, loss_fn, _CycleData([(ids, labels)]), sgd, iterations,
+               autocast_dtype=torch.bfloat16, samples_per_batch=batch)

@@ -1,0 +1,164 @@
+// crossover_abi.cu -- extern "C" entry points of libcrossover.so (see include/crossover.h).
+//
+// Host-side work per call is O(n_tensors): validate, build the chunk prefix,
+// copy descriptors into a by-value kernel-parameter block, launch.  No device
+// allocation, no synchronisation, no host<->device copies.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "crossover.h"
+#include "crossover_internal.h"
+
+namespace cs {
+thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return 0;
+  return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static int64_t chunks_of(int64_t numel) { return (numel + kChunk - 1) / kChunk; }
+
+template <int CAP>
+static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
+  static thread_local PackArgs<CAP> a;  // ~28 KB for the large capacity: keep off the stack
+  a.n = n;
+  int64_t c = 0;
+  for (int i = 0; i < n; ++i) {
+    a.chunk_begin[i] = (int)c;
+    a.src[i] = d[i].src;
+    a.dst[i] = d[i].dst;
+    a.numel[i] = d[i].numel;
+    c += chunks_of(d[i].numel);
+  }
+  a.chunk_begin[n] = (int)c;
+  if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_pack: %lld chunks exceed grid limit", (long long)c);
+  a.total_chunks = (int)c;
+  return cuda_status(launch_pack<CAP>(a, s), "cs_pack launch");
+}
+
+template <int CAP>
+static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources, int nsrc,
+                        float* snapshot, const cs_sgd_hyper* h, cudaStream_t s) {
+  static thread_local UpdateArgs<CAP> a;
+  a.n = n;
+  a.nsrc = nsrc;
+  a.pad_ = 0;
+  a.snapshot = snapshot;
+  for (int k = 0; k < CS_MAX_SOURCES; ++k) a.base[k] = k < nsrc ? sources[k] : 0;
+  a.h = *h;
+  int64_t c = 0;
+  for (int i = 0; i < n; ++i) {
+    a.chunk_begin[i] = (int)c;
+    a.param[i] = d[i].param;
+    a.mom[i] = d[i].momentum_buf;
+    a.grad_off[i] = d[i].grad_offset;
+    a.snap_off[i] = d[i].snap_offset;
+    a.numel[i] = d[i].numel;
+    c += chunks_of(d[i].numel);
+  }
+  a.chunk_begin[n] = (int)c;
+  if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_unpack_sgd: %lld chunks exceed grid limit", (long long)c);
+  a.total_chunks = (int)c;
+  const bool mom = h->momentum != 0.0f;
+  return cuda_status(launch_unpack_sgd<CAP>(a, mom, s), "cs_unpack_sgd launch");
+}
+
+}  // namespace cs
+
+using namespace cs;
+
+extern "C" {
+
+int cs_abi_version(void) { return CS_ABI_VERSION; }
+
+const char* cs_last_error(void) { return g_last_error.c_str(); }
+
+int cs_pack(const cs_pack_desc* descs, int n, void* stream) {
+  if (n < 0 || (n > 0 && descs == nullptr))
+    return set_error(CS_ERR_ARG, "cs_pack: invalid descriptor array (n=%d)", n);
+  for (int i = 0; i < n; ++i) {
+    if (descs[i].numel < 0)
+      return set_error(CS_ERR_ARG, "cs_pack: tensor %d has negative numel", i);
+    if (descs[i].numel > 0 && (descs[i].src == nullptr || descs[i].dst == nullptr))
+      return set_error(CS_ERR_ARG, "cs_pack: tensor %d has a null pointer", i);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int b = 0; b < n; b += kCapLarge) {
+    const int m = std::min(kCapLarge, n - b);
+    int rc = m <= kCapSmall ? pack_batch<kCapSmall>(descs + b, m, s)
+           : m <= kCapMid   ? pack_batch<kCapMid>(descs + b, m, s)
+                            : pack_batch<kCapLarge>(descs + b, m, s);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int cs_unpack_sgd(const cs_update_desc* descs, int n, const uint64_t* sources,
+                  int n_sources, float* snapshot, const cs_sgd_hyper* hyper,
+                  void* stream) {
+  if (n < 0 || (n > 0 && descs == nullptr))
+    return set_error(CS_ERR_ARG, "cs_unpack_sgd: invalid descriptor array (n=%d)", n);
+  if (hyper == nullptr) return set_error(CS_ERR_ARG, "cs_unpack_sgd: hyper is NULL");
+  if (n_sources < 1 || n_sources > CS_MAX_SOURCES || sources == nullptr)
+    return set_error(CS_ERR_ARG, "cs_unpack_sgd: n_sources=%d outside [1, %d]", n_sources,
+                     CS_MAX_SOURCES);
+  if (hyper->divisor < 1)
+    return set_error(CS_ERR_ARG, "cs_unpack_sgd: divisor must be >= 1 (got %d)", hyper->divisor);
+  if (!(hyper->lr > 0.0f))
+    return set_error(CS_ERR_ARG, "cs_unpack_sgd: learning rate must be > 0");
+  if (hyper->rounding != CS_ROUND_REFERENCE && hyper->rounding != CS_ROUND_TORCH)
+    return set_error(CS_ERR_ARG, "cs_unpack_sgd: unknown rounding mode %d", hyper->rounding);
+  if (hyper->rounding == CS_ROUND_REFERENCE &&
+      (hyper->momentum != 0.0f || hyper->weight_decay != 0.0f))
+    return set_error(CS_ERR_ARG,
+                     "cs_unpack_sgd: reference rounding has no momentum / weight decay");
+  if (hyper->nesterov && (hyper->momentum <= 0.0f || hyper->dampening_complement != 1.0f))
+    return set_error(CS_ERR_ARG, "cs_unpack_sgd: nesterov needs momentum > 0 and dampening 0");
+  const bool mom = hyper->momentum != 0.0f;
+  for (int i = 0; i < n; ++i) {
+    if (descs[i].numel < 0)
+      return set_error(CS_ERR_ARG, "cs_unpack_sgd: tensor %d has negative numel", i);
+    if (descs[i].numel > 0 && (descs[i].param == nullptr || (mom && descs[i].momentum_buf == nullptr)))
+      return set_error(CS_ERR_ARG, "cs_unpack_sgd: tensor %d has a null pointer", i);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int b = 0; b < n; b += kCapLarge) {
+    const int m = std::min(kCapLarge, n - b);
+    int rc = m <= kCapSmall ? update_batch<kCapSmall>(descs + b, m, sources, n_sources, snapshot, hyper, s)
+           : m <= kCapMid   ? update_batch<kCapMid>(descs + b, m, sources, n_sources, snapshot, hyper, s)
+                            : update_batch<kCapLarge>(descs + b, m, sources, n_sources, snapshot, hyper, s);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+size_t cs_gradient_stats_workspace_bytes(int64_t numel) {
+  return 256 + (size_t)stats_grid(numel) * 2 * sizeof(double);
+}
+
+int cs_gradient_stats(const float* data, int64_t numel, double* out, void* workspace,
+                      void* stream) {
+  if (numel < 0 || out == nullptr || workspace == nullptr || (numel > 0 && data == nullptr))
+    return set_error(CS_ERR_ARG, "cs_gradient_stats: invalid arguments");
+  return cuda_status(launch_stats(data, numel, out, workspace, (cudaStream_t)stream),
+                     "cs_gradient_stats launch");
+}
+
+}  // extern "C"

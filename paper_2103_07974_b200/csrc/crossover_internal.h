@@ -1,0 +1,62 @@
+// crossover_internal.h -- launch-parameter layouts shared by the kernels and the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "crossover.h"
+
+namespace cs {
+
+constexpr int kThreads = 256;                      // 8 warps per CTA
+constexpr int kUnroll = 4;                         // 128-bit loads in flight per thread
+constexpr int kChunk = kThreads * 4 * kUnroll;     // 4096 fp32 = 16 KB per CTA
+constexpr int kStatsMaxGrid = 148 * 8;             // fixed -> deterministic partial order
+
+// descriptor capacities per launch (kernel parameters are <= 32 KB on sm_70+)
+constexpr int kCapSmall = 16;
+constexpr int kCapMid = 128;
+constexpr int kCapLarge = 512;
+
+template <int CAP>
+struct PackArgs {
+  int n;
+  int total_chunks;
+  int chunk_begin[CAP + 1];
+  const float* src[CAP];
+  float* dst[CAP];
+  int64_t numel[CAP];
+};
+
+template <int CAP>
+struct UpdateArgs {
+  int n;
+  int total_chunks;
+  int nsrc;
+  int pad_;
+  float* snapshot;
+  uint64_t base[CS_MAX_SOURCES];
+  cs_sgd_hyper h;
+  int chunk_begin[CAP + 1];
+  float* param[CAP];
+  float* mom[CAP];
+  uint64_t grad_off[CAP];
+  uint64_t snap_off[CAP];
+  int64_t numel[CAP];
+};
+
+static_assert(sizeof(PackArgs<kCapLarge>) < 32000, "pack args exceed kernel param space");
+static_assert(sizeof(UpdateArgs<kCapLarge>) < 32000, "update args exceed kernel param space");
+
+template <int CAP>
+cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s);
+template <int CAP>
+cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
+cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
+                         cudaStream_t s);
+int stats_grid(int64_t numel);
+
+// thread-local error reporting shared by every translation unit of the library
+int set_error(int code, const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+
+}  // namespace cs

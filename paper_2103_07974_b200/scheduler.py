@@ -1,0 +1,468 @@
+"""The crossover scheduler as a device pipeline of CUDA streams and events.
+
+Reference: colosim.scheduler (scheduler.py:55-258) -- a rotation driver over one
+GPU lane and one NIC lane, with two policies:
+
+* ``crossover`` (Alg. 1, scheduler.py:141-174): apps take turns on the GPU in
+  plan order; when app j's backward ends its fused gradient is queued on the
+  NIC and the GPU moves on to app j+1, so j's sync overlaps j+1's compute.
+  Compute (j, t) may start only after sync (j, t-1) completed (bypassed at
+  t = 1); if the head app is not ready the GPU idles -- it never skips ahead.
+* ``sequential`` (scheduler.py:177-193): compute, then sync to completion while
+  the GPU idles, then the next app.
+
+Device mapping (one process per GPU, every rank hosts every app):
+
+  compute stream  (lane gpu0):  [wait update_done[j]]  fwd(j,t)  bwd(j,t)  record bwd_done
+  comm stream     (lane nic0):  wait bwd_done  K1 pack -> C1 NCCL all-reduce -> K2 update
+                                record update_done[j]
+
+The single comm stream is the reference's single FIFO NIC lane shared by all
+apps: a later app's sync can never overtake an earlier one, which
+is what makes strict head-of-line stalling equivalent to the reference even
+when one app's sync is long.  The host only enqueues; it never blocks inside
+``step()``.  The emitted span order -- compute (j, t) then sync (j, t), slot by
+slot in rotation order -- is the reference's append order (engine.py:146) and is
+returned as a measured ``Trace``.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from dataclasses import dataclass, field
+from enum import Enum
+from fractions import Fraction
+from typing import Any, Callable, Sequence
+
+import torch
+
+from .comm import NcclCommunicator
+from .engine import GPU_LANE_ID, NIC_LANE_ID, Phase, SpanRecorder, Trace
+from .errors import ConfigError, DeadlockError
+from .fusion import FusedGradientSync, SgdSettings
+from .workload import JobProfile
+
+__all__ = [
+    "Policy",
+    "App",
+    "SchedulePlan",
+    "JobRuntimeState",
+    "CrossoverScheduler",
+    "simulate",
+    "schedule_crossover",
+    "schedule_sequential",
+    "rotation_schedule",
+    "steady_state_period",
+    "predicted_speedup",
+    "overlap_roofline",
+    "GPU_LANE_ID",
+    "NIC_LANE_ID",
+]
+
+
+class Policy(Enum):
+    CROSSOVER = "crossover"
+    SEQUENTIAL = "sequential"
+
+
+@dataclass
+class App:
+    """A co-located data-parallel training app (the device analogue of JobProfile).
+
+    ``loss_fn(model, batch)`` runs the forward pass and returns a scalar loss;
+    ``data(iteration, worker)`` returns that worker's batch for iteration t
+    (1-based; ``worker`` is the global worker index = rank * local_workers + w)
+    as a tuple of tensors, either already on the device or in (pinned) host
+    memory -- host batches are copied on a dedicated H2D stream.
+    """
+
+    job_id: str
+    model: torch.nn.Module
+    loss_fn: Callable[[torch.nn.Module, Any], torch.Tensor]
+    data: Callable[[int, int], Sequence[torch.Tensor]]
+    sgd: SgdSettings
+    iterations: int
+    local_workers: int = 1
+    autocast_dtype: torch.dtype | None = None
+    params: list[torch.Tensor] | None = None
+    samples_per_batch: int = 0   # for samples/s accounting (per worker)
+
+    def __post_init__(self):
+        if self.iterations < 1:
+            raise ValueError(f"job {self.job_id!r}: iterations must be >= 1")
+        if self.params is None:
+            self.params = [p for p in self.model.parameters() if p.requires_grad]
+
+
+@dataclass(frozen=True)
+class SchedulePlan:
+    """Ordered apps sharing the GPU(s) plus the policy (scheduler.py:60-77).
+
+    Job order is the rotation order.  ``jobs`` may hold :class:`App` objects
+    (device execution) or reference ``JobProfile`` records (schedule-only).
+    """
+
+    policy: Policy
+    jobs: tuple
+    cluster: Any = None
+
+    def __post_init__(self):
+        object.__setattr__(self, "jobs", tuple(self.jobs))
+        if not self.jobs:
+            raise ValueError("plan must contain at least one job")
+        ids = [j.job_id for j in self.jobs]
+        if len(set(ids)) != len(ids):
+            raise ValueError("job ids must be unique within a plan")
+
+
+@dataclass
+class JobRuntimeState:
+    """Per-app bookkeeping of the rotation driver (scheduler.py:80-87) + device state."""
+
+    job_id: str
+    next_iteration: int = 1
+    awaiting_sync: bool = False
+    sync_of_iteration: int = 0
+    # device side
+    app: App | None = None
+    sync: FusedGradientSync | None = None
+    update_done: Any = None          # torch.cuda.Event of the last K2
+    held: Any = None                 # gradients still read by the comm stream
+    losses: list = field(default_factory=list)
+
+
+def rotation_schedule(job_order: Sequence[str], iterations: Sequence[int]) -> list[tuple[str, str, str, int]]:
+    """The emitted phase schedule for a plan, as the device pipeline issues it.
+
+    Rotation in plan order from a cursor, skipping exhausted apps
+    (scheduler.py:106-115); each dispatched slot emits forward, backward on the
+    GPU lane then the sync on the NIC lane (scheduler.py:117-128).  The order is
+    a pure function of (job order, budgets) -- identical for both policies.
+    """
+    done = {j: 0 for j in job_order}
+    budget = dict(zip(job_order, iterations))
+    out = []
+    n = len(job_order)
+    cursor = 0
+    remaining = sum(iterations)
+    while remaining:
+        for k in range(n):
+            j = job_order[(cursor + k) % n]
+            if done[j] < budget[j]:
+                cursor = (cursor + k) % n
+                break
+        j = job_order[cursor]
+        t = done[j] + 1
+        out += [(GPU_LANE_ID, j, "forward", t), (GPU_LANE_ID, j, "backward", t),
+                (NIC_LANE_ID, j, "sync", t)]
+        done[j] = t
+        remaining -= 1
+        cursor = (cursor + 1) % n
+    return out
+
+
+class _KernelTimer:
+    """CUDA-event brackets around K1/C1/K2 on the comm stream (for the roofline)."""
+
+    def __init__(self, stream):
+        self.stream = stream
+        self.records: list[tuple[str, Any, Any]] = []
+        self._open: dict[str, Any] = {}
+
+    def begin(self, name: str) -> None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self._open[name] = ev
+
+    def end(self, name: str) -> None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self.records.append((name, self._open.pop(name), ev))
+
+    def summary(self) -> dict[str, list[float]]:
+        out: dict[str, list[float]] = {}
+        for name, a, b in self.records:
+            b.synchronize()
+            out.setdefault(name, []).append(a.elapsed_time(b))
+        return out
+
+    def clear(self) -> None:
+        self.records.clear()
+
+
+class CrossoverScheduler:
+    """Registers co-located apps and steps them under crossover or sequential sync.
+
+    One instance per process (= per GPU).  ``step()`` dispatches one rotation
+    slot (one app's forward+backward plus its sync) and returns immediately;
+    ``run()`` steps until every app exhausted its budget and returns the
+    measured trace.
+    """
+
+    def __init__(self, policy: Policy = Policy.CROSSOVER, device: torch.device | int | None = None,
+                 comm: NcclCommunicator | None = None, record_spans: bool = True,
+                 record_weights: bool = False, align: int = 32, sync_mode: str = "auto",
+                 time_kernels: bool = False, comm_priority: int = -1,
+                 perturb: tuple[int, int] | None = None):
+        if not torch.cuda.is_available():
+            raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
+        if not isinstance(policy, Policy):
+            raise ValueError("policy must be a Policy")
+        self.policy = policy
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else (device.index if isinstance(device, torch.device) else device))
+        self.comm = comm
+        self.rank = comm.rank if comm is not None else 0
+        self.align = align
+        self.sync_mode = sync_mode
+        self.record_weights = record_weights
+        self.perturb = perturb
+        with torch.cuda.device(self.device):
+            self.compute_stream = torch.cuda.Stream(self.device)
+            lo, hi = torch.cuda.Stream.priority_range()
+            prio = max(hi, min(lo, comm_priority))
+            self.comm_stream = torch.cuda.Stream(self.device, priority=prio)
+            self.h2d_stream = torch.cuda.Stream(self.device)
+        self.recorder = SpanRecorder(torch, record_spans)
+        self.timer = _KernelTimer(self.comm_stream) if time_kernels else None
+        self.states: list[JobRuntimeState] = []
+        self.cursor = 0
+        self._last_update = None
+        self._started = False
+
+    # -- registration (≙ building a SchedulePlan of JobProfiles) -------------
+    def register(self, app: App) -> JobRuntimeState:
+        if self._started:
+            raise ConfigError("register every app before the first step()")
+        if any(s.job_id == app.job_id for s in self.states):
+            raise ValueError("job ids must be unique within a plan")
+        for p in app.params:
+            if p.device != self.device:
+                raise ConfigError(f"job {app.job_id!r}: parameters must be on {self.device}")
+        sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
+                                 self.sync_mode, app.iterations if self.record_weights else 0)
+        st = JobRuntimeState(app.job_id, app=app, sync=sync)
+        self.states.append(st)
+        return st
+
+    @property
+    def job_order(self) -> list[str]:
+        return [s.job_id for s in self.states]
+
+    # -- rotation (scheduler.py:106-122) -------------------------------------
+    def _next_with_work(self) -> JobRuntimeState | None:
+        n = len(self.states)
+        for k in range(n):
+            probe = (self.cursor + k) % n
+            st = self.states[probe]
+            if st.next_iteration <= st.app.iterations:
+                self.cursor = probe
+                return st
+        return None
+
+    def pending(self) -> list[tuple[str, int]]:
+        out = []
+        for st in self.states:
+            if st.next_iteration <= st.app.iterations:
+                out.append((st.job_id, st.next_iteration))
+        return out
+
+    def _to_device(self, batch: Sequence[torch.Tensor]) -> tuple:
+        if all(not isinstance(x, torch.Tensor) or x.device == self.device for x in batch):
+            return tuple(batch)
+        with torch.cuda.stream(self.h2d_stream):
+            dev = tuple(x.to(self.device, non_blocking=True) if isinstance(x, torch.Tensor) else x
+                        for x in batch)
+        ev = torch.cuda.Event()
+        ev.record(self.h2d_stream)
+        self.compute_stream.wait_event(ev)
+        for x in dev:
+            if isinstance(x, torch.Tensor):
+                x.record_stream(self.compute_stream)
+        return dev
+
+    def step(self) -> bool:
+        """Dispatch one rotation slot; False once every app is exhausted."""
+        if not self.states:
+            raise ConfigError("no apps registered")
+        if not self._started:
+            self._started = True
+            self.recorder.start(self.compute_stream)
+        st = self._next_with_work()
+        if st is None:
+            return False
+        app, t = st.app, st.next_iteration
+        cs, ms = self.compute_stream, self.comm_stream
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+        with torch.cuda.stream(cs):
+            # Alg. 1 readiness (scheduler.py:158): compute (j, t) after sync (j, t-1).
+            if self.policy is Policy.CROSSOVER:
+                if t > 1:
+                    cs.wait_event(st.update_done)
+            elif self._last_update is not None:
+                # sequential baseline: the GPU idles until the previous sync completed
+                cs.wait_event(self._last_update)
+            # stream-ordered after this app's own K2, so the caching allocator may
+            # now reuse the previous iteration's gradient memory on this stream
+            st.held = None
+            workers = [self.rank * app.local_workers + w for w in range(app.local_workers)]
+            batches = [self._to_device(app.data(t, w)) for w in workers]
+            e_f0 = ev()
+            e_f0.record(cs)
+            amp = (torch.autocast("cuda", dtype=app.autocast_dtype) if app.autocast_dtype
+                   else contextlib.nullcontext())
+            losses = []
+            with amp:
+                for b in batches:
+                    losses.append(app.loss_fn(app.model, b))
+            e_f1 = ev()
+            e_f1.record(cs)
+            grads = [list(torch.autograd.grad(loss, app.params, allow_unused=True))
+                     for loss in losses]
+            e_b1 = ev()
+            e_b1.record(cs)
+        st.losses.append(losses[0].detach())
+        st.held = grads
+        st.awaiting_sync, st.sync_of_iteration = True, t
+
+        with torch.cuda.stream(ms):
+            ms.wait_event(e_b1)
+            e_s0 = ev()
+            e_s0.record(ms)
+            st.sync.sync(grads, ms.cuda_stream, t - 1 if self.record_weights else None, self.timer)
+            if self.perturb is not None and self.perturb == (self.job_index(st.job_id), t):
+                _nudge_first_coordinate(app.params[0], st.sync, t - 1 if self.record_weights else None)
+            e_s1 = ev()
+            e_s1.record(ms)
+        st.update_done = e_s1
+        self._last_update = e_s1
+
+        self.recorder.add(GPU_LANE_ID, st.job_id, Phase.FORWARD, t, e_f0, e_f1)
+        self.recorder.add(GPU_LANE_ID, st.job_id, Phase.BACKWARD, t, e_f1, e_b1)
+        self.recorder.add(NIC_LANE_ID, st.job_id, Phase.SYNC, t, e_s0, e_s1)
+        st.next_iteration = t + 1
+        self.cursor = (self.cursor + 1) % len(self.states)
+        return True
+
+    def job_index(self, job_id: str) -> int:
+        return self.job_order.index(job_id)
+
+    def drain(self) -> None:
+        """Wait for the final syncs (the drain of Alg. 1) and release gradients."""
+        join = torch.cuda.Event()
+        join.record(self.comm_stream)
+        self.compute_stream.wait_event(join)
+        self.compute_stream.synchronize()
+        self.comm_stream.synchronize()
+        for st in self.states:
+            st.held = None
+            st.awaiting_sync = False
+        if self.comm is not None:
+            self.comm.check_async_error()
+
+    def run(self) -> Trace:
+        """Step every app through its budget; returns the measured trace."""
+        while self.step():
+            pass
+        self.drain()
+        stuck = self.pending()
+        if stuck:
+            raise DeadlockError(stuck[0][0], stuck[0][1], f"policy={self.policy.value}")
+        return self.recorder.resolve()
+
+    def weights(self, job_id: str) -> torch.Tensor:
+        """[iterations, bucket] per-iteration weights captured by K2 (record_weights=True)."""
+        st = self.states[self.job_index(job_id)]
+        if st.sync.snapshot is None:
+            raise ConfigError("record_weights=False")
+        return st.sync.snapshot
+
+    @property
+    def kernel_launches(self) -> int:
+        return sum(s.sync.kernel_launches for s in self.states)
+
+
+def _nudge_first_coordinate(param: torch.Tensor, sync: FusedGradientSync, row: int | None) -> None:
+    """Fault-injection hook of run_crossover (equivalence.py:214-219): +1 ulp on p[0]."""
+    flat = torch.as_strided(param, (1,), (1,))
+    flat.copy_(torch.nextafter(flat, torch.full_like(flat, float("inf"))))
+    if row is not None:
+        sync.snapshot[row, :1].copy_(flat)
+
+
+# -- reference-shaped entry points --------------------------------------------
+
+def _run_plan(plan: SchedulePlan, **kw) -> Trace:
+    if not all(isinstance(j, App) for j in plan.jobs):
+        raise ConfigError("device execution needs App jobs (JobProfile plans have no model)")
+    sched = CrossoverScheduler(plan.policy, **kw)
+    for app in plan.jobs:
+        sched.register(app)
+    try:
+        return sched.run()
+    except DeadlockError as exc:
+        raise DeadlockError(exc.job_id, exc.iteration, f"policy={plan.policy.value}") from exc
+
+
+def schedule_crossover(plan: SchedulePlan, **kw) -> Trace:
+    """Run the plan on the device under Alg. 1 (scheduler.py:209-212)."""
+    if plan.policy is not Policy.CROSSOVER:
+        raise ValueError("plan.policy must be crossover")
+    return _run_plan(plan, **kw)
+
+
+def schedule_sequential(plan: SchedulePlan, **kw) -> Trace:
+    """Run the plan on the device under the non-overlapped baseline (scheduler.py:215-218)."""
+    if plan.policy is not Policy.SEQUENTIAL:
+        raise ValueError("plan.policy must be sequential")
+    return _run_plan(plan, **kw)
+
+
+def simulate(plan: SchedulePlan, **kw) -> Trace:
+    """Run the plan under its configured policy (scheduler.py:221-225)."""
+    return schedule_crossover(plan, **kw) if plan.policy is Policy.CROSSOVER else schedule_sequential(plan, **kw)
+
+
+# -- closed forms (scheduler.py:228-258) and the overlap roofline --------------
+
+def _homogeneous(comps: Sequence[int], comms: Sequence[int]) -> tuple[int, int]:
+    if len(set(comps)) != 1 or len(set(comms)) != 1:
+        raise ValueError("closed forms require homogeneous jobs (equal compute and sync "
+                         "durations); simulate heterogeneous plans instead")
+    return comps[0], comms[0]
+
+
+def steady_state_period(policy: Policy, comps: Sequence[int], comms: Sequence[int]) -> int:
+    """N*max(comp, comm) under crossover, N*(comp+comm) sequential (homogeneous)."""
+    comp, comm = _homogeneous(comps, comms)
+    n = len(comps)
+    return n * max(comp, comm) if policy is Policy.CROSSOVER else n * (comp + comm)
+
+
+def predicted_speedup(comps: Sequence[int], comms: Sequence[int]) -> Fraction:
+    """(comp + comm) / max(comp, comm) = 1 + rho while rho <= 1 (homogeneous)."""
+    comp, comm = _homogeneous(comps, comms)
+    return Fraction(comp + comm, max(comp, comm))
+
+
+def overlap_roofline(comps: Sequence[float], comms: Sequence[float]) -> dict[str, float]:
+    """Per-rotation lower bounds on the crossover period.
+
+    ``north_star``: max(Σcomp, Σcomm).  ``tight``: the reference's bound that
+    also includes maxᵢ(compᵢ + commᵢ) (tests/test_scheduler.py:260-269).
+    ``sequential``: Σ(compᵢ + commᵢ), the back-to-back period.
+    """
+    s_comp, s_comm = float(sum(comps)), float(sum(comms))
+    tight = max(s_comp, s_comm, max(c + m for c, m in zip(comps, comms)))
+    return {"north_star": max(s_comp, s_comm), "tight": tight, "sequential": s_comp + s_comm}
+
+
+def profile_of(app: App, forward_ns: int, backward_ns: int) -> JobProfile:
+    """Reference JobProfile of a registered app with measured durations."""
+    from .workload import tensor_specs_from_module
+
+    fwd, bwd = max(int(forward_ns), 0), max(int(backward_ns), 0)
+    if fwd + bwd == 0:
+        bwd = 1  # JobProfile requires forward + backward > 0 (workload.py:61-62)
+    return JobProfile(app.job_id, fwd, bwd, tensor_specs_from_module(app.model), app.iterations)

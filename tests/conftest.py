@@ -1,0 +1,48 @@
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+sys.path.insert(0, str(ROOT))
+
+try:
+    from hypothesis import settings
+
+    settings.register_profile("ci", derandomize=True, deadline=None)
+    settings.load_profile("ci")
+except ImportError:  # pragma: no cover
+    pass
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+
+
+@pytest.fixture(scope="session")
+def schedule_golden():
+    return json.loads((GOLDEN / "schedule.json").read_text())["cases"]
+
+
+@pytest.fixture(scope="session")
+def equivalence_golden():
+    meta = json.loads((GOLDEN / "equivalence_meta.json").read_text())
+    arrays = dict(np.load(GOLDEN / "equivalence.npz"))
+    return meta, arrays
+
+
+@pytest.fixture(scope="session")
+def fixtures_golden():
+    return json.loads((GOLDEN / "fixtures.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def cuda_device():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda", 0)

@@ -1,0 +1,90 @@
+"""libcrossover.so loads on a CPU-only host and exports exactly what include/crossover.h declares."""
+
+import ctypes
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def _declared():
+    text = (ROOT / "include" / "crossover.h").read_text()
+    return sorted(set(re.findall(r"CS_API\s+[\w\s\*]+?\b(cs_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ("cs_pack", "cs_unpack_sgd", "cs_nccl_init", "cs_nccl_allreduce_sum_f32",
+                 "cs_nccl_destroy", "cs_last_error", "cs_gradient_stats"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2103_07974_b200 import _lib
+
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (cs_\w+)", out))
+    assert set(_declared()) <= exported
+    for name in _declared():
+        assert hasattr(_lib.lib, name)
+        assert name in _lib.EXPORTS, f"{name} not bound in _lib.EXPORTS"
+
+
+def test_library_is_sm100a():
+    from paper_2103_07974_b200 import _lib
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_layouts():
+    from paper_2103_07974_b200 import _lib
+
+    assert _lib.PACK_DESC.itemsize == 24
+    assert _lib.UPDATE_DESC.itemsize == 40
+    assert ctypes.sizeof(_lib.SgdHyper) == 32
+    assert _lib.lib.cs_abi_version() == 1
+
+
+def test_argument_errors_without_gpu():
+    """Invalid calls fail in host validation with a message; nothing reaches CUDA."""
+    from paper_2103_07974_b200 import _lib
+
+    assert _lib.lib.cs_pack(None, -1, None) == _lib.CS_ERR_ARG
+    assert b"invalid descriptor" in _lib.lib.cs_last_error()
+    d = np.zeros(1, dtype=_lib.PACK_DESC)
+    d["numel"] = 5
+    with pytest.raises(_lib.CrossoverLibError, match="null pointer"):
+        _lib.pack(d, 0)
+    u = np.zeros(1, dtype=_lib.UPDATE_DESC)
+    h = _lib.SgdHyper(lr=0.1, divisor=0, rounding=0)
+    with pytest.raises(_lib.CrossoverLibError, match="divisor"):
+        _lib.unpack_sgd(u, np.zeros(1, dtype=np.uint64), 0, h, 0)
+    h = _lib.SgdHyper(lr=0.1, momentum=0.9, divisor=1, rounding=_lib.CS_ROUND_REFERENCE)
+    with pytest.raises(_lib.CrossoverLibError, match="reference rounding"):
+        _lib.unpack_sgd(u, np.zeros(1, dtype=np.uint64), 0, h, 0)
+    assert _lib.lib.cs_unpack_sgd(u.ctypes.data, 1, np.zeros(9, dtype=np.uint64).ctypes.data, 9,
+                                  None, ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=1)), None) == _lib.CS_ERR_ARG
+    assert _lib.lib.cs_nccl_init(None, 0, 0, None, 0, 0) == _lib.CS_ERR_ARG
+
+
+def test_nccl_version_is_torchs():
+    import torch
+
+    from paper_2103_07974_b200 import _lib
+
+    v = _lib.lib.cs_nccl_version()
+    major, minor, patch = torch.cuda.nccl.version()
+    assert v == major * 10000 + minor * 100 + patch
+
+
+def test_product_has_no_oracle_dependency():
+    """The product package never imports the CPU oracle (no fallback path)."""
+    for path in (ROOT / "paper_2103_07974_b200").rglob("*.py"):
+        src = path.read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), path
