@@ -385,10 +385,11 @@ class CrossoverScheduler:
 
 def _nudge_first_coordinate(param: torch.Tensor, sync: FusedGradientSync, row: int | None) -> None:
     """Fault-injection hook of run_crossover (equivalence.py:214-219): +1 ulp on p[0]."""
-    flat = torch.as_strided(param, (1,), (1,))
-    flat.copy_(torch.nextafter(flat, torch.full_like(flat, float("inf"))))
-    if row is not None:
-        sync.snapshot[row, :1].copy_(flat)
+    with torch.no_grad():
+        flat = torch.as_strided(param, (1,), (1,))
+        flat.copy_(torch.nextafter(flat, torch.full_like(flat, float("inf"))))
+        if row is not None:
+            sync.snapshot[row, :1].copy_(flat)
 
 
 # -- reference-shaped entry points --------------------------------------------

@@ -1,0 +1,113 @@
+"""Multi-rank parity check of the NCCL path (launched by tests/test_gpu_multirank.py).
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P tests/mp_crossover_check.py OUT.json
+
+Each rank is one data-parallel worker (worker index = rank, ≙ equivalence.py:131):
+K1 packs its gradients, NCCL sums the bucket over NVLink, K2 divides by W and
+updates.  Rank 0 checks (a) per-iteration weights vs the reference golden /
+oracle within the fp32 tolerance, (b) at W = 2 bitwise equality with the
+single-GPU run that reduces W simulated workers left to right (two-operand
+IEEE addition is commutative), (c) the bit-exact schedule and trace legality.
+"""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle import sgd as osgd  # noqa: E402
+from paper_2103_07974_b200.apps import (LossKind, MlpConfig, SgdConfig, linear_app,  # noqa: E402
+                                        mlp_app)
+from paper_2103_07974_b200.comm import NcclCommunicator  # noqa: E402
+from paper_2103_07974_b200.engine import schedule_key, validate_trace  # noqa: E402
+from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy, rotation_schedule  # noqa: E402
+
+
+def main():
+    out_path = sys.argv[1]
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = NcclCommunicator(rank, world)
+    res = {"world": world, "ok": True, "checks": []}
+
+    # (1) MLP config 1 over real ranks
+    T = 8
+    specs = [(11, 0), (12, 1)]
+    s = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True)
+    for k, (ds, rs) in enumerate(specs):
+        s.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world), f"mlp{k}", rs, T, dev,
+                           local_workers=1, worker_count=world))
+    tr = s.run()
+    w_ranks = [s.weights(f"mlp{k}").cpu() for k in range(2)]
+    legal = validate_trace(tr) == [] and schedule_key(tr) == rotation_schedule(["mlp0", "mlp1"], [T, T])
+    res["checks"].append({"name": "mlp_trace_legal_and_schedule_exact", "ok": legal})
+
+    # (2) linear reference problem (W = world workers) -> compared with the oracle on rank 0
+    lcfg = [SgdConfig(0.05, world, LossKind.LEAST_SQUARES, 123), SgdConfig(0.05, world, LossKind.LOGISTIC, 124)]
+    s2 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True)
+    for k, c in enumerate(lcfg):
+        s2.register(linear_app(c, f"lin{k}", 40 + k, 20, dev, local_workers=1))
+    s2.run()
+    lin = [s2.weights(f"lin{k}")[:, :8].cpu().numpy().astype(np.float64) for k in range(2)]
+
+    # every rank must hold identical weights after every iteration
+    for k in range(2):
+        gathered = [torch.empty_like(w_ranks[k]) for _ in range(world)] if rank == 0 else None
+        dist.gather(w_ranks[k], gathered, dst=0)
+        if rank == 0:
+            same = all(torch.equal(gathered[0], x) for x in gathered)
+            res["checks"].append({"name": f"ranks_identical_mlp{k}", "ok": bool(same)})
+
+    if rank == 0:
+        ref = osgd.run_mlp_crossover(specs, T, workers=world)
+        from paper_2103_07974_b200.workload import BucketLayout
+
+        lay = BucketLayout.build([256 * 784, 256, 10 * 256, 10], 32)
+        worst = 0.0
+        for k in range(2):
+            w = w_ranks[k].numpy().astype(np.float64)
+            for t in range(T):
+                for i, o in enumerate(lay.offsets):
+                    r = ref[k][t][i].reshape(-1)
+                    worst = max(worst, float(np.max(np.abs(w[t, o:o + r.size] - r) / (1e-5 + 1e-3 * np.abs(r)))))
+        res["checks"].append({"name": "mlp_vs_oracle", "ok": worst <= 1.0, "worst_ratio": worst})
+
+        jobs = [osgd.LinearJob(0.05, world, c.loss.value, c.dataset_seed, 40 + k) for k, c in enumerate(lcfg)]
+        lref = osgd.run_crossover(jobs, 20)
+        lw = 0.0
+        for k in range(2):
+            r = np.stack(lref[k])
+            lw = max(lw, float(np.max(np.abs(lin[k] - r) / (1e-5 + 1e-4 * np.abs(r)))))
+        res["checks"].append({"name": "linear_vs_oracle", "ok": lw <= 1.0, "worst_ratio": lw})
+
+        if world == 2:
+            # single-GPU run with 2 simulated workers, reduced left to right by K2
+            s3 = CrossoverScheduler(Policy.CROSSOVER, record_weights=True)
+            for k, (ds, rs) in enumerate(specs):
+                s3.register(mlp_app(MlpConfig(dataset_seed=ds, workers=2), f"mlp{k}", rs, T, dev))
+            s3.run()
+            same = all(torch.equal(s3.weights(f"mlp{k}").cpu(), w_ranks[k]) for k in range(2))
+            res["checks"].append({"name": "nccl_w2_bitwise_eq_simulated_w2", "ok": bool(same)})
+        res["ok"] = all(c["ok"] for c in res["checks"])
+        Path(out_path).write_text(json.dumps(res, indent=1))
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0 and not res["ok"]:
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()
