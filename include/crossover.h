@@ -90,6 +90,15 @@ typedef struct cs_sgd_hyper {
 CS_API int cs_abi_version(void);
 CS_API const char* cs_last_error(void);
 
+/* Kernel implementation used by cs_pack / cs_unpack_sgd (process-wide).
+ * CS_VARIANT_TMA (default): persistent CTAs streaming through a shared-memory
+ * stage ring with cp.async.bulk loads/stores and mbarriers.
+ * CS_VARIANT_REGISTER: one CTA per 4096-element chunk, 128-bit register loads.
+ * Both produce bit-identical results. */
+enum { CS_VARIANT_TMA = 0, CS_VARIANT_REGISTER = 1 };
+CS_API int cs_set_kernel_variant(int variant);
+CS_API int cs_get_kernel_variant(void);
+
 /* K1: gather n tensors into the bucket (128-bit vector path when src and dst
  * are 16-byte aligned, scalar otherwise).  Bit-exact copy. */
 CS_API int cs_pack(const cs_pack_desc* descs, int n, void* stream);

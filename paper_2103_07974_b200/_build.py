@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libcrossover.so"
-SOURCES = ["crossover_kernels.cu", "crossover_abi.cu", "crossover_nccl.cu"]
+SOURCES = ["crossover_kernels.cu", "crossover_tma.cu", "crossover_abi.cu", "crossover_nccl.cu"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -42,7 +42,7 @@ def needs_rebuild() -> bool:
     if not LIB_PATH.exists():
         return True
     mtime = LIB_PATH.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.h")) + [REPO_DIR / "include" / "crossover.h"]
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [REPO_DIR / "include" / "crossover.h"]
     return any(d.stat().st_mtime > mtime for d in deps)
 
 

@@ -21,6 +21,8 @@ CS_NCCL_UNIQUE_ID_BYTES = 128
 CS_MAX_SOURCES = 8
 CS_ROUND_REFERENCE = 0
 CS_ROUND_TORCH = 1
+CS_VARIANT_TMA = 0
+CS_VARIANT_REGISTER = 1
 
 # numpy mirrors of the C descriptor structs (layouts asserted below)
 PACK_DESC = np.dtype([("src", "<u8"), ("dst", "<u8"), ("numel", "<i8")])
@@ -47,6 +49,8 @@ class CrossoverLibError(RuntimeError):
 EXPORTS = {
     "cs_abi_version": ([], ctypes.c_int),
     "cs_last_error": ([], ctypes.c_char_p),
+    "cs_set_kernel_variant": ([ctypes.c_int], ctypes.c_int),
+    "cs_get_kernel_variant": ([], ctypes.c_int),
     "cs_pack": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "cs_unpack_sgd": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                        ctypes.c_void_p, ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),
@@ -113,3 +117,12 @@ def gradient_stats_workspace_bytes(numel: int) -> int:
 
 def gradient_stats(data: int, numel: int, out: int, workspace: int, stream: int) -> None:
     check("cs_gradient_stats", lib.cs_gradient_stats(data, numel, out, workspace, stream))
+
+
+def set_kernel_variant(variant: int) -> None:
+    """Select the K1/K2 implementation (CS_VARIANT_TMA or CS_VARIANT_REGISTER)."""
+    check("cs_set_kernel_variant", lib.cs_set_kernel_variant(variant))
+
+
+def kernel_variant() -> int:
+    return int(lib.cs_get_kernel_variant())

@@ -33,24 +33,28 @@ int cuda_status(cudaError_t e, const char* where) {
   return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
 }
 
-static int64_t chunks_of(int64_t numel) { return (numel + kChunk - 1) / kChunk; }
+static int g_variant = CS_VARIANT_TMA;
+
+static int64_t chunks_of(int64_t numel, int chunk) { return (numel + chunk - 1) / chunk; }
 
 template <int CAP>
 static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
   static thread_local PackArgs<CAP> a;  // ~28 KB for the large capacity: keep off the stack
   a.n = n;
+  const bool tma = g_variant == CS_VARIANT_TMA;
+  const int chunk = tma ? tma_pack_chunk() : kChunk;
   int64_t c = 0;
   for (int i = 0; i < n; ++i) {
     a.chunk_begin[i] = (int)c;
     a.src[i] = d[i].src;
     a.dst[i] = d[i].dst;
     a.numel[i] = d[i].numel;
-    c += chunks_of(d[i].numel);
+    c += chunks_of(d[i].numel, chunk);
   }
   a.chunk_begin[n] = (int)c;
   if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_pack: %lld chunks exceed grid limit", (long long)c);
   a.total_chunks = (int)c;
-  return cuda_status(launch_pack<CAP>(a, s), "cs_pack launch");
+  return cuda_status(tma ? launch_pack_tma<CAP>(a, s) : launch_pack<CAP>(a, s), "cs_pack launch");
 }
 
 template <int CAP>
@@ -63,6 +67,9 @@ static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources,
   a.snapshot = snapshot;
   for (int k = 0; k < CS_MAX_SOURCES; ++k) a.base[k] = k < nsrc ? sources[k] : 0;
   a.h = *h;
+  const bool mom = h->momentum != 0.0f;
+  const bool tma = g_variant == CS_VARIANT_TMA;
+  const int chunk = tma ? tma_update_chunk(nsrc, mom) : kChunk;
   int64_t c = 0;
   for (int i = 0; i < n; ++i) {
     a.chunk_begin[i] = (int)c;
@@ -71,13 +78,13 @@ static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources,
     a.grad_off[i] = d[i].grad_offset;
     a.snap_off[i] = d[i].snap_offset;
     a.numel[i] = d[i].numel;
-    c += chunks_of(d[i].numel);
+    c += chunks_of(d[i].numel, chunk);
   }
   a.chunk_begin[n] = (int)c;
   if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_unpack_sgd: %lld chunks exceed grid limit", (long long)c);
   a.total_chunks = (int)c;
-  const bool mom = h->momentum != 0.0f;
-  return cuda_status(launch_unpack_sgd<CAP>(a, mom, s), "cs_unpack_sgd launch");
+  return cuda_status(tma ? launch_unpack_sgd_tma<CAP>(a, mom, s) : launch_unpack_sgd<CAP>(a, mom, s),
+                     "cs_unpack_sgd launch");
 }
 
 }  // namespace cs
@@ -89,6 +96,15 @@ extern "C" {
 int cs_abi_version(void) { return CS_ABI_VERSION; }
 
 const char* cs_last_error(void) { return g_last_error.c_str(); }
+
+int cs_set_kernel_variant(int variant) {
+  if (variant != CS_VARIANT_TMA && variant != CS_VARIANT_REGISTER)
+    return set_error(CS_ERR_ARG, "cs_set_kernel_variant: unknown variant %d", variant);
+  g_variant = variant;
+  return 0;
+}
+
+int cs_get_kernel_variant(void) { return g_variant; }
 
 int cs_pack(const cs_pack_desc* descs, int n, void* stream) {
   if (n < 0 || (n > 0 && descs == nullptr))

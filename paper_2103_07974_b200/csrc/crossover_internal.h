@@ -12,6 +12,14 @@ constexpr int kUnroll = 4;                         // 128-bit loads in flight pe
 constexpr int kChunk = kThreads * 4 * kUnroll;     // 4096 fp32 = 16 KB per CTA
 constexpr int kStatsMaxGrid = 148 * 8;             // fixed -> deterministic partial order
 
+// TMA (cp.async.bulk) variants: one persistent CTA per SM, stage ring in shared memory
+constexpr int kTmaBarrierBytes = 128;              // mbarriers in front of the stage ring
+constexpr int kTmaSmemBudget = 200 * 1024;         // dynamic shared memory per CTA
+constexpr int kTmaMaxStages = 8;
+constexpr int kTmaMinStages = 3;
+constexpr int kTmaPackChunk = 8192;                // fp32 per stage for K1 (32 KB)
+constexpr int kTmaMaxChunk = 4096;                 // fp32 per stream per stage for K2
+
 // descriptor capacities per launch (kernel parameters are <= 32 KB on sm_70+)
 constexpr int kCapSmall = 16;
 constexpr int kCapMid = 128;
@@ -51,6 +59,12 @@ template <int CAP>
 cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s);
 template <int CAP>
 cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
+template <int CAP>
+cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s);
+template <int CAP>
+cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
+int tma_pack_chunk();
+int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
                          cudaStream_t s);
 int stats_grid(int64_t numel);

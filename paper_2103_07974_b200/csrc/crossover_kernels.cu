@@ -20,6 +20,7 @@
 
 #include "crossover.h"
 #include "crossover_internal.h"
+#include "crossover_sgd.cuh"
 
 namespace cs {
 
@@ -97,33 +98,6 @@ pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
 // ---------------------------------------------------------------------------
 // K2: fixed-order reduce over sources, average, SGD update
 // ---------------------------------------------------------------------------
-struct Rule {
-  float lr, mu, one_minus_damp, wd;
-  int nesterov, first, rounding;
-  float divisor;
-  int has_mom;
-};
-
-// One element of the update.  Returns the new parameter and updates *buf.
-__device__ __forceinline__ float sgd_elem(const Rule& r, float acc, float p, float* buf) {
-  // equivalence.py:160  acc / len(grads)  (IEEE division; == *1/W for W = 2^k)
-  float d = __fdiv_rn(acc, r.divisor);
-  if (r.rounding == CS_ROUND_REFERENCE) {
-    // equivalence.py:167  parameters - learning_rate * averaged  (two roundings)
-    return __fsub_rn(p, __fmul_rn(r.lr, d));
-  }
-  // torch.optim.SGD (_single_tensor_sgd): grad.add(param, alpha=wd);
-  // buf.mul_(mu).add_(grad, alpha=1-damp); grad = grad.add(buf, alpha=mu) | buf;
-  // param.add_(grad, alpha=-lr).  add(x, alpha=a) is one FMA in ATen (vec::fmadd).
-  if (r.wd != 0.0f) d = __fmaf_rn(r.wd, p, d);
-  if (r.has_mom) {
-    float b = r.first ? d : __fmaf_rn(r.one_minus_damp, d, __fmul_rn(r.mu, *buf));
-    *buf = b;
-    d = r.nesterov ? __fmaf_rn(r.mu, b, d) : b;
-  }
-  return __fmaf_rn(-r.lr, d, p);
-}
-
 template <int CAP, bool kMom>
 __global__ void __launch_bounds__(kThreads)
 unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
@@ -134,11 +108,7 @@ unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
   const int n = rem < kChunk ? (int)rem : kChunk;
   const int tid = threadIdx.x;
 
-  Rule r;
-  r.lr = a.h.lr; r.mu = a.h.momentum; r.one_minus_damp = a.h.dampening_complement;
-  r.wd = a.h.weight_decay;
-  r.nesterov = a.h.nesterov; r.first = a.h.first_step; r.rounding = a.h.rounding;
-  r.divisor = (float)a.h.divisor; r.has_mom = kMom;
+  const Rule r = make_rule(a.h, kMom);
 
   float* __restrict__ p = a.param[i] + e0;
   float* __restrict__ m = kMom ? a.mom[i] + e0 : nullptr;

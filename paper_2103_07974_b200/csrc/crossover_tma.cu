@@ -1,0 +1,361 @@
+// crossover_tma.cu -- TMA-pipelined (cp.async.bulk + mbarrier) versions of K1 and K2.
+//
+// Persistent CTAs (one per SM, grid = #SMs) walk the chunk list with stride
+// gridDim.x.  Thread 0 is the TMA producer: it keeps up to STAGES chunks of
+// every input stream in flight with 1-D bulk copies global -> shared that
+// complete on a per-stage mbarrier (expect_tx).  All 256 threads compute out
+// of shared memory (LDS.128, conflict-free), write the results back into the
+// same stage buffers, fence the generic->async proxy, and thread 0 streams
+// them out with bulk stores shared -> global (bulk_group).  A stage is
+// refilled one iteration after its store was issued (wait_group.read 1), so
+// STAGES-2 loads are always in flight per SM without any register staging.
+//
+// Chunks whose addresses are not 16-byte aligned (exact reference layout with
+// odd offsets, views at odd offsets) skip the bulk path: the producer arrives
+// on the stage barrier without transactions and the consumers process the
+// chunk straight from global memory.  Tails (numel % 4) are always handled
+// by direct global accesses.  Arithmetic is identical to crossover_kernels.cu
+// (same sgd_elem), so results are bit-identical to the register variant.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "crossover.h"
+#include "crossover_internal.h"
+#include "crossover_sgd.cuh"
+
+namespace cs {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int CAP>
+__device__ __forceinline__ int find_seg(const int* cb, int n, int c) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (cb[mid] <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+struct Chunk {
+  int seg;
+  int64_t e0;
+  int n;
+};
+
+template <int CAP, typename Args>
+__device__ __forceinline__ Chunk chunk_at(const Args& a, int c, int chunk) {
+  Chunk k;
+  k.seg = find_seg<CAP>(a.chunk_begin, a.n, c);
+  k.e0 = (int64_t)(c - a.chunk_begin[k.seg]) * chunk;
+  const int64_t rem = a.numel[k.seg] - k.e0;
+  k.n = rem < chunk ? (int)rem : chunk;
+  return k;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// K1 (TMA): bucket <- gradients, staged through shared memory
+// ---------------------------------------------------------------------------
+template <int CAP>
+__global__ void __launch_bounds__(kThreads, 1)
+pack_tma_kernel(const __grid_constant__ PackArgs<CAP> a, int chunk, int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)smem;
+  float* slots = (float*)(smem + kTmaBarrierBytes);
+  const int tid = threadIdx.x;
+  const int G = gridDim.x;
+  const int my_n = (a.total_chunks - (int)blockIdx.x + G - 1) / G;
+
+  auto vec_ok = [&](const Chunk& k) {
+    return ((((uintptr_t)(a.src[k.seg] + k.e0)) | ((uintptr_t)(a.dst[k.seg] + k.e0))) & 15u) == 0;
+  };
+  auto issue = [&](int i) {
+    const int slot = i % stages;
+    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+    const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
+    if (vec_ok(k) && bytes) {
+      mbar_arrive_expect_tx(&full[slot], bytes);
+      bulk_load(slots + (size_t)slot * chunk, a.src[k.seg] + k.e0, bytes, &full[slot]);
+    } else {
+      mbar_arrive(&full[slot]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < stages && i < my_n; ++i) issue(i);
+
+  for (int i = 0; i < my_n; ++i) {
+    const int slot = i % stages;
+    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+    const float* src = a.src[k.seg] + k.e0;
+    float* dst = a.dst[k.seg] + k.e0;
+    const bool vec = vec_ok(k);
+    const int n4 = vec ? (k.n & ~3) : 0;
+    mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
+    for (int e = n4 + tid; e < k.n; e += kThreads) dst[e] = src[e];   // tail / misaligned
+    __syncthreads();
+    if (tid == 0) {
+      if (n4) bulk_store(dst, slots + (size_t)slot * chunk, (uint32_t)n4 * 4u);
+      bulk_commit();
+      if (i >= 1 && i - 1 + stages < my_n) {
+        bulk_wait_read_1();  // stage of iteration i-1 has been read out by its store
+        issue(i - 1 + stages);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// K2 (TMA): sources + param (+ momentum) -> param (+ momentum, snapshot)
+// stage layout: [g_0 | g_1 | ... | g_{S-1} | p | m], each `chunk` floats
+// ---------------------------------------------------------------------------
+template <int CAP, bool kMom>
+__global__ void __launch_bounds__(kThreads, 1)
+unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)smem;
+  float* slots = (float*)(smem + kTmaBarrierBytes);
+  const int tid = threadIdx.x;
+  const int G = gridDim.x;
+  const int my_n = (a.total_chunks - (int)blockIdx.x + G - 1) / G;
+  const int nsrc = a.nsrc;
+  const int nin = nsrc + 1 + (kMom ? 1 : 0);
+  const size_t stage_floats = (size_t)nin * chunk;
+
+  Rule r = make_rule(a.h, kMom);
+
+  auto gsrc = [&](int s, const Chunk& k) {
+    return (const float*)(a.base[s] + a.grad_off[k.seg] + (uint64_t)k.e0 * 4u);
+  };
+  auto snap_ptr = [&](const Chunk& k) {
+    return a.snapshot ? (float*)((char*)a.snapshot + a.snap_off[k.seg]) + k.e0 : nullptr;
+  };
+  auto vec_ok = [&](const Chunk& k) {
+    uintptr_t al = (uintptr_t)(a.param[k.seg] + k.e0);
+    if (kMom) al |= (uintptr_t)(a.mom[k.seg] + k.e0);
+    if (a.snapshot) al |= (uintptr_t)snap_ptr(k);
+    for (int s = 0; s < nsrc; ++s) al |= (uintptr_t)gsrc(s, k);
+    return (al & 15u) == 0;
+  };
+  auto issue = [&](int i) {
+    const int slot = i % stages;
+    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+    const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
+    if (vec_ok(k) && bytes) {
+      float* st = slots + (size_t)slot * stage_floats;
+      mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nin);
+      for (int s = 0; s < nsrc; ++s) bulk_load(st + (size_t)s * chunk, gsrc(s, k), bytes, &full[slot]);
+      bulk_load(st + (size_t)nsrc * chunk, a.param[k.seg] + k.e0, bytes, &full[slot]);
+      if (kMom) bulk_load(st + (size_t)(nsrc + 1) * chunk, a.mom[k.seg] + k.e0, bytes, &full[slot]);
+    } else {
+      mbar_arrive(&full[slot]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < stages && i < my_n; ++i) issue(i);
+
+  for (int i = 0; i < my_n; ++i) {
+    const int slot = i % stages;
+    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+    float* p = a.param[k.seg] + k.e0;
+    float* m = kMom ? a.mom[k.seg] + k.e0 : nullptr;
+    float* snap = snap_ptr(k);
+    const bool vec = vec_ok(k);
+    const int n4 = vec ? (k.n & ~3) : 0;
+    float* st = slots + (size_t)slot * stage_floats;
+    float* sp = st + (size_t)nsrc * chunk;
+    float* sm = sp + chunk;
+    mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
+    for (int e4 = tid * 4; e4 < n4; e4 += kThreads * 4) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < nsrc; ++s) {
+        const float4 g = *(const float4*)(st + (size_t)s * chunk + e4);
+        acc.x = __fadd_rn(acc.x, g.x); acc.y = __fadd_rn(acc.y, g.y);
+        acc.z = __fadd_rn(acc.z, g.z); acc.w = __fadd_rn(acc.w, g.w);
+      }
+      float4 pv = *(const float4*)(sp + e4);
+      float4 mv = kMom ? *(const float4*)(sm + e4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      pv.x = sgd_elem(r, acc.x, pv.x, &mv.x);
+      pv.y = sgd_elem(r, acc.y, pv.y, &mv.y);
+      pv.z = sgd_elem(r, acc.z, pv.z, &mv.z);
+      pv.w = sgd_elem(r, acc.w, pv.w, &mv.w);
+      *(float4*)(sp + e4) = pv;
+      if (kMom) *(float4*)(sm + e4) = mv;
+    }
+    for (int e = n4 + tid; e < k.n; e += kThreads) {   // tail / misaligned: global memory
+      float acc = 0.0f;
+      for (int s = 0; s < nsrc; ++s) acc = __fadd_rn(acc, gsrc(s, k)[e]);
+      float b = kMom ? m[e] : 0.0f;
+      const float np = sgd_elem(r, acc, p[e], &b);
+      p[e] = np;
+      if (kMom) m[e] = b;
+      if (snap) snap[e] = np;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      if (n4) {
+        const uint32_t bytes = (uint32_t)n4 * 4u;
+        bulk_store(p, sp, bytes);
+        if (kMom) bulk_store(m, sm, bytes);
+        if (snap) bulk_store(snap, sp, bytes);
+      }
+      bulk_commit();
+      if (i >= 1 && i - 1 + stages < my_n) {
+        bulk_wait_read_1();
+        issue(i - 1 + stages);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+template <typename K>
+static cudaError_t opt_in_smem(K kernel, int bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int tma_pack_chunk() { return kTmaPackChunk; }
+
+int tma_update_chunk(int nsrc, bool mom) {
+  const int nin = nsrc + 1 + (mom ? 1 : 0);
+  int chunk = kTmaMaxChunk;
+  while (chunk > 1024 && (size_t)nin * chunk * 4 * kTmaMinStages > (size_t)kTmaSmemBudget) chunk >>= 1;
+  return chunk;
+}
+
+static int stages_for(size_t stage_bytes) {
+  int st = (int)((kTmaSmemBudget - kTmaBarrierBytes) / stage_bytes);
+  if (st > kTmaMaxStages) st = kTmaMaxStages;
+  return st;
+}
+
+template <int CAP>
+cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s) {
+  if (a.total_chunks == 0) return cudaSuccess;
+  const int chunk = kTmaPackChunk;
+  const int stages = stages_for((size_t)chunk * 4);
+  const int smem = kTmaBarrierBytes + stages * chunk * 4;
+  cudaError_t e = opt_in_smem(pack_tma_kernel<CAP>, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = a.total_chunks < sm_count() ? a.total_chunks : sm_count();
+  pack_tma_kernel<CAP><<<grid, kThreads, smem, s>>>(a, chunk, stages);
+  return cudaGetLastError();
+}
+
+template <int CAP>
+cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s) {
+  if (a.total_chunks == 0) return cudaSuccess;
+  const int chunk = tma_update_chunk(a.nsrc, mom);
+  const int nin = a.nsrc + 1 + (mom ? 1 : 0);
+  const int stages = stages_for((size_t)nin * chunk * 4);
+  if (stages < 2) return cudaErrorInvalidConfiguration;
+  const int smem = kTmaBarrierBytes + stages * nin * chunk * 4;
+  const int grid = a.total_chunks < sm_count() ? a.total_chunks : sm_count();
+  cudaError_t e;
+  if (mom) {
+    e = opt_in_smem(unpack_sgd_tma_kernel<CAP, true>, smem);
+    if (e != cudaSuccess) return e;
+    unpack_sgd_tma_kernel<CAP, true><<<grid, kThreads, smem, s>>>(a, chunk, stages);
+  } else {
+    e = opt_in_smem(unpack_sgd_tma_kernel<CAP, false>, smem);
+    if (e != cudaSuccess) return e;
+    unpack_sgd_tma_kernel<CAP, false><<<grid, kThreads, smem, s>>>(a, chunk, stages);
+  }
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_pack_tma<kCapSmall>(const PackArgs<kCapSmall>&, cudaStream_t);
+template cudaError_t launch_pack_tma<kCapMid>(const PackArgs<kCapMid>&, cudaStream_t);
+template cudaError_t launch_pack_tma<kCapLarge>(const PackArgs<kCapLarge>&, cudaStream_t);
+template cudaError_t launch_unpack_sgd_tma<kCapSmall>(const UpdateArgs<kCapSmall>&, bool, cudaStream_t);
+template cudaError_t launch_unpack_sgd_tma<kCapMid>(const UpdateArgs<kCapMid>&, bool, cudaStream_t);
+template cudaError_t launch_unpack_sgd_tma<kCapLarge>(const UpdateArgs<kCapLarge>&, bool, cudaStream_t);
+
+}  // namespace cs

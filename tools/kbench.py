@@ -1,0 +1,87 @@
+"""Microbenchmark of K1/K2 variants at ResNet-50 / VGG-16 bucket sizes (device-timed).
+
+    python tools/kbench.py [--model resnet50] [--iters 20]
+
+Each timed launch is preceded by an L2 flush (write of a 512 MB buffer), so
+every byte comes from HBM.  Reports algorithmic GB/s (SURVEY §8d bytes) and
+the fraction of the measured HBM peak.
+"""
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    import torchvision
+
+    from paper_2103_07974_b200 import _lib
+    from paper_2103_07974_b200.fusion import FusedGradientSync, SgdSettings
+
+    dev = torch.device("cuda", 0)
+    m = getattr(torchvision.models, args.model)()
+    shapes = [p.shape for p in m.parameters()]
+    params = [torch.randn(s, device=dev) for s in shapes]
+    grads = [torch.randn(s, device=dev) for s in shapes]
+    S = sum(p.numel() for p in params) * 4
+    flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=dev)
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    stream = torch.cuda.current_stream()
+
+    def timeit(fn, iters):
+        ts = []
+        for _ in range(3):
+            flush.fill_(1); fn()
+        for _ in range(iters):
+            flush.fill_(1)
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(); fn(); b.record(); b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts), min(ts)
+
+    res = {"model": args.model, "S_bytes": S, "peak_gbs": peak, "rows": []}
+    src = torch.empty(S // 4, device=dev); dst = torch.empty_like(src)
+    med, best = timeit(lambda: dst.copy_(src), args.iters)
+    res["rows"].append({"name": "torch_copy(S)", "bytes": 2 * S, "us": med * 1e3, "GB/s": 2 * S / med / 1e6})
+    cases = [
+        ("k1_pack", dict(sgd=SgdSettings(0.1), mode="bucket", lw=1), "pack", 2 * S),
+        ("k2_direct_momentum", dict(sgd=SgdSettings(0.1, momentum=0.9, weight_decay=1e-4), mode="direct", lw=1), "update", 5 * S),
+        ("k2_bucket_momentum", dict(sgd=SgdSettings(0.1, momentum=0.9, weight_decay=1e-4), mode="bucket", lw=1), "update", 5 * S),
+        ("k2_bucket_plain_ref", dict(sgd=SgdSettings(0.1), mode="bucket", lw=1), "update", 3 * S),
+        ("k2_bucket_2src_momentum", dict(sgd=SgdSettings(0.1, momentum=0.9), mode="bucket", lw=2), "update", 6 * S),
+    ]
+    for variant_name, variant in (("tma", _lib.CS_VARIANT_TMA), ("register", _lib.CS_VARIANT_REGISTER)):
+        _lib.set_kernel_variant(variant)
+        for name, kw, what, nbytes in cases:
+            s = FusedGradientSync(params, kw["sgd"], local_workers=kw["lw"], mode=kw["mode"])
+            gl = [grads] * kw["lw"]
+            if what == "pack":
+                fn = lambda: s.pack(gl, stream.cuda_stream)
+            elif kw["mode"] == "direct":
+                fn = lambda: s.update(stream.cuda_stream, grads)
+            else:
+                s.pack(gl, stream.cuda_stream)
+                fn = lambda: s.update(stream.cuda_stream)
+            med, best = timeit(fn, args.iters)
+            res["rows"].append({"name": f"{name}[{variant_name}]", "bytes": nbytes, "us": round(med * 1e3, 2),
+                                "best_us": round(best * 1e3, 2), "GB/s": round(nbytes / med / 1e6, 1),
+                                "frac_of_peak": round(nbytes / med / 1e6 / peak, 4)})
+    for r in res["rows"]:
+        print(f"{r['name']:40s} {r['us']:9.2f} us  {r['GB/s']:8.1f} GB/s  {r.get('frac_of_peak', '')}")
+    if args.out:
+        Path(args.out).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
