@@ -13,12 +13,13 @@ constexpr int kChunk = kThreads * 4 * kUnroll;     // 4096 fp32 = 16 KB per CTA
 constexpr int kStatsMaxGrid = 148 * 8;             // fixed -> deterministic partial order
 
 // TMA (cp.async.bulk) variants: one persistent CTA per SM, stage ring in shared memory
-constexpr int kTmaBarrierBytes = 128;              // mbarriers in front of the stage ring
+constexpr int kTmaBarrierBytes = 256;              // mbarriers in front of the stage ring
+constexpr int kTmaWsThreads = 64 + 256;            // producer warp + store warp + 8 consumer warps
 constexpr int kTmaSmemBudget = 200 * 1024;         // dynamic shared memory per CTA
 constexpr int kTmaMaxStages = 8;
-constexpr int kTmaMinStages = 3;
+constexpr int kTmaMinStages = 6;
 constexpr int kTmaPackChunk = 8192;                // fp32 per stage for K1 (32 KB)
-constexpr int kTmaMaxChunk = 4096;                 // fp32 per stream per stage for K2
+constexpr int kTmaMaxChunk = 2048;                 // fp32 per stream per stage for K2
 
 // descriptor capacities per launch (kernel parameters are <= 32 KB on sm_70+)
 constexpr int kCapSmall = 16;

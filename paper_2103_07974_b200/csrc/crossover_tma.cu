@@ -170,23 +170,35 @@ pack_tma_kernel(const __grid_constant__ PackArgs<CAP> a, int chunk, int stages) 
 }
 
 // ---------------------------------------------------------------------------
-// K2 (TMA): sources + param (+ momentum) -> param (+ momentum, snapshot)
+// K2 (TMA, warp-specialised): sources + param (+ momentum) -> param (+ momentum, snapshot)
+//   warp 0  producer : waits empty[s], issues the stage's bulk loads on full[s]
+//   warp 1  storer   : waits computed[s], issues bulk stores, frees stage s once its
+//                      store has been read out of shared memory (kStoreLag groups behind)
+//   warps 2+ consumers: wait full[s], update in shared memory, arrive computed[s]
 // stage layout: [g_0 | g_1 | ... | g_{S-1} | p | m], each `chunk` floats
 // ---------------------------------------------------------------------------
+constexpr int kStoreLag = 2;
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 template <int CAP, bool kMom>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kTmaWsThreads, 1)
 unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
+  uint64_t* computed = full + kTmaMaxStages;
+  uint64_t* empty = computed + kTmaMaxStages;
   float* slots = (float*)(smem + kTmaBarrierBytes);
-  const int tid = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int my_n = (a.total_chunks - (int)blockIdx.x + G - 1) / G;
   const int nsrc = a.nsrc;
   const int nin = nsrc + 1 + (kMom ? 1 : 0);
   const size_t stage_floats = (size_t)nin * chunk;
-
-  Rule r = make_rule(a.h, kMom);
+  constexpr int kConsumers = kTmaWsThreads - 64;
 
   auto gsrc = [&](int s, const Chunk& k) {
     return (const float*)(a.base[s] + a.grad_off[k.seg] + (uint64_t)k.e0 * 4u);
@@ -199,44 +211,79 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
     if (kMom) al |= (uintptr_t)(a.mom[k.seg] + k.e0);
     if (a.snapshot) al |= (uintptr_t)snap_ptr(k);
     for (int s = 0; s < nsrc; ++s) al |= (uintptr_t)gsrc(s, k);
-    return (al & 15u) == 0;
-  };
-  auto issue = [&](int i) {
-    const int slot = i % stages;
-    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
-    const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
-    if (vec_ok(k) && bytes) {
-      float* st = slots + (size_t)slot * stage_floats;
-      mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nin);
-      for (int s = 0; s < nsrc; ++s) bulk_load(st + (size_t)s * chunk, gsrc(s, k), bytes, &full[slot]);
-      bulk_load(st + (size_t)nsrc * chunk, a.param[k.seg] + k.e0, bytes, &full[slot]);
-      if (kMom) bulk_load(st + (size_t)(nsrc + 1) * chunk, a.mom[k.seg] + k.e0, bytes, &full[slot]);
-    } else {
-      mbar_arrive(&full[slot]);
-    }
+    return (al & 15u) == 0 && k.n >= 4;
   };
 
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&computed[s], kConsumers / 32);
+      mbar_init(&empty[s], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int i = 0; i < stages && i < my_n; ++i) issue(i);
 
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < my_n; ++i) {
+        const int slot = i % stages;
+        if (i >= stages) mbar_wait(&empty[slot], (uint32_t)((i / stages) + 1) & 1u);
+        const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+        if (vec_ok(k)) {
+          const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
+          float* st = slots + (size_t)slot * stage_floats;
+          mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nin);
+          for (int s = 0; s < nsrc; ++s) bulk_load(st + (size_t)s * chunk, gsrc(s, k), bytes, &full[slot]);
+          bulk_load(st + (size_t)nsrc * chunk, a.param[k.seg] + k.e0, bytes, &full[slot]);
+          if (kMom) bulk_load(st + (size_t)(nsrc + 1) * chunk, a.mom[k.seg] + k.e0, bytes, &full[slot]);
+        } else {
+          mbar_arrive(&full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int i = 0; i < my_n; ++i) {
+        const int slot = i % stages;
+        mbar_wait(&computed[slot], (uint32_t)(i / stages) & 1u);
+        const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+        if (vec_ok(k)) {
+          const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
+          float* sp = slots + (size_t)slot * stage_floats + (size_t)nsrc * chunk;
+          bulk_store(a.param[k.seg] + k.e0, sp, bytes);
+          if (kMom) bulk_store(a.mom[k.seg] + k.e0, sp + chunk, bytes);
+          float* snap = snap_ptr(k);
+          if (snap) bulk_store(snap, sp, bytes);
+        }
+        bulk_commit();
+        bulk_wait_read<kStoreLag>();
+        const int j = i - kStoreLag;                    // its store has left shared memory
+        if (j >= 0 && j + stages < my_n) mbar_arrive(&empty[j % stages]);
+      }
+      bulk_wait_read<0>();
+      for (int j = my_n - kStoreLag; j < my_n; ++j)
+        if (j >= 0 && j + stages < my_n) mbar_arrive(&empty[j % stages]);
+      bulk_wait_all();
+    }
+    return;
+  }
+
+  // consumers
+  const Rule r = make_rule(a.h, kMom);
+  const int ctid = threadIdx.x - 64;
   for (int i = 0; i < my_n; ++i) {
     const int slot = i % stages;
     const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
-    float* p = a.param[k.seg] + k.e0;
-    float* m = kMom ? a.mom[k.seg] + k.e0 : nullptr;
-    float* snap = snap_ptr(k);
     const bool vec = vec_ok(k);
     const int n4 = vec ? (k.n & ~3) : 0;
     float* st = slots + (size_t)slot * stage_floats;
     float* sp = st + (size_t)nsrc * chunk;
     float* sm = sp + chunk;
     mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
-    for (int e4 = tid * 4; e4 < n4; e4 += kThreads * 4) {
+    for (int e4 = ctid * 4; e4 < n4; e4 += kConsumers * 4) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s = 0; s < nsrc; ++s) {
         const float4 g = *(const float4*)(st + (size_t)s * chunk + e4);
@@ -252,32 +299,24 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
       *(float4*)(sp + e4) = pv;
       if (kMom) *(float4*)(sm + e4) = mv;
     }
-    for (int e = n4 + tid; e < k.n; e += kThreads) {   // tail / misaligned: global memory
-      float acc = 0.0f;
-      for (int s = 0; s < nsrc; ++s) acc = __fadd_rn(acc, gsrc(s, k)[e]);
-      float b = kMom ? m[e] : 0.0f;
-      const float np = sgd_elem(r, acc, p[e], &b);
-      p[e] = np;
-      if (kMom) m[e] = b;
-      if (snap) snap[e] = np;
+    if (n4 < k.n) {                                     // tail / misaligned: global memory
+      float* p = a.param[k.seg] + k.e0;
+      float* m = kMom ? a.mom[k.seg] + k.e0 : nullptr;
+      float* snap = snap_ptr(k);
+      for (int e = n4 + ctid; e < k.n; e += kConsumers) {
+        float acc = 0.0f;
+        for (int s = 0; s < nsrc; ++s) acc = __fadd_rn(acc, gsrc(s, k)[e]);
+        float b = kMom ? m[e] : 0.0f;
+        const float np = sgd_elem(r, acc, p[e], &b);
+        p[e] = np;
+        if (kMom) m[e] = b;
+        if (snap) snap[e] = np;
+      }
     }
     fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      if (n4) {
-        const uint32_t bytes = (uint32_t)n4 * 4u;
-        bulk_store(p, sp, bytes);
-        if (kMom) bulk_store(m, sm, bytes);
-        if (snap) bulk_store(snap, sp, bytes);
-      }
-      bulk_commit();
-      if (i >= 1 && i - 1 + stages < my_n) {
-        bulk_wait_read_1();
-        issue(i - 1 + stages);
-      }
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&computed[slot]);
   }
-  if (tid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -306,7 +345,8 @@ int tma_pack_chunk() { return kTmaPackChunk; }
 int tma_update_chunk(int nsrc, bool mom) {
   const int nin = nsrc + 1 + (mom ? 1 : 0);
   int chunk = kTmaMaxChunk;
-  while (chunk > 1024 && (size_t)nin * chunk * 4 * kTmaMinStages > (size_t)kTmaSmemBudget) chunk >>= 1;
+  while (chunk > 512 && (size_t)nin * chunk * 4 * kTmaMinStages > (size_t)(kTmaSmemBudget - kTmaBarrierBytes))
+    chunk >>= 1;
   return chunk;
 }
 
@@ -335,18 +375,18 @@ cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream
   const int chunk = tma_update_chunk(a.nsrc, mom);
   const int nin = a.nsrc + 1 + (mom ? 1 : 0);
   const int stages = stages_for((size_t)nin * chunk * 4);
-  if (stages < 2) return cudaErrorInvalidConfiguration;
+  if (stages <= kStoreLag) return cudaErrorInvalidConfiguration;
   const int smem = kTmaBarrierBytes + stages * nin * chunk * 4;
   const int grid = a.total_chunks < sm_count() ? a.total_chunks : sm_count();
   cudaError_t e;
   if (mom) {
     e = opt_in_smem(unpack_sgd_tma_kernel<CAP, true>, smem);
     if (e != cudaSuccess) return e;
-    unpack_sgd_tma_kernel<CAP, true><<<grid, kThreads, smem, s>>>(a, chunk, stages);
+    unpack_sgd_tma_kernel<CAP, true><<<grid, kTmaWsThreads, smem, s>>>(a, chunk, stages);
   } else {
     e = opt_in_smem(unpack_sgd_tma_kernel<CAP, false>, smem);
     if (e != cudaSuccess) return e;
-    unpack_sgd_tma_kernel<CAP, false><<<grid, kThreads, smem, s>>>(a, chunk, stages);
+    unpack_sgd_tma_kernel<CAP, false><<<grid, kTmaWsThreads, smem, s>>>(a, chunk, stages);
   }
   return cudaGetLastError();
 }

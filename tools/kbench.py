@@ -36,15 +36,23 @@ def main():
     grads = [torch.randn(s, device=dev) for s in shapes]
     S = sum(p.numel() for p in params) * 4
     flush = torch.empty(512 * 2**20, dtype=torch.uint8, device=dev)
+    clean = torch.ones(128 * 2**20, dtype=torch.float32, device=dev)
+
+    def do_flush():
+        # write 512 MB, then read 512 MB: L2 ends up holding clean lines only, so the
+        # timed kernel pays neither cache hits nor somebody else's dirty write-backs
+        flush.fill_(1)
+        clean.sum()
+
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     stream = torch.cuda.current_stream()
 
     def timeit(fn, iters):
         ts = []
         for _ in range(3):
-            flush.fill_(1); fn()
+            do_flush(); fn()
         for _ in range(iters):
-            flush.fill_(1)
+            do_flush()
             a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
             a.record(); fn(); b.record(); b.synchronize()
             ts.append(a.elapsed_time(b))
