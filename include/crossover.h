@@ -98,6 +98,10 @@ CS_API const char* cs_last_error(void);
 enum { CS_VARIANT_TMA = 0, CS_VARIANT_REGISTER = 1 };
 CS_API int cs_set_kernel_variant(int variant);
 CS_API int cs_get_kernel_variant(void);
+/* Launch-shape knobs of the TMA variant (0 restores the built-in heuristic):
+ * "k1_chunk", "k2_chunk" (fp32 elements per stream per stage), "k2_stages",
+ * "ctas_per_sm".  Results never depend on them. */
+CS_API int cs_tune(const char* key, int value);
 
 /* K1: gather n tensors into the bucket (128-bit vector path when src and dst
  * are 16-byte aligned, scalar otherwise).  Bit-exact copy. */

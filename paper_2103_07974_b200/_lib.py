@@ -51,6 +51,7 @@ EXPORTS = {
     "cs_last_error": ([], ctypes.c_char_p),
     "cs_set_kernel_variant": ([ctypes.c_int], ctypes.c_int),
     "cs_get_kernel_variant": ([], ctypes.c_int),
+    "cs_tune": ([ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
     "cs_pack": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "cs_unpack_sgd": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                        ctypes.c_void_p, ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),
@@ -126,3 +127,8 @@ def set_kernel_variant(variant: int) -> None:
 
 def kernel_variant() -> int:
     return int(lib.cs_get_kernel_variant())
+
+
+def tune(key: str, value: int) -> None:
+    """Launch-shape knob of the TMA kernels (see include/crossover.h cs_tune)."""
+    check("cs_tune", lib.cs_tune(key.encode(), value))

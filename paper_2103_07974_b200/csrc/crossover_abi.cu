@@ -106,6 +106,17 @@ int cs_set_kernel_variant(int variant) {
 
 int cs_get_kernel_variant(void) { return g_variant; }
 
+int cs_tune(const char* key, int value) {
+  if (key == nullptr || value < 0) return set_error(CS_ERR_ARG, "cs_tune: invalid arguments");
+  const std::string k(key);
+  if (k == "k1_chunk" && (value == 0 || (value % 1024 == 0 && value <= 16384))) g_tune_k1_chunk = value;
+  else if (k == "k2_chunk" && (value == 0 || (value % 256 == 0 && value <= 8192))) g_tune_k2_chunk = value;
+  else if (k == "k2_stages" && value <= kTmaMaxStages) g_tune_k2_stages = value;
+  else if (k == "ctas_per_sm" && value <= 4) g_tune_ctas_per_sm = value;
+  else return set_error(CS_ERR_ARG, "cs_tune: unknown key or bad value (%s=%d)", key, value);
+  return 0;
+}
+
 int cs_pack(const cs_pack_desc* descs, int n, void* stream) {
   if (n < 0 || (n > 0 && descs == nullptr))
     return set_error(CS_ERR_ARG, "cs_pack: invalid descriptor array (n=%d)", n);

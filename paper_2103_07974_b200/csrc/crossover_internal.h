@@ -65,6 +65,7 @@ cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s);
 template <int CAP>
 cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
 int tma_pack_chunk();
+extern int g_tune_k1_chunk, g_tune_k2_chunk, g_tune_k2_stages, g_tune_ctas_per_sm;
 int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
                          cudaStream_t s);

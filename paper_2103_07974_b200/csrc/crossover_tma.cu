@@ -115,7 +115,7 @@ __device__ __forceinline__ Chunk chunk_at(const Args& a, int c, int chunk) {
 // K1 (TMA): bucket <- gradients, staged through shared memory
 // ---------------------------------------------------------------------------
 template <int CAP>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads)
 pack_tma_kernel(const __grid_constant__ PackArgs<CAP> a, int chunk, int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
@@ -185,7 +185,7 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 
 template <int CAP, bool kMom>
-__global__ void __launch_bounds__(kTmaWsThreads, 1)
+__global__ void __launch_bounds__(kTmaWsThreads)
 unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
@@ -340,9 +340,13 @@ static cudaError_t opt_in_smem(K kernel, int bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-int tma_pack_chunk() { return kTmaPackChunk; }
+// experiment knobs (cs_tune); 0 = built-in heuristics
+int g_tune_k1_chunk = 0, g_tune_k2_chunk = 0, g_tune_k2_stages = 0, g_tune_ctas_per_sm = 0;
+
+int tma_pack_chunk() { return g_tune_k1_chunk ? g_tune_k1_chunk : kTmaPackChunk; }
 
 int tma_update_chunk(int nsrc, bool mom) {
+  if (g_tune_k2_chunk) return g_tune_k2_chunk;
   const int nin = nsrc + 1 + (mom ? 1 : 0);
   int chunk = kTmaMaxChunk;
   while (chunk > 512 && (size_t)nin * chunk * 4 * kTmaMinStages > (size_t)(kTmaSmemBudget - kTmaBarrierBytes))
@@ -350,21 +354,26 @@ int tma_update_chunk(int nsrc, bool mom) {
   return chunk;
 }
 
-static int stages_for(size_t stage_bytes) {
-  int st = (int)((kTmaSmemBudget - kTmaBarrierBytes) / stage_bytes);
-  if (st > kTmaMaxStages) st = kTmaMaxStages;
-  return st;
+static int tma_grid(int total) {
+  const int g = sm_count() * (g_tune_ctas_per_sm > 0 ? g_tune_ctas_per_sm : 1);
+  return total < g ? total : g;
+}
+
+static int budget() {
+  return g_tune_ctas_per_sm > 1 ? kTmaSmemBudget / g_tune_ctas_per_sm : kTmaSmemBudget;
 }
 
 template <int CAP>
 cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
-  const int chunk = kTmaPackChunk;
-  const int stages = stages_for((size_t)chunk * 4);
+  const int chunk = tma_pack_chunk();
+  int stages = (budget() - kTmaBarrierBytes) / (chunk * 4);
+  if (stages > kTmaMaxStages) stages = kTmaMaxStages;
+  if (stages < 2) return cudaErrorInvalidConfiguration;
   const int smem = kTmaBarrierBytes + stages * chunk * 4;
   cudaError_t e = opt_in_smem(pack_tma_kernel<CAP>, smem);
   if (e != cudaSuccess) return e;
-  const int grid = a.total_chunks < sm_count() ? a.total_chunks : sm_count();
+  const int grid = tma_grid(a.total_chunks);
   pack_tma_kernel<CAP><<<grid, kThreads, smem, s>>>(a, chunk, stages);
   return cudaGetLastError();
 }
@@ -374,10 +383,12 @@ cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream
   if (a.total_chunks == 0) return cudaSuccess;
   const int chunk = tma_update_chunk(a.nsrc, mom);
   const int nin = a.nsrc + 1 + (mom ? 1 : 0);
-  const int stages = stages_for((size_t)nin * chunk * 4);
+  int stages = (budget() - kTmaBarrierBytes) / (nin * chunk * 4);
+  if (stages > kTmaMaxStages) stages = kTmaMaxStages;
+  if (g_tune_k2_stages && g_tune_k2_stages < stages) stages = g_tune_k2_stages;
   if (stages <= kStoreLag) return cudaErrorInvalidConfiguration;
   const int smem = kTmaBarrierBytes + stages * nin * chunk * 4;
-  const int grid = a.total_chunks < sm_count() ? a.total_chunks : sm_count();
+  const int grid = tma_grid(a.total_chunks);
   cudaError_t e;
   if (mom) {
     e = opt_in_smem(unpack_sgd_tma_kernel<CAP, true>, smem);

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default="")
+    ap.add_argument("--only", default="", help="substring filter on case[variant] names")
+    ap.add_argument("--sweep", action="store_true", help="sweep TMA launch shapes (cs_tune)")
     args = ap.parse_args()
     import torchvision
 
@@ -72,6 +74,8 @@ def main():
     for variant_name, variant in (("tma", _lib.CS_VARIANT_TMA), ("register", _lib.CS_VARIANT_REGISTER)):
         _lib.set_kernel_variant(variant)
         for name, kw, what, nbytes in cases:
+            if args.only and args.only not in f"{name}[{variant_name}]":
+                continue
             s = FusedGradientSync(params, kw["sgd"], local_workers=kw["lw"], mode=kw["mode"])
             gl = [grads] * kw["lw"]
             if what == "pack":
@@ -85,6 +89,33 @@ def main():
             res["rows"].append({"name": f"{name}[{variant_name}]", "bytes": nbytes, "us": round(med * 1e3, 2),
                                 "best_us": round(best * 1e3, 2), "GB/s": round(nbytes / med / 1e6, 1),
                                 "frac_of_peak": round(nbytes / med / 1e6 / peak, 4)})
+    if args.sweep:
+        _lib.set_kernel_variant(_lib.CS_VARIANT_TMA)
+        sm = FusedGradientSync(params, SgdSettings(0.1, momentum=0.9, weight_decay=1e-4), mode="direct")
+        for cps in (1, 2):
+            for chunk in (1024, 2048, 4096):
+                for st in (0, 4):
+                    _lib.tune("ctas_per_sm", cps); _lib.tune("k2_chunk", chunk); _lib.tune("k2_stages", st)
+                    try:
+                        med, best = timeit(lambda: sm.update(stream.cuda_stream, grads), args.iters)
+                    except Exception as e:  # noqa: BLE001
+                        print("sweep k2", cps, chunk, st, "failed", e); continue
+                    res["rows"].append({"name": f"sweep_k2[cps={cps},chunk={chunk},stages={st or 'auto'}]",
+                                        "bytes": 5 * S, "us": round(med * 1e3, 2), "GB/s": round(5 * S / med / 1e6, 1),
+                                        "frac_of_peak": round(5 * S / med / 1e6 / peak, 4)})
+        sp = FusedGradientSync(params, SgdSettings(0.1), mode="bucket")
+        for cps in (1, 2):
+            for chunk in (4096, 8192, 16384):
+                _lib.tune("ctas_per_sm", cps); _lib.tune("k1_chunk", chunk)
+                try:
+                    med, best = timeit(lambda: sp.pack([grads], stream.cuda_stream), args.iters)
+                except Exception as e:  # noqa: BLE001
+                    print("sweep k1", cps, chunk, "failed", e); continue
+                res["rows"].append({"name": f"sweep_k1[cps={cps},chunk={chunk}]", "bytes": 2 * S,
+                                    "us": round(med * 1e3, 2), "GB/s": round(2 * S / med / 1e6, 1),
+                                    "frac_of_peak": round(2 * S / med / 1e6 / peak, 4)})
+        for k in ("ctas_per_sm", "k2_chunk", "k2_stages", "k1_chunk"):
+            _lib.tune(k, 0)
     for r in res["rows"]:
         print(f"{r['name']:40s} {r['us']:9.2f} us  {r['GB/s']:8.1f} GB/s  {r.get('frac_of_peak', '')}")
     if args.out:
