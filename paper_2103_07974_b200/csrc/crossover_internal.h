@@ -14,7 +14,7 @@ constexpr int kStatsMaxGrid = 148 * 8;             // fixed -> deterministic par
 
 // TMA (cp.async.bulk) variants: one persistent CTA per SM, stage ring in shared memory
 constexpr int kTmaBarrierBytes = 256;              // mbarriers in front of the stage ring
-constexpr int kTmaWsThreads = 64 + 256;            // producer warp + store warp + 8 consumer warps
+constexpr int kTmaWsThreads = 32 + 256;            // producer warp + 8 consumer warps
 constexpr int kTmaSmemBudget = 200 * 1024;         // dynamic shared memory per CTA
 constexpr int kTmaMaxStages = 8;
 constexpr int kTmaMinStages = 6;

@@ -79,6 +79,11 @@ __device__ __forceinline__ void bulk_wait_read_1() {
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+__device__ __forceinline__ void st_v4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -187,10 +192,12 @@ __device__ __forceinline__ void bulk_wait_read() {
 template <int CAP, bool kMom>
 __global__ void __launch_bounds__(kTmaWsThreads)
 unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages) {
+  // warp 0: TMA producer.  warps 1..: consumers read the stage from shared memory and
+  // write results straight to global memory with 128-bit stores (no store proxy, so a
+  // stage is free as soon as every consumer warp has read it).
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
-  uint64_t* computed = full + kTmaMaxStages;
-  uint64_t* empty = computed + kTmaMaxStages;
+  uint64_t* empty = full + kTmaMaxStages;
   float* slots = (float*)(smem + kTmaBarrierBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -198,7 +205,7 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
   const int nsrc = a.nsrc;
   const int nin = nsrc + 1 + (kMom ? 1 : 0);
   const size_t stage_floats = (size_t)nin * chunk;
-  constexpr int kConsumers = kTmaWsThreads - 64;
+  constexpr int kConsumers = kTmaWsThreads - 32;
 
   auto gsrc = [&](int s, const Chunk& k) {
     return (const float*)(a.base[s] + a.grad_off[k.seg] + (uint64_t)k.e0 * 4u);
@@ -217,8 +224,7 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&computed[s], kConsumers / 32);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
     }
     fence_mbar_init();
   }
@@ -244,44 +250,20 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
     }
     return;
   }
-  if (warp == 1) {
-    if (lane == 0) {
-      for (int i = 0; i < my_n; ++i) {
-        const int slot = i % stages;
-        mbar_wait(&computed[slot], (uint32_t)(i / stages) & 1u);
-        const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
-        if (vec_ok(k)) {
-          const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
-          float* sp = slots + (size_t)slot * stage_floats + (size_t)nsrc * chunk;
-          bulk_store(a.param[k.seg] + k.e0, sp, bytes);
-          if (kMom) bulk_store(a.mom[k.seg] + k.e0, sp + chunk, bytes);
-          float* snap = snap_ptr(k);
-          if (snap) bulk_store(snap, sp, bytes);
-        }
-        bulk_commit();
-        bulk_wait_read<kStoreLag>();
-        const int j = i - kStoreLag;                    // its store has left shared memory
-        if (j >= 0 && j + stages < my_n) mbar_arrive(&empty[j % stages]);
-      }
-      bulk_wait_read<0>();
-      for (int j = my_n - kStoreLag; j < my_n; ++j)
-        if (j >= 0 && j + stages < my_n) mbar_arrive(&empty[j % stages]);
-      bulk_wait_all();
-    }
-    return;
-  }
 
-  // consumers
   const Rule r = make_rule(a.h, kMom);
-  const int ctid = threadIdx.x - 64;
+  const int ctid = threadIdx.x - 32;
   for (int i = 0; i < my_n; ++i) {
     const int slot = i % stages;
     const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
     const bool vec = vec_ok(k);
     const int n4 = vec ? (k.n & ~3) : 0;
-    float* st = slots + (size_t)slot * stage_floats;
-    float* sp = st + (size_t)nsrc * chunk;
-    float* sm = sp + chunk;
+    const float* st = slots + (size_t)slot * stage_floats;
+    const float* sp = st + (size_t)nsrc * chunk;
+    const float* sm = sp + chunk;
+    float* p = a.param[k.seg] + k.e0;
+    float* m = kMom ? a.mom[k.seg] + k.e0 : nullptr;
+    float* snap = snap_ptr(k);
     mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
     for (int e4 = ctid * 4; e4 < n4; e4 += kConsumers * 4) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -296,26 +278,21 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
       pv.y = sgd_elem(r, acc.y, pv.y, &mv.y);
       pv.z = sgd_elem(r, acc.z, pv.z, &mv.z);
       pv.w = sgd_elem(r, acc.w, pv.w, &mv.w);
-      *(float4*)(sp + e4) = pv;
-      if (kMom) *(float4*)(sm + e4) = mv;
+      st_v4(p + e4, pv);
+      if (kMom) st_v4(m + e4, mv);
+      if (snap) st_v4(snap + e4, pv);
     }
-    if (n4 < k.n) {                                     // tail / misaligned: global memory
-      float* p = a.param[k.seg] + k.e0;
-      float* m = kMom ? a.mom[k.seg] + k.e0 : nullptr;
-      float* snap = snap_ptr(k);
-      for (int e = n4 + ctid; e < k.n; e += kConsumers) {
-        float acc = 0.0f;
-        for (int s = 0; s < nsrc; ++s) acc = __fadd_rn(acc, gsrc(s, k)[e]);
-        float b = kMom ? m[e] : 0.0f;
-        const float np = sgd_elem(r, acc, p[e], &b);
-        p[e] = np;
-        if (kMom) m[e] = b;
-        if (snap) snap[e] = np;
-      }
-    }
-    fence_proxy_async();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&computed[slot]);
+    if (lane == 0) mbar_arrive(&empty[slot]);           // stage may be refilled
+    for (int e = n4 + ctid; e < k.n; e += kConsumers) {  // tail / misaligned: global memory
+      float acc = 0.0f;
+      for (int s = 0; s < nsrc; ++s) acc = __fadd_rn(acc, gsrc(s, k)[e]);
+      float b = kMom ? m[e] : 0.0f;
+      const float np = sgd_elem(r, acc, p[e], &b);
+      p[e] = np;
+      if (kMom) m[e] = b;
+      if (snap) snap[e] = np;
+    }
   }
 }
 
@@ -386,7 +363,7 @@ cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream
   int stages = (budget() - kTmaBarrierBytes) / (nin * chunk * 4);
   if (stages > kTmaMaxStages) stages = kTmaMaxStages;
   if (g_tune_k2_stages && g_tune_k2_stages < stages) stages = g_tune_k2_stages;
-  if (stages <= kStoreLag) return cudaErrorInvalidConfiguration;
+  if (stages < 2) return cudaErrorInvalidConfiguration;
   const int smem = kTmaBarrierBytes + stages * nin * chunk * 4;
   const int grid = tma_grid(a.total_chunks);
   cudaError_t e;
