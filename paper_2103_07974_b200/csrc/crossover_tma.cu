@@ -88,77 +88,95 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int CAP>
-__device__ __forceinline__ int find_seg(const int* cb, int n, int c) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (cb[mid] <= c) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
+// Descriptor tables live in __grid_constant__ kernel parameters (constant bank).
+// A persistent CTA touches every descriptor many times, and dependent constant-
+// cache misses on one producer thread serialise the whole pipeline, so each CTA
+// first copies the n descriptors it needs into shared memory and walks its
+// (monotonically increasing) chunk sequence with a cursor instead of a search.
 struct Chunk {
   int seg;
   int64_t e0;
   int n;
 };
 
-template <int CAP, typename Args>
-__device__ __forceinline__ Chunk chunk_at(const Args& a, int c, int chunk) {
-  Chunk k;
-  k.seg = find_seg<CAP>(a.chunk_begin, a.n, c);
-  k.e0 = (int64_t)(c - a.chunk_begin[k.seg]) * chunk;
-  const int64_t rem = a.numel[k.seg] - k.e0;
-  k.n = rem < chunk ? (int)rem : chunk;
-  return k;
+struct Cursor {
+  int seg = 0;
+  __device__ __forceinline__ Chunk at(const int* cb, const int64_t* numel, int c, int chunk) {
+    while (cb[seg + 1] <= c) ++seg;
+    Chunk k;
+    k.seg = seg;
+    k.e0 = (int64_t)(c - cb[seg]) * chunk;
+    const int64_t rem = numel[seg] - k.e0;
+    k.n = rem < chunk ? (int)rem : chunk;
+    return k;
+  }
+};
+
+__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~(size_t)127; }
+
+// shared-memory table sizes (bytes) for n descriptors
+__host__ __device__ inline size_t pack_table_bytes(int n) {
+  return align128((size_t)(n + 1) * 4 + (size_t)n * 24);
+}
+__host__ __device__ inline size_t update_table_bytes(int n) {
+  return align128((size_t)(n + 1) * 4 + (size_t)n * 40);
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
 // K1 (TMA): bucket <- gradients, staged through shared memory
+//   all threads: copy descriptor table to smem; thread 0 = producer + storer
 // ---------------------------------------------------------------------------
 template <int CAP>
 __global__ void __launch_bounds__(kThreads)
 pack_tma_kernel(const __grid_constant__ PackArgs<CAP> a, int chunk, int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
-  float* slots = (float*)(smem + kTmaBarrierBytes);
+  const int n = a.n;
+  int64_t* t_numel = (int64_t*)(smem + kTmaBarrierBytes);
+  const float** t_src = (const float**)(t_numel + n);
+  float** t_dst = (float**)(t_src + n);
+  int* t_cb = (int*)(t_dst + n);
+  float* slots = (float*)(smem + kTmaBarrierBytes + pack_table_bytes(n));
   const int tid = threadIdx.x;
   const int G = gridDim.x;
   const int my_n = (a.total_chunks - (int)blockIdx.x + G - 1) / G;
 
-  auto vec_ok = [&](const Chunk& k) {
-    return ((((uintptr_t)(a.src[k.seg] + k.e0)) | ((uintptr_t)(a.dst[k.seg] + k.e0))) & 15u) == 0;
-  };
-  auto issue = [&](int i) {
-    const int slot = i % stages;
-    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
-    const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
-    if (vec_ok(k) && bytes) {
-      mbar_arrive_expect_tx(&full[slot], bytes);
-      bulk_load(slots + (size_t)slot * chunk, a.src[k.seg] + k.e0, bytes, &full[slot]);
-    } else {
-      mbar_arrive(&full[slot]);
-    }
-  };
-
+  for (int i = tid; i <= n; i += kThreads) {
+    t_cb[i] = a.chunk_begin[i];
+    if (i < n) { t_numel[i] = a.numel[i]; t_src[i] = a.src[i]; t_dst[i] = a.dst[i]; }
+  }
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
+
+  auto vec_ok = [&](const Chunk& k) {
+    return ((((uintptr_t)(t_src[k.seg] + k.e0)) | ((uintptr_t)(t_dst[k.seg] + k.e0))) & 15u) == 0;
+  };
+  Cursor prod, cons;
+  auto issue = [&](int i) {
+    const int slot = i % stages;
+    const Chunk k = prod.at(t_cb, t_numel, (int)blockIdx.x + i * G, chunk);
+    const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
+    if (vec_ok(k) && bytes) {
+      mbar_arrive_expect_tx(&full[slot], bytes);
+      bulk_load(slots + (size_t)slot * chunk, t_src[k.seg] + k.e0, bytes, &full[slot]);
+    } else {
+      mbar_arrive(&full[slot]);
+    }
+  };
   if (tid == 0)
     for (int i = 0; i < stages && i < my_n; ++i) issue(i);
 
   for (int i = 0; i < my_n; ++i) {
     const int slot = i % stages;
-    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
-    const float* src = a.src[k.seg] + k.e0;
-    float* dst = a.dst[k.seg] + k.e0;
-    const bool vec = vec_ok(k);
-    const int n4 = vec ? (k.n & ~3) : 0;
+    const Chunk k = cons.at(t_cb, t_numel, (int)blockIdx.x + i * G, chunk);
+    const float* src = t_src[k.seg] + k.e0;
+    float* dst = t_dst[k.seg] + k.e0;
+    const int n4 = vec_ok(k) ? (k.n & ~3) : 0;
     mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
     for (int e = n4 + tid; e < k.n; e += kThreads) dst[e] = src[e];   // tail / misaligned
     __syncthreads();
@@ -176,29 +194,25 @@ pack_tma_kernel(const __grid_constant__ PackArgs<CAP> a, int chunk, int stages) 
 
 // ---------------------------------------------------------------------------
 // K2 (TMA, warp-specialised): sources + param (+ momentum) -> param (+ momentum, snapshot)
-//   warp 0  producer : waits empty[s], issues the stage's bulk loads on full[s]
-//   warp 1  storer   : waits computed[s], issues bulk stores, frees stage s once its
-//                      store has been read out of shared memory (kStoreLag groups behind)
-//   warps 2+ consumers: wait full[s], update in shared memory, arrive computed[s]
+//   warp 0     producer : waits empty[s], issues the stage's bulk loads on full[s]
+//   warps 1..8 consumers: wait full[s], read the stage from shared memory, update,
+//                         store straight to global (STG.128), arrive empty[s]
 // stage layout: [g_0 | g_1 | ... | g_{S-1} | p | m], each `chunk` floats
 // ---------------------------------------------------------------------------
-constexpr int kStoreLag = 2;
-
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-
 template <int CAP, bool kMom>
 __global__ void __launch_bounds__(kTmaWsThreads)
 unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages) {
-  // warp 0: TMA producer.  warps 1..: consumers read the stage from shared memory and
-  // write results straight to global memory with 128-bit stores (no store proxy, so a
-  // stage is free as soon as every consumer warp has read it).
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + kTmaMaxStages;
-  float* slots = (float*)(smem + kTmaBarrierBytes);
+  const int n = a.n;
+  int64_t* t_numel = (int64_t*)(smem + kTmaBarrierBytes);
+  uint64_t* t_goff = (uint64_t*)(t_numel + n);
+  uint64_t* t_soff = t_goff + n;
+  float** t_param = (float**)(t_soff + n);
+  float** t_mom = t_param + n;
+  int* t_cb = (int*)(t_mom + n);
+  float* slots = (float*)(smem + kTmaBarrierBytes + update_table_bytes(n));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int my_n = (a.total_chunks - (int)blockIdx.x + G - 1) / G;
@@ -206,21 +220,18 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
   const int nin = nsrc + 1 + (kMom ? 1 : 0);
   const size_t stage_floats = (size_t)nin * chunk;
   constexpr int kConsumers = kTmaWsThreads - 32;
+  uint64_t base[CS_MAX_SOURCES];
+#pragma unroll
+  for (int s = 0; s < CS_MAX_SOURCES; ++s) base[s] = a.base[s];
+  float* const snapshot = a.snapshot;
 
-  auto gsrc = [&](int s, const Chunk& k) {
-    return (const float*)(a.base[s] + a.grad_off[k.seg] + (uint64_t)k.e0 * 4u);
-  };
-  auto snap_ptr = [&](const Chunk& k) {
-    return a.snapshot ? (float*)((char*)a.snapshot + a.snap_off[k.seg]) + k.e0 : nullptr;
-  };
-  auto vec_ok = [&](const Chunk& k) {
-    uintptr_t al = (uintptr_t)(a.param[k.seg] + k.e0);
-    if (kMom) al |= (uintptr_t)(a.mom[k.seg] + k.e0);
-    if (a.snapshot) al |= (uintptr_t)snap_ptr(k);
-    for (int s = 0; s < nsrc; ++s) al |= (uintptr_t)gsrc(s, k);
-    return (al & 15u) == 0 && k.n >= 4;
-  };
-
+  for (int i = threadIdx.x; i <= n; i += kTmaWsThreads) {
+    t_cb[i] = a.chunk_begin[i];
+    if (i < n) {
+      t_numel[i] = a.numel[i]; t_goff[i] = a.grad_off[i]; t_soff[i] = a.snap_off[i];
+      t_param[i] = a.param[i]; t_mom[i] = a.mom[i];
+    }
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
@@ -230,19 +241,34 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
   }
   __syncthreads();
 
+  auto gsrc = [&](int s, const Chunk& k) {
+    return (const float*)(base[s] + t_goff[k.seg] + (uint64_t)k.e0 * 4u);
+  };
+  auto snap_ptr = [&](const Chunk& k) {
+    return snapshot ? (float*)((char*)snapshot + t_soff[k.seg]) + k.e0 : nullptr;
+  };
+  auto vec_ok = [&](const Chunk& k) {
+    uintptr_t al = (uintptr_t)(t_param[k.seg] + k.e0);
+    if (kMom) al |= (uintptr_t)(t_mom[k.seg] + k.e0);
+    if (snapshot) al |= (uintptr_t)snap_ptr(k);
+    for (int s = 0; s < nsrc; ++s) al |= (uintptr_t)gsrc(s, k);
+    return (al & 15u) == 0 && k.n >= 4;
+  };
+
+  Cursor cur;
   if (warp == 0) {
     if (lane == 0) {
       for (int i = 0; i < my_n; ++i) {
         const int slot = i % stages;
         if (i >= stages) mbar_wait(&empty[slot], (uint32_t)((i / stages) + 1) & 1u);
-        const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
+        const Chunk k = cur.at(t_cb, t_numel, (int)blockIdx.x + i * G, chunk);
         if (vec_ok(k)) {
           const uint32_t bytes = (uint32_t)(k.n & ~3) * 4u;
           float* st = slots + (size_t)slot * stage_floats;
           mbar_arrive_expect_tx(&full[slot], bytes * (uint32_t)nin);
           for (int s = 0; s < nsrc; ++s) bulk_load(st + (size_t)s * chunk, gsrc(s, k), bytes, &full[slot]);
-          bulk_load(st + (size_t)nsrc * chunk, a.param[k.seg] + k.e0, bytes, &full[slot]);
-          if (kMom) bulk_load(st + (size_t)(nsrc + 1) * chunk, a.mom[k.seg] + k.e0, bytes, &full[slot]);
+          bulk_load(st + (size_t)nsrc * chunk, t_param[k.seg] + k.e0, bytes, &full[slot]);
+          if (kMom) bulk_load(st + (size_t)(nsrc + 1) * chunk, t_mom[k.seg] + k.e0, bytes, &full[slot]);
         } else {
           mbar_arrive(&full[slot]);
         }
@@ -255,14 +281,13 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
   const int ctid = threadIdx.x - 32;
   for (int i = 0; i < my_n; ++i) {
     const int slot = i % stages;
-    const Chunk k = chunk_at<CAP>(a, (int)blockIdx.x + i * G, chunk);
-    const bool vec = vec_ok(k);
-    const int n4 = vec ? (k.n & ~3) : 0;
+    const Chunk k = cur.at(t_cb, t_numel, (int)blockIdx.x + i * G, chunk);
+    const int n4 = vec_ok(k) ? (k.n & ~3) : 0;
     const float* st = slots + (size_t)slot * stage_floats;
     const float* sp = st + (size_t)nsrc * chunk;
     const float* sm = sp + chunk;
-    float* p = a.param[k.seg] + k.e0;
-    float* m = kMom ? a.mom[k.seg] + k.e0 : nullptr;
+    float* p = t_param[k.seg] + k.e0;
+    float* m = kMom ? t_mom[k.seg] + k.e0 : nullptr;
     float* snap = snap_ptr(k);
     mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
     for (int e4 = ctid * 4; e4 < n4; e4 += kConsumers * 4) {
@@ -326,7 +351,8 @@ int tma_update_chunk(int nsrc, bool mom) {
   if (g_tune_k2_chunk) return g_tune_k2_chunk;
   const int nin = nsrc + 1 + (mom ? 1 : 0);
   int chunk = kTmaMaxChunk;
-  while (chunk > 512 && (size_t)nin * chunk * 4 * kTmaMinStages > (size_t)(kTmaSmemBudget - kTmaBarrierBytes))
+  while (chunk > 512 && (size_t)nin * chunk * 4 * kTmaMinStages >
+                           (size_t)(kTmaSmemBudget - kTmaBarrierBytes) - update_table_bytes(kCapLarge))
     chunk >>= 1;
   return chunk;
 }
@@ -344,10 +370,11 @@ template <int CAP>
 cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
   const int chunk = tma_pack_chunk();
-  int stages = (budget() - kTmaBarrierBytes) / (chunk * 4);
+  const int table = (int)pack_table_bytes(a.n);
+  int stages = (budget() - kTmaBarrierBytes - table) / (chunk * 4);
   if (stages > kTmaMaxStages) stages = kTmaMaxStages;
   if (stages < 2) return cudaErrorInvalidConfiguration;
-  const int smem = kTmaBarrierBytes + stages * chunk * 4;
+  const int smem = kTmaBarrierBytes + table + stages * chunk * 4;
   cudaError_t e = opt_in_smem(pack_tma_kernel<CAP>, smem);
   if (e != cudaSuccess) return e;
   const int grid = tma_grid(a.total_chunks);
@@ -360,11 +387,12 @@ cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream
   if (a.total_chunks == 0) return cudaSuccess;
   const int chunk = tma_update_chunk(a.nsrc, mom);
   const int nin = a.nsrc + 1 + (mom ? 1 : 0);
-  int stages = (budget() - kTmaBarrierBytes) / (nin * chunk * 4);
+  const int table = (int)update_table_bytes(a.n);
+  int stages = (budget() - kTmaBarrierBytes - table) / (nin * chunk * 4);
   if (stages > kTmaMaxStages) stages = kTmaMaxStages;
   if (g_tune_k2_stages && g_tune_k2_stages < stages) stages = g_tune_k2_stages;
   if (stages < 2) return cudaErrorInvalidConfiguration;
-  const int smem = kTmaBarrierBytes + stages * nin * chunk * 4;
+  const int smem = kTmaBarrierBytes + table + stages * nin * chunk * 4;
   const int grid = tma_grid(a.total_chunks);
   cudaError_t e;
   if (mom) {
