@@ -91,16 +91,17 @@ CS_API int cs_abi_version(void);
 CS_API const char* cs_last_error(void);
 
 /* Kernel implementation used by cs_pack / cs_unpack_sgd (process-wide).
- * CS_VARIANT_TMA (default): persistent CTAs streaming through a shared-memory
- * stage ring with cp.async.bulk loads/stores and mbarriers.
- * CS_VARIANT_REGISTER: one CTA per 4096-element chunk, 128-bit register loads.
+ * CS_VARIANT_REGISTER (default): one CTA per chunk, 128-bit register loads/stores.
+ * CS_VARIANT_TMA: persistent CTAs streaming through a shared-memory stage ring
+ * with cp.async.bulk loads (+ bulk stores in K1) and mbarriers.
  * Both produce bit-identical results. */
 enum { CS_VARIANT_TMA = 0, CS_VARIANT_REGISTER = 1 };
 CS_API int cs_set_kernel_variant(int variant);
 CS_API int cs_get_kernel_variant(void);
 /* Launch-shape knobs of the TMA variant (0 restores the built-in heuristic):
  * "k1_chunk", "k2_chunk" (fp32 elements per stream per stage), "k2_stages",
- * "ctas_per_sm".  Results never depend on them. */
+ * "ctas_per_sm"; of the register variant: "reg_shape" (0..4: unroll x CTAs/SM).
+ * Results never depend on them. */
 CS_API int cs_tune(const char* key, int value);
 
 /* K1: gather n tensors into the bucket (128-bit vector path when src and dst

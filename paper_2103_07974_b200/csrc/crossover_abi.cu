@@ -33,7 +33,7 @@ int cuda_status(cudaError_t e, const char* where) {
   return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
 }
 
-static int g_variant = CS_VARIANT_TMA;
+static int g_variant = CS_VARIANT_REGISTER;
 
 static int64_t chunks_of(int64_t numel, int chunk) { return (numel + chunk - 1) / chunk; }
 
@@ -42,7 +42,7 @@ static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
   static thread_local PackArgs<CAP> a;  // ~28 KB for the large capacity: keep off the stack
   a.n = n;
   const bool tma = g_variant == CS_VARIANT_TMA;
-  const int chunk = tma ? tma_pack_chunk() : kChunk;
+  const int chunk = tma ? tma_pack_chunk() : reg_pack_chunk();
   int64_t c = 0;
   for (int i = 0; i < n; ++i) {
     a.chunk_begin[i] = (int)c;
@@ -69,7 +69,7 @@ static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources,
   a.h = *h;
   const bool mom = h->momentum != 0.0f;
   const bool tma = g_variant == CS_VARIANT_TMA;
-  const int chunk = tma ? tma_update_chunk(nsrc, mom) : kChunk;
+  const int chunk = tma ? tma_update_chunk(nsrc, mom) : reg_update_chunk();
   int64_t c = 0;
   for (int i = 0; i < n; ++i) {
     a.chunk_begin[i] = (int)c;
@@ -113,6 +113,8 @@ int cs_tune(const char* key, int value) {
   else if (k == "k2_chunk" && (value == 0 || (value % 256 == 0 && value <= 8192))) g_tune_k2_chunk = value;
   else if (k == "k2_stages" && value <= kTmaMaxStages) g_tune_k2_stages = value;
   else if (k == "ctas_per_sm" && value <= 4) g_tune_ctas_per_sm = value;
+  else if (k == "k2_debug" && value <= 2) g_tune_k2_debug = value;  // ablation only: wrong results
+  else if (k == "reg_shape" && value <= 4) g_tune_reg_shape = value;
   else return set_error(CS_ERR_ARG, "cs_tune: unknown key or bad value (%s=%d)", key, value);
   return 0;
 }

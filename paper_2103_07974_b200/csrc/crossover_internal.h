@@ -8,8 +8,6 @@
 namespace cs {
 
 constexpr int kThreads = 256;                      // 8 warps per CTA
-constexpr int kUnroll = 4;                         // 128-bit loads in flight per thread
-constexpr int kChunk = kThreads * 4 * kUnroll;     // 4096 fp32 = 16 KB per CTA
 constexpr int kStatsMaxGrid = 148 * 8;             // fixed -> deterministic partial order
 
 // TMA (cp.async.bulk) variants: one persistent CTA per SM, stage ring in shared memory
@@ -65,7 +63,10 @@ cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s);
 template <int CAP>
 cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
 int tma_pack_chunk();
-extern int g_tune_k1_chunk, g_tune_k2_chunk, g_tune_k2_stages, g_tune_ctas_per_sm;
+int reg_pack_chunk();
+int reg_update_chunk();
+extern int g_tune_reg_shape;
+extern int g_tune_k1_chunk, g_tune_k2_chunk, g_tune_k2_stages, g_tune_ctas_per_sm, g_tune_k2_debug;
 int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
                          cudaStream_t s);

@@ -1,4 +1,4 @@
-// crossover_kernels.cu -- sm_100a kernels of the crossover step.
+// crossover_kernels.cu -- register-path sm_100a kernels of the crossover step.
 //
 //   K1  pack_kernel        gradient fusion into one contiguous bucket
 //                          (reference: workload.fuse_gradients, workload.py:94-101)
@@ -9,12 +9,14 @@
 //
 // All three are HBM-streaming kernels: no data reuse, so no shared-memory
 // staging and no tensor cores.  Work is cut into fixed CHUNK-element chunks
-// (one CTA each) so a 64-element BatchNorm bias and a 2.4M-element conv weight
-// get the same per-CTA shape; the tensor owning a chunk is found by a binary
-// search over the chunk prefix held in __grid_constant__ kernel parameters
-// (uniform per CTA -> constant-cache broadcast, no device-side table, no
-// per-step H2D copy).  Each thread keeps UNROLL independent 128-bit loads in
-// flight before its first store.
+// (one CTA each, CHUNK = 256 threads x 4 floats x U) so a 64-element BatchNorm
+// bias and a 2.4M-element conv weight get the same per-CTA shape; the tensor
+// owning a chunk is found by a binary search over the chunk prefix held in
+// __grid_constant__ kernel parameters (uniform per CTA -> constant-cache
+// broadcast, no device-side table, no per-step H2D copy).  Each thread keeps
+// U independent 128-bit loads per stream in flight before its first store.
+// The launch shape (U, CTAs per SM) is a template choice selected at run time
+// (reg_shape(), cs_tune "reg_shape"); results never depend on it.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,6 +25,8 @@
 #include "crossover_sgd.cuh"
 
 namespace cs {
+
+int g_tune_reg_shape = 0;
 
 // ---------------------------------------------------------------------------
 // 128-bit memory helpers (inline PTX so the cache policy is explicit)
@@ -49,7 +53,6 @@ __device__ __forceinline__ void st_v4(float* p, float4 v) {
                : "memory");
 }
 
-template <int CAP>
 __device__ __forceinline__ int find_segment(const int* chunk_begin, int n, int c) {
   // largest i with chunk_begin[i] <= c (zero-chunk tensors are skipped naturally)
   int lo = 0, hi = n - 1;
@@ -63,16 +66,17 @@ __device__ __forceinline__ int find_segment(const int* chunk_begin, int n, int c
 // ---------------------------------------------------------------------------
 // K1: pack
 // ---------------------------------------------------------------------------
-template <int CAP>
+template <int CAP, int U>
 __global__ void __launch_bounds__(kThreads)
 pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
+  constexpr int CH = kThreads * 4 * U;
   const int c = blockIdx.x;
-  const int i = find_segment<CAP>(a.chunk_begin, a.n, c);
-  const int64_t e0 = (int64_t)(c - a.chunk_begin[i]) * kChunk;
+  const int i = find_segment(a.chunk_begin, a.n, c);
+  const int64_t e0 = (int64_t)(c - a.chunk_begin[i]) * CH;
   const float* __restrict__ src = a.src[i] + e0;
   float* __restrict__ dst = a.dst[i] + e0;
   const int64_t rem = a.numel[i] - e0;
-  const int n = rem < kChunk ? (int)rem : kChunk;
+  const int n = rem < CH ? (int)rem : CH;
   const int tid = threadIdx.x;
 
   if ((((uintptr_t)src) | ((uintptr_t)dst)) & 15u) {
@@ -81,14 +85,14 @@ pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
     return;
   }
   const int nvec = n >> 2;
-  float4 v[kUnroll];
+  float4 v[U];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int idx = u * kThreads + tid;
     if (idx < nvec) v[u] = ld_stream(src + 4 * idx);
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int idx = u * kThreads + tid;
     if (idx < nvec) st_v4(dst + 4 * idx, v[u]);
   }
@@ -98,16 +102,16 @@ pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
 // ---------------------------------------------------------------------------
 // K2: fixed-order reduce over sources, average, SGD update
 // ---------------------------------------------------------------------------
-template <int CAP, bool kMom>
-__global__ void __launch_bounds__(kThreads)
+template <int CAP, bool kMom, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
+  constexpr int CH = kThreads * 4 * U;
   const int c = blockIdx.x;
-  const int i = find_segment<CAP>(a.chunk_begin, a.n, c);
-  const int64_t e0 = (int64_t)(c - a.chunk_begin[i]) * kChunk;
+  const int i = find_segment(a.chunk_begin, a.n, c);
+  const int64_t e0 = (int64_t)(c - a.chunk_begin[i]) * CH;
   const int64_t rem = a.numel[i] - e0;
-  const int n = rem < kChunk ? (int)rem : kChunk;
+  const int n = rem < CH ? (int)rem : CH;
   const int tid = threadIdx.x;
-
   const Rule r = make_rule(a.h, kMom);
 
   float* __restrict__ p = a.param[i] + e0;
@@ -136,11 +140,12 @@ unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
   }
 
   const int nvec = n >> 2;
-  float4 acc[kUnroll], pv[kUnroll], mv[kUnroll];
+  float4 acc[U], pv[U], mv[U];
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int idx = u * kThreads + tid;
     acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mv[u] = acc[u];
     if (idx < nvec) {
       pv[u] = ld_rw(p + 4 * idx);
       if (kMom) mv[u] = ld_rw(m + 4 * idx);
@@ -148,14 +153,14 @@ unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
   }
   for (int s = 0; s < nsrc; ++s) {
     const float* g = (const float*)(a.base[s] + goff);
-    float4 gv[kUnroll];
+    float4 gv[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int idx = u * kThreads + tid;
-      if (idx < nvec) gv[u] = ld_stream(g + 4 * idx);
+      gv[u] = idx < nvec ? ld_stream(g + 4 * idx) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       acc[u].x = __fadd_rn(acc[u].x, gv[u].x);
       acc[u].y = __fadd_rn(acc[u].y, gv[u].y);
       acc[u].z = __fadd_rn(acc[u].z, gv[u].z);
@@ -163,7 +168,7 @@ unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
     }
   }
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int idx = u * kThreads + tid;
     if (idx < nvec) {
       float4 o;
@@ -254,19 +259,41 @@ stats_kernel(const float* __restrict__ data, int64_t numel, double* __restrict__
 
 // ---------------------------------------------------------------------------
 // host-side launchers (called from crossover_abi.cu)
+//   reg shapes: 0 = (U4, 2 CTA/SM)  1 = (U4, 3)  2 = (U2, 4)  3 = (U8, 1)  4 = (U2, 3)
 // ---------------------------------------------------------------------------
+static int shape_unroll(int shape) {
+  static const int u[] = {4, 4, 2, 8, 2};
+  return u[shape];
+}
+
+int reg_pack_chunk() { return kThreads * 4 * (g_tune_reg_shape == 3 ? 8 : 4); }
+int reg_update_chunk() { return kThreads * 4 * shape_unroll(g_tune_reg_shape); }
+
 template <int CAP>
 cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
-  pack_kernel<CAP><<<a.total_chunks, kThreads, 0, s>>>(a);
+  if (g_tune_reg_shape == 3) pack_kernel<CAP, 8><<<a.total_chunks, kThreads, 0, s>>>(a);
+  else pack_kernel<CAP, 4><<<a.total_chunks, kThreads, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int CAP, bool kMom>
+static void launch_update_shape(const UpdateArgs<CAP>& a, cudaStream_t s) {
+  const int g = a.total_chunks;
+  switch (g_tune_reg_shape) {
+    case 1: unpack_sgd_kernel<CAP, kMom, 4, 3><<<g, kThreads, 0, s>>>(a); break;
+    case 2: unpack_sgd_kernel<CAP, kMom, 2, 4><<<g, kThreads, 0, s>>>(a); break;
+    case 3: unpack_sgd_kernel<CAP, kMom, 8, 1><<<g, kThreads, 0, s>>>(a); break;
+    case 4: unpack_sgd_kernel<CAP, kMom, 2, 3><<<g, kThreads, 0, s>>>(a); break;
+    default: unpack_sgd_kernel<CAP, kMom, 4, 2><<<g, kThreads, 0, s>>>(a); break;
+  }
 }
 
 template <int CAP>
 cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
-  if (mom) unpack_sgd_kernel<CAP, true><<<a.total_chunks, kThreads, 0, s>>>(a);
-  else unpack_sgd_kernel<CAP, false><<<a.total_chunks, kThreads, 0, s>>>(a);
+  if (mom) launch_update_shape<CAP, true>(a, s);
+  else launch_update_shape<CAP, false>(a, s);
   return cudaGetLastError();
 }
 

@@ -201,7 +201,7 @@ pack_tma_kernel(const __grid_constant__ PackArgs<CAP> a, int chunk, int stages) 
 // ---------------------------------------------------------------------------
 template <int CAP, bool kMom>
 __global__ void __launch_bounds__(kTmaWsThreads)
-unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages) {
+unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int stages, int debug) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + kTmaMaxStages;
@@ -290,6 +290,7 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
     float* m = kMom ? t_mom[k.seg] + k.e0 : nullptr;
     float* snap = snap_ptr(k);
     mbar_wait(&full[slot], (uint32_t)(i / stages) & 1u);
+    if (debug == 2) { __syncwarp(); if (lane == 0) mbar_arrive(&empty[slot]); continue; }
     for (int e4 = ctid * 4; e4 < n4; e4 += kConsumers * 4) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s = 0; s < nsrc; ++s) {
@@ -303,6 +304,7 @@ unpack_sgd_tma_kernel(const __grid_constant__ UpdateArgs<CAP> a, int chunk, int 
       pv.y = sgd_elem(r, acc.y, pv.y, &mv.y);
       pv.z = sgd_elem(r, acc.z, pv.z, &mv.z);
       pv.w = sgd_elem(r, acc.w, pv.w, &mv.w);
+      if (debug == 1) { if (pv.x == 12345.f && mv.x == 3.f) st_v4(p + e4, pv); continue; }
       st_v4(p + e4, pv);
       if (kMom) st_v4(m + e4, mv);
       if (snap) st_v4(snap + e4, pv);
@@ -344,6 +346,7 @@ static cudaError_t opt_in_smem(K kernel, int bytes) {
 
 // experiment knobs (cs_tune); 0 = built-in heuristics
 int g_tune_k1_chunk = 0, g_tune_k2_chunk = 0, g_tune_k2_stages = 0, g_tune_ctas_per_sm = 0;
+int g_tune_k2_debug = 0;
 
 int tma_pack_chunk() { return g_tune_k1_chunk ? g_tune_k1_chunk : kTmaPackChunk; }
 
@@ -398,11 +401,11 @@ cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream
   if (mom) {
     e = opt_in_smem(unpack_sgd_tma_kernel<CAP, true>, smem);
     if (e != cudaSuccess) return e;
-    unpack_sgd_tma_kernel<CAP, true><<<grid, kTmaWsThreads, smem, s>>>(a, chunk, stages);
+    unpack_sgd_tma_kernel<CAP, true><<<grid, kTmaWsThreads, smem, s>>>(a, chunk, stages, g_tune_k2_debug);
   } else {
     e = opt_in_smem(unpack_sgd_tma_kernel<CAP, false>, smem);
     if (e != cudaSuccess) return e;
-    unpack_sgd_tma_kernel<CAP, false><<<grid, kTmaWsThreads, smem, s>>>(a, chunk, stages);
+    unpack_sgd_tma_kernel<CAP, false><<<grid, kTmaWsThreads, smem, s>>>(a, chunk, stages, g_tune_k2_debug);
   }
   return cudaGetLastError();
 }

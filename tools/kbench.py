@@ -92,6 +92,7 @@ def main():
     if args.sweep:
         _lib.set_kernel_variant(_lib.CS_VARIANT_TMA)
         sm = FusedGradientSync(params, SgdSettings(0.1, momentum=0.9, weight_decay=1e-4), mode="direct")
+        sp0 = FusedGradientSync(params, SgdSettings(0.1), mode="bucket")
         for cps in (1, 2):
             for chunk in (1024, 2048, 4096):
                 for st in (0, 4):
@@ -114,6 +115,24 @@ def main():
                 res["rows"].append({"name": f"sweep_k1[cps={cps},chunk={chunk}]", "bytes": 2 * S,
                                     "us": round(med * 1e3, 2), "GB/s": round(2 * S / med / 1e6, 1),
                                     "frac_of_peak": round(2 * S / med / 1e6 / peak, 4)})
+        _lib.set_kernel_variant(_lib.CS_VARIANT_REGISTER)
+        for shape in range(5):
+            _lib.tune("reg_shape", shape)
+            for nm, obj, fn2, nb in (("k2_direct_momentum", sm, lambda: sm.update(stream.cuda_stream, grads), 5 * S),
+                                     ("k1_pack", sp0, lambda: sp0.pack([grads], stream.cuda_stream), 2 * S)):
+                med, best = timeit(fn2, args.iters)
+                res["rows"].append({"name": f"reg_{nm}[shape={shape}]", "bytes": nb, "us": round(med * 1e3, 2),
+                                    "GB/s": round(nb / med / 1e6, 1), "frac_of_peak": round(nb / med / 1e6 / peak, 4)})
+        _lib.tune("reg_shape", 0)
+        _lib.set_kernel_variant(_lib.CS_VARIANT_TMA)
+        for dbg in (1, 2):
+            for cps in (1, 2):
+                _lib.tune("ctas_per_sm", cps); _lib.tune("k2_chunk", 2048); _lib.tune("k2_stages", 0)
+                _lib.tune("k2_debug", dbg)
+                med, best = timeit(lambda: sm.update(stream.cuda_stream, grads), args.iters)
+                res["rows"].append({"name": f"ablate_k2[debug={dbg},cps={cps}]", "bytes": 5 * S,
+                                    "us": round(med * 1e3, 2), "GB/s": round(5 * S / med / 1e6, 1)})
+        _lib.tune("k2_debug", 0)
         for k in ("ctas_per_sm", "k2_chunk", "k2_stages", "k1_chunk"):
             _lib.tune(k, 0)
     for r in res["rows"]:
