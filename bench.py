@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     ap.add_argument("--trace-out", default="")
+    ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     return ap.parse_args()
 
 
@@ -215,8 +216,8 @@ def run_ours(args):
 
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
-    base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank)
-            for j in range(args.jobs)]
+    base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
+                  graphed=not args.no_graphs) for j in range(args.jobs)]
     host_data = None if args.no_e2e else [
         apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + j, dev, host_uint8=True))
         for j in range(args.jobs)]
@@ -329,7 +330,8 @@ def run_ours(args):
             "data": "synthetic (random-init weights, N(0,1) images / random labels)",
             "config": {"workload": f"{args.jobs}x {args.model} co-located, crossover, batch "
                                    f"{args.batch}/GPU, bf16 autocast, fp32 params/grads, "
-                                   f"SGD momentum 0.9 wd 1e-4",
+                                   f"SGD momentum 0.9 wd 1e-4"
+                                   + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs"),
                        "jobs": args.jobs, "model": args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": sync0.mode},

@@ -255,34 +255,64 @@ def _image_loss(model, batch):
     return F.cross_entropy(model(x), y)
 
 
+class _GraphedImageModel(torch.nn.Module):
+    """Forward and backward of a model captured as two CUDA graphs.
+
+    torch.cuda.make_graphed_callables captures the forward and the backward
+    separately, so the scheduler can still record the forward/backward span
+    boundary between the two replays; parameters stay the module's own
+    tensors (K2 updates them in place and the next replay reads the new
+    values), inputs are copied into the graph's static input buffer, and the
+    gradients come back in static graph memory -- stable addresses that the
+    scheduler keeps alive until the app's K2 has consumed them.
+    """
+
+    def __init__(self, model: torch.nn.Module, sample: torch.Tensor):
+        super().__init__()
+        self.inner = model
+        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+            self.graphed = torch.cuda.make_graphed_callables(model, (sample,), num_warmup_iters=3)
+
+    def forward(self, x):
+        return self.graphed(x)
+
+
 def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
                device: torch.device, seed: int, host_data: bool, sgd: SgdSettings,
-               n_batches: int = 2) -> App:
+               n_batches: int = 2, graphed: bool = False) -> App:
     model = model.to(device).to(memory_format=torch.channels_last)
     data = _CycleData(synthetic_image_batches(batch, n_batches, seed, device, host_uint8=host_data))
-    return App(job_id, model, _image_loss, data, sgd, iterations,
-               autocast_dtype=torch.bfloat16, samples_per_batch=batch)
+    params = [p for p in model.parameters() if p.requires_grad]
+    if graphed:
+        sample = torch.randn((batch, 3, 224, 224), device=device, dtype=torch.bfloat16
+                             ).contiguous(memory_format=torch.channels_last)
+        model = _GraphedImageModel(model, sample)
+    return App(job_id, model, _image_loss, data, sgd, iterations, params=params,
+               autocast_dtype=torch.bfloat16, samples_per_batch=batch,
+               autocast_cache=not graphed)
 
 
 DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
 
 
 def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
-                 host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD) -> App:
+                 host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
+                 graphed: bool = False) -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device, seed,
-                      host_data, sgd)
+                      host_data, sgd, graphed=graphed)
 
 
 def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
-              host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD) -> App:
+              host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
+              graphed: bool = False) -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device, seed,
-                      host_data, sgd)
+                      host_data, sgd, graphed=graphed)
 
 
 def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,

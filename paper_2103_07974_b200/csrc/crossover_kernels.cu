@@ -26,7 +26,7 @@
 
 namespace cs {
 
-int g_tune_reg_shape = 0;
+int g_tune_reg_shape = 1;  // U=4, 3 CTAs/SM: best measured K2 shape (kbench sweep)
 
 // ---------------------------------------------------------------------------
 // 128-bit memory helpers (inline PTX so the cache policy is explicit)

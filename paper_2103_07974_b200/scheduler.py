@@ -86,6 +86,7 @@ class App:
     autocast_dtype: torch.dtype | None = None
     params: list[torch.Tensor] | None = None
     samples_per_batch: int = 0   # for samples/s accounting (per worker)
+    autocast_cache: bool = True  # must be False when the model replays CUDA graphs
 
     def __post_init__(self):
         if self.iterations < 1:
@@ -310,8 +311,8 @@ class CrossoverScheduler:
             batches = [self._to_device(app.data(t, w)) for w in workers]
             e_f0 = ev()
             e_f0.record(cs)
-            amp = (torch.autocast("cuda", dtype=app.autocast_dtype) if app.autocast_dtype
-                   else contextlib.nullcontext())
+            amp = (torch.autocast("cuda", dtype=app.autocast_dtype, cache_enabled=app.autocast_cache)
+                   if app.autocast_dtype else contextlib.nullcontext())
             losses = []
             with amp:
                 for b in batches:

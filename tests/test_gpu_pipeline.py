@@ -176,3 +176,20 @@ def test_resnet50_two_jobs_smoke(cuda_device):
     assert validate_trace(tr) == []
     assert all(torch.isfinite(l).all() for st in s.states for l in st.losses)
     assert any(not torch.equal(a, b) for a, b in zip(before, s.states[0].app.params[:3]))
+
+
+def test_resnet50_graphed_two_jobs(cuda_device):
+    """Forward/backward replayed as CUDA graphs: same pipeline, legal trace, finite losses."""
+    from paper_2103_07974_b200.apps import resnet50_app
+    from paper_2103_07974_b200.engine import schedule_key, validate_trace
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy, rotation_schedule
+
+    s = CrossoverScheduler(Policy.CROSSOVER)
+    for k in range(2):
+        s.register(resnet50_app(f"g{k}", 8, 4, cuda_device, seed=k, graphed=True))
+    before = s.states[1].app.params[0].detach().clone()
+    tr = s.run()
+    assert schedule_key(tr) == rotation_schedule(["g0", "g1"], [4, 4])
+    assert validate_trace(tr) == []
+    assert all(torch.isfinite(l).all() for st in s.states for l in st.losses)
+    assert not torch.equal(before, s.states[1].app.params[0])

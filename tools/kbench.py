@@ -93,6 +93,9 @@ def main():
         _lib.set_kernel_variant(_lib.CS_VARIANT_TMA)
         sm = FusedGradientSync(params, SgdSettings(0.1, momentum=0.9, weight_decay=1e-4), mode="direct")
         sp0 = FusedGradientSync(params, SgdSettings(0.1), mode="bucket")
+        sp0.pack([grads], stream.cuda_stream)
+        s2 = FusedGradientSync(params, SgdSettings(0.1, momentum=0.9), mode="bucket", local_workers=2)
+        s2.pack([grads, grads], stream.cuda_stream)
         for cps in (1, 2):
             for chunk in (1024, 2048, 4096):
                 for st in (0, 4):
@@ -119,6 +122,8 @@ def main():
         for shape in range(5):
             _lib.tune("reg_shape", shape)
             for nm, obj, fn2, nb in (("k2_direct_momentum", sm, lambda: sm.update(stream.cuda_stream, grads), 5 * S),
+                                     ("k2_bucket_plain_ref", sp0, lambda: sp0.update(stream.cuda_stream), 3 * S),
+                                     ("k2_bucket_2src_momentum", s2, lambda: s2.update(stream.cuda_stream), 6 * S),
                                      ("k1_pack", sp0, lambda: sp0.pack([grads], stream.cuda_stream), 2 * S)):
                 med, best = timeit(fn2, args.iters)
                 res["rows"].append({"name": f"reg_{nm}[shape={shape}]", "bytes": nb, "us": round(med * 1e3, 2),
