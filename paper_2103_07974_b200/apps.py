@@ -270,6 +270,9 @@ class _GraphedImageModel(torch.nn.Module):
     def __init__(self, model: torch.nn.Module, sample: torch.Tensor):
         super().__init__()
         self.inner = model
+        quiet = getattr(torch.autograd.graph, "set_warn_on_accumulate_grad_stream_mismatch", None)
+        if quiet is not None:  # capture runs on a side stream by design
+            quiet(False)
         with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
             self.graphed = torch.cuda.make_graphed_callables(model, (sample,), num_warmup_iters=3)
 
