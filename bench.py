@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"],
+                    help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
+                         "the fused NVLink P2P kernel; auto = bucket")
     return ap.parse_args()
 
 
@@ -184,93 +187,162 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+class Harness:
+    """Per-process plumbing shared by bench.py and tools/sweep.py: device, comm, barrier, max."""
 
-    from paper_2103_07974_b200 import apps
-    from paper_2103_07974_b200.comm import NcclCommunicator
-    from paper_2103_07974_b200.engine import Phase, schedule_key, trace_to_chrome_json, validate_trace
-    from paper_2103_07974_b200.scheduler import (CrossoverScheduler, Policy, overlap_roofline,
-                                                 rotation_schedule)
+    def __init__(self, nccl_max_ctas: int = 0):
+        import torch
+        import torch.distributed as dist
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.backends.cudnn.benchmark = True
-    comm = NcclCommunicator(rank, world, max_ctas=args.nccl_max_ctas) if world > 1 else None
+        from paper_2103_07974_b200.comm import NcclCommunicator
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.local = dist_env()
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1 and not dist.is_initialized():
+            dist.init_process_group("gloo", rank=self.rank, world_size=self.world)
+        torch.backends.cudnn.benchmark = True
+        self.comm = NcclCommunicator(self.rank, self.world, max_ctas=nccl_max_ctas) if self.world > 1 else None
 
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = self.torch.tensor([x], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def close(self):
+        if self.comm is not None:
+            self.comm.close()
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
+              time_kernels: bool = True, sync_mode: str = "auto"):
+    """W untimed rotations, drain + barrier, then K timed rotations (CUDA events, max over ranks).
+
+    A rotation = every app in `base` steps once.  With `host_data` every step's batch is copied
+    H2D from pinned host memory and every loss is read back D2H (the e2e measurement).
+    """
+    import torch
+
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler
+
+    mode = sync_mode if h.world > 1 else "auto"
+    sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode)
+    for j, a in enumerate(base):
+        sched.register(dataclasses.replace(a, iterations=W + K,
+                                           data=host_data[j] if host_data else a.data))
+    loss_host = torch.zeros(len(base), dtype=torch.float32).pin_memory()
+    cs, ms = sched.compute_stream, sched.comm_stream
+
+    def one_rotation():
+        for j in range(len(base)):
+            sched.step()
+            if host_data:  # D2H of this step's result
+                with torch.cuda.stream(cs):
+                    loss_host[j:j + 1].copy_(sched.states[j].losses[-1].float().view(1), non_blocking=True)
+
+    for _ in range(W):
+        one_rotation()
+    sched.drain()
+    h.barrier()
+    if sched.timer is not None:
+        sched.timer.clear()
+    launches0 = sched.kernel_launches
+    n_spans0 = len(sched.recorder._pending)
+    clk = Clocks(h.local) if clocks else None
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(cs)
+    for _ in range(K):
+        one_rotation()
+    join = torch.cuda.Event()
+    join.record(ms)
+    cs.wait_event(join)
+    end.record(cs)
+    end.synchronize()
+    clk_info = clk.stop() if clk else None
+    ms_total = h.max_over_ranks(start.elapsed_time(end))
+    trace = sched.recorder.resolve()
+    sched.drain()
+    sched.close()
+    out = {"ms": ms_total, "trace": trace, "timed_spans": trace.spans[n_spans0:],
+           "kernels": sched.timer.summary() if sched.timer is not None else {},
+           "launches": sched.kernel_launches - launches0, "clocks": clk_info, "sched": sched}
+    return out
+
+
+def phase_medians(spans, order):
+    """Per-job median compute (fwd + bwd) and sync durations in ms."""
+    from paper_2103_07974_b200.engine import Phase
+
+    def med(job, phase):
+        vals = [s.end - s.start for s in spans if s.job_id == job and s.phase is phase]
+        return statistics.median(vals) / 1e6 if vals else 0.0
+
+    comp = [med(j, Phase.FORWARD) + med(j, Phase.BACKWARD) for j in order]
+    comm = [med(j, Phase.SYNC) for j in order]
+    return comp, comm
+
+
+def kernel_summary(kern: dict, sync) -> dict:
+    out = {}
+    if "k2_update" in kern:
+        t = statistics.mean(kern["k2_update"])
+        out["k2_update"] = {"ms": round(t, 4), "bytes": sync.k2_bytes(),
+                            "GB/s": round(sync.k2_bytes() / (t / 1e3) / 1e9, 1)}
+    if "k1_pack" in kern:
+        t = statistics.mean(kern["k1_pack"])
+        out["k1_pack"] = {"ms": round(t, 4), "bytes": sync.k1_bytes(),
+                          "GB/s": round(sync.k1_bytes() / (t / 1e3) / 1e9, 1)}
+    for name in ("c1_reduce_scatter", "c1_all_gather"):
+        if name in kern:
+            t = statistics.mean(kern[name])
+            out[name] = {"ms": round(t, 4), "bus_bytes": sync.c1_bus_bytes() / 2,
+                         "busbw_GB/s": round(sync.c1_bus_bytes() / 2 / (t / 1e3) / 1e9, 1)}
+    if "k2_p2p_fused" in kern:
+        t = statistics.mean(kern["k2_p2p_fused"])
+        nv = sync.c1_bus_bytes()
+        out["k2_p2p_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes(),
+                               "GB/s": round(sync.k2_bytes() / (t / 1e3) / 1e9, 1),
+                               "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
+    if "c1_allreduce" in kern:
+        t = statistics.mean(kern["c1_allreduce"])
+        out["c1_allreduce"] = {"ms": round(t, 4), "bus_bytes": sync.c1_bus_bytes(),
+                               "busbw_GB/s": round(sync.c1_bus_bytes() / (t / 1e3) / 1e9, 1),
+                               "peak_GB/s": 900.0}
+    return out
+
+
+def run_ours(args):
+    from paper_2103_07974_b200 import apps
+    from paper_2103_07974_b200.engine import schedule_key, trace_to_chrome_json, validate_trace
+    from paper_2103_07974_b200.scheduler import Policy, overlap_roofline, rotation_schedule
+
+    h = Harness(args.nccl_max_ctas)
+    rank, world, dev = h.rank, h.world, h.dev
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
+    flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False
     base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
-                  graphed=not args.no_graphs) for j in range(args.jobs)]
+                  graphed=not args.no_graphs, flat=flat) for j in range(args.jobs)]
     host_data = None if args.no_e2e else [
         apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + j, dev, host_uint8=True))
         for j in range(args.jobs)]
     samples_per_rot = args.jobs * args.batch * world
 
-    def timed(policy: Policy, e2e: bool, clocks: bool = False):
-        sched = CrossoverScheduler(policy, comm=comm, time_kernels=not e2e)
-        for j, a in enumerate(base):
-            app = dataclasses.replace(a, iterations=W + K,
-                                      data=host_data[j] if e2e else a.data)
-            sched.register(app)
-        loss_host = torch.zeros(len(base), dtype=torch.float32).pin_memory()
-        cs, ms = sched.compute_stream, sched.comm_stream
-
-        def one_rotation():
-            for j in range(len(base)):
-                sched.step()
-                if e2e:  # D2H of this step's result
-                    st = sched.states[j]
-                    with torch.cuda.stream(cs):
-                        loss_host[j:j + 1].copy_(st.losses[-1].float().view(1), non_blocking=True)
-
-        for _ in range(W):
-            one_rotation()
-        sched.drain()
-        barrier()
-        if sched.timer is not None:
-            sched.timer.clear()
-        launches0 = sched.kernel_launches
-        n_spans0 = len(sched.recorder._pending)
-        clk = Clocks(local) if clocks else None
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        start.record(cs)
-        for _ in range(K):
-            one_rotation()
-        join = torch.cuda.Event()
-        join.record(ms)
-        cs.wait_event(join)
-        end.record(cs)
-        end.synchronize()
-        clk_info = clk.stop() if clk else None
-        ms_total = max_over_ranks(start.elapsed_time(end))
-        launches = sched.kernel_launches - launches0
-        trace = sched.recorder.resolve()
-        timed_spans = trace.spans[n_spans0:]
-        kern = sched.timer.summary() if sched.timer is not None else {}
-        sched.drain()
-        return {"ms": ms_total, "trace": trace, "timed_spans": timed_spans, "kernels": kern,
-                "launches": launches, "clocks": clk_info, "sched": sched}
-
-    cross = timed(Policy.CROSSOVER, e2e=False, clocks=True)
-    seq = timed(Policy.SEQUENTIAL, e2e=False)
-    e2e = None if args.no_e2e else timed(Policy.CROSSOVER, e2e=True)
+    sm = args.sync_mode
+    cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm)
+    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm)
+    e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
+                                             time_kernels=False, sync_mode=sm)
 
     # legality + bit-exact schedule of the measured runs
     order = [a.job_id for a in base]
@@ -278,14 +350,7 @@ def run_ours(args):
         assert validate_trace(r["trace"]) == [], validate_trace(r["trace"])[:3]
         assert schedule_key(r["trace"]) == rotation_schedule(order, [W + K] * len(order))
 
-    def per_job(spans, job, phases):
-        vals = [s.end - s.start for s in spans if s.job_id == job and s.phase in phases]
-        return statistics.median(vals) / 1e6 if vals else 0.0
-
-    # per-job compute / sync medians of the sequential run (no overlap -> isolated costs)
-    comp = [per_job(seq["timed_spans"], j, (Phase.FORWARD,)) + per_job(seq["timed_spans"], j, (Phase.BACKWARD,))
-            for j in order]
-    comm_t = [per_job(seq["timed_spans"], j, (Phase.SYNC,)) for j in order]
+    comp, comm_t = phase_medians(seq["timed_spans"], order)
     roof = overlap_roofline(comp, comm_t)
     rot_cross = cross["ms"] / K
     rot_seq = seq["ms"] / K
@@ -294,19 +359,9 @@ def run_ours(args):
 
     hbm_peak, peak_kind = peaks()
     sync0 = cross["sched"].states[0].sync
-    k2_ms = statistics.mean(cross["kernels"].get("k2_update", [0.0]))
-    k2_bytes = sync0.k2_bytes()
-    k2_gbs = k2_bytes / (k2_ms / 1e3) / 1e9 if k2_ms else 0.0
-    kernels = {"k2_update": {"ms": round(k2_ms, 4), "bytes": k2_bytes, "GB/s": round(k2_gbs, 1)}}
-    if "k1_pack" in cross["kernels"]:
-        k1_ms = statistics.mean(cross["kernels"]["k1_pack"])
-        kernels["k1_pack"] = {"ms": round(k1_ms, 4), "bytes": sync0.k1_bytes(),
-                              "GB/s": round(sync0.k1_bytes() / (k1_ms / 1e3) / 1e9, 1)}
-    if "c1_allreduce" in cross["kernels"]:
-        c1_ms = statistics.mean(cross["kernels"]["c1_allreduce"])
-        kernels["c1_allreduce"] = {"ms": round(c1_ms, 4), "bus_bytes": sync0.c1_bus_bytes(),
-                                   "busbw_GB/s": round(sync0.c1_bus_bytes() / (c1_ms / 1e3) / 1e9, 1),
-                                   "peak_GB/s": 900.0}
+    kernels = kernel_summary(cross["kernels"], sync0)
+    kernels_isolated = kernel_summary(seq["kernels"], sync0)
+    k2_gbs = kernels.get("k2_update", kernels.get("k2_p2p_fused", {})).get("GB/s", 0.0)
 
     out = None
     if rank == 0:
@@ -345,10 +400,11 @@ def run_ours(args):
                                  "comp_ms": [round(c, 4) for c in comp],
                                  "comm_ms": [round(c, 4) for c in comm_t]},
             "roofline": {"kernel": "k2_update (fused 1/W average + SGD-momentum)", "bound": "hbm",
-                         "achieved": round(k2_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(k2_gbs / hbm_peak, 4), "traffic": None,
-                         "peak_kind": peak_kind, "bytes_per_launch": k2_bytes},
+                         "peak_kind": peak_kind, "bytes_per_launch": sync0.k2_bytes()},
             "kernels": kernels,
+            "kernels_isolated": kernels_isolated,
             "gpu_launches": cross["launches"],
             "clocks": cross["clocks"],
             "e2e": e2e_line,
@@ -356,10 +412,7 @@ def run_ours(args):
         }
         if args.trace_out:
             Path(args.trace_out).write_text(trace_to_chrome_json(cross["trace"]))
-    if comm is not None:
-        comm.close()
-    if world > 1:
-        dist.destroy_process_group()
+    h.close()
     if out is not None:
         print(json.dumps(out), flush=True)
 

@@ -131,6 +131,33 @@ CS_API size_t cs_gradient_stats_workspace_bytes(int64_t numel);
 CS_API int cs_gradient_stats(const float* data, int64_t numel, double* out,
                       void* workspace, void* stream);
 
+/* Collective-fused update over NVLink peer memory (replaces reduce-scatter + K2 +
+ * all-gather).  For this rank's shard of an app's flat parameters:
+ *   acc = 0 + src[0][k] + ... + src[W-1][k]   (rank order == equivalence.py:156-159)
+ *   p   = SGD(p, acc / W)                      (cs_sgd_hyper rules; momentum shard local)
+ *   dst[r][k] = p  for every rank r            (fused all-gather; remote NVLink stores)
+ * src[r] / dst[r] are rank r's bucket shard / flat-parameter shard as mapped in THIS
+ * process (cs_ipc_open_handle for peers).  The caller orders it between two barriers. */
+typedef struct cs_p2p_desc {
+  uint64_t src[CS_MAX_SOURCES];
+  uint64_t dst[CS_MAX_SOURCES];
+  float* param;          /* this rank's parameter shard (== dst[rank]) */
+  float* momentum_buf;   /* this rank's momentum shard, NULL when momentum == 0 */
+  int64_t numel;         /* shard length (fp32 elements) */
+  int32_t nranks;        /* W, 2..CS_MAX_SOURCES */
+  int32_t pad_;
+} cs_p2p_desc;
+CS_API int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* desc, const cs_sgd_hyper* hyper,
+                                   void* stream);
+
+/* IPC-capable device memory (cudaMalloc'd, zero-filled) and its peer mapping. */
+#define CS_IPC_HANDLE_BYTES 64
+CS_API int cs_device_alloc(size_t bytes, void** ptr);
+CS_API int cs_device_free(void* ptr);
+CS_API int cs_ipc_get_handle(void* ptr, uint8_t* out /* CS_IPC_HANDLE_BYTES */);
+CS_API int cs_ipc_open_handle(const uint8_t* handle, void** ptr);
+CS_API int cs_ipc_close_handle(void* ptr);
+
 /* NCCL communicator over NVLink / NVSwitch (one per process, one per job set).
  * min_ctas / max_ctas <= 0 leave NCCL's defaults. */
 CS_API int cs_nccl_version(void);

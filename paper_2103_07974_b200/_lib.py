@@ -37,6 +37,15 @@ class SgdHyper(ctypes.Structure):
                 ("divisor", ctypes.c_int32), ("rounding", ctypes.c_int32)]
 
 
+CS_IPC_HANDLE_BYTES = 64
+
+
+class P2PDesc(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_uint64 * CS_MAX_SOURCES), ("dst", ctypes.c_uint64 * CS_MAX_SOURCES),
+                ("param", ctypes.c_void_p), ("momentum_buf", ctypes.c_void_p),
+                ("numel", ctypes.c_int64), ("nranks", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
 class CrossoverLibError(RuntimeError):
     """A libcrossover.so call returned a non-zero status."""
 
@@ -58,6 +67,13 @@ EXPORTS = {
     "cs_gradient_stats_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "cs_gradient_stats": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p], ctypes.c_int),
+    "cs_p2p_reduce_sgd_bcast": ([ctypes.POINTER(P2PDesc), ctypes.POINTER(SgdHyper), ctypes.c_void_p],
+                                ctypes.c_int),
+    "cs_device_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cs_device_free": ([ctypes.c_void_p], ctypes.c_int),
+    "cs_ipc_get_handle": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "cs_ipc_open_handle": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cs_ipc_close_handle": ([ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_version": ([], ctypes.c_int),
     "cs_nccl_get_unique_id": ([ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_init": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int,

@@ -24,8 +24,24 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from .fusion import SgdSettings
+from .fusion import SgdSettings, flatten_parameters
 from .scheduler import App
+
+
+def _world() -> int:
+    import torch.distributed as dist
+
+    return dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+
+
+def _flatten(params, flat):
+    """flatten_parameters for the sharded / p2p sync (shards = world size); None when not asked.
+
+    ``flat`` is False, True (torch allocation, sharded NCCL sync) or "ipc" (cudaMalloc'd,
+    mappable by peers, p2p sync)."""
+    if not flat:
+        return None
+    return flatten_parameters(params, 32, _world(), ipc=(flat == "ipc"))[0]
 
 __all__ = [
     "LossKind",
@@ -43,6 +59,7 @@ __all__ = [
     "vgg16_app",
     "bert_app",
     "synthetic_image_batches",
+    "synthetic_app",
 ]
 
 
@@ -197,19 +214,20 @@ def _ce_loss(model, batch):
 
 def mlp_app(config: MlpConfig, job_id: str, rng_seed: int, iterations: int,
             device: torch.device, local_workers: int | None = None,
-            worker_count: int | None = None) -> App:
+            worker_count: int | None = None, flat: bool = False) -> App:
     """Config 1 app: two of these co-located, W = 2, batch 64 per worker."""
     x, y = make_mlp_dataset(config)
     workers = config.workers if worker_count is None else worker_count
     idx = _index_table(rng_seed, iterations, workers, config.dataset_size, config.batch_size)
     model = _mlp_module(config, mlp_initial_parameters(config, rng_seed)).to(device)
+    flat_params = _flatten(list(model.parameters()), flat)
     data = _GatherData(torch.as_tensor(x, dtype=torch.float32, device=device),
                        torch.as_tensor(y, dtype=torch.int64, device=device),
                        torch.as_tensor(idx, device=device))
     return App(job_id, model, _ce_loss, data,
                SgdSettings(config.learning_rate, momentum=config.momentum), iterations,
                local_workers=config.workers if local_workers is None else local_workers,
-               samples_per_batch=config.batch_size)
+               samples_per_batch=config.batch_size, flat_params=flat_params)
 
 
 # ---------------------------------------------------------------------------
@@ -282,17 +300,18 @@ class _GraphedImageModel(torch.nn.Module):
 
 def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
                device: torch.device, seed: int, host_data: bool, sgd: SgdSettings,
-               n_batches: int = 2, graphed: bool = False) -> App:
+               n_batches: int = 2, graphed: bool = False, flat: bool = False) -> App:
     model = model.to(device).to(memory_format=torch.channels_last)
     data = _CycleData(synthetic_image_batches(batch, n_batches, seed, device, host_uint8=host_data))
     params = [p for p in model.parameters() if p.requires_grad]
+    flat_params = _flatten(params, flat)          # before any graph captures the addresses
     if graphed:
         sample = torch.randn((batch, 3, 224, 224), device=device, dtype=torch.bfloat16
                              ).contiguous(memory_format=torch.channels_last)
         model = _GraphedImageModel(model, sample)
     return App(job_id, model, _image_loss, data, sgd, iterations, params=params,
                autocast_dtype=torch.bfloat16, samples_per_batch=batch,
-               autocast_cache=not graphed)
+               autocast_cache=not graphed, flat_params=flat_params)
 
 
 DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
@@ -300,22 +319,22 @@ DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
 
 def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
-                 graphed: bool = False) -> App:
+                 graphed: bool = False, flat: bool = False) -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed)
+                      host_data, sgd, graphed=graphed, flat=flat)
 
 
 def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
-              host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
-              graphed: bool = False) -> App:
+                 host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
+                 graphed: bool = False, flat: bool = False) -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed)
+                      host_data, sgd, graphed=graphed, flat=flat)
 
 
 def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,
@@ -345,3 +364,42 @@ def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: tor
 
     return App(job_id, wrap, loss_fn, _CycleData([(ids, labels)]), sgd, iterations,
                autocast_dtype=torch.bfloat16, samples_per_batch=batch)
+
+
+# ---------------------------------------------------------------------------
+# config 4: synthetic bucket of S bytes vs a fixed compute kernel
+# ---------------------------------------------------------------------------
+class _SyntheticModel(torch.nn.Module):
+    def __init__(self, numels: list[int], seed: int, device):
+        super().__init__()
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        self.weights = torch.nn.ParameterList(
+            [torch.nn.Parameter((torch.randn(n, generator=g) * 0.01).to(device)) for n in numels])
+        self.coef = [torch.randn(n, generator=g).to(device) for n in numels]
+
+
+def synthetic_app(job_id: str, bucket_bytes: int, iterations: int, device: torch.device,
+                  gemm_n: int = 8192, gemm_reps: int = 3, n_tensors: int = 16, seed: int = 0,
+                  sgd: SgdSettings = SgdSettings(lr=1e-3), flat: bool = False) -> App:
+    """An app whose compute is a fixed bf16 GEMM chain (gemm_reps x [n,n]@[n,n]) and whose
+    fused gradient is `bucket_bytes` of fp32 (mirrors cli._payload_for_ratio, cli.py:79-98:
+    the sweep dials the payload against a fixed compute time)."""
+    numel = max(bucket_bytes // 4, n_tensors)
+    sizes = [numel // n_tensors] * n_tensors
+    sizes[-1] += numel - sum(sizes)
+    model = _SyntheticModel(sizes, seed, device)
+    g = torch.Generator(device=device).manual_seed(seed)
+    a = torch.randn(gemm_n, gemm_n, device=device, dtype=torch.bfloat16, generator=g)
+    b = torch.randn(gemm_n, gemm_n, device=device, dtype=torch.bfloat16, generator=g) / gemm_n ** 0.5
+
+    def loss_fn(m, batch):
+        x = a
+        with torch.no_grad():
+            for _ in range(gemm_reps):
+                x = x @ b
+        s = sum((w * c).sum() for w, c in zip(m.weights, m.coef))
+        return s + x[0, 0].float() * 0.0
+
+    flat_params = _flatten(list(model.weights), flat)
+    return App(job_id, model, loss_fn, lambda t, w: (), sgd, iterations, samples_per_batch=1,
+               flat_params=flat_params)

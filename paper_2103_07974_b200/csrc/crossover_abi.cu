@@ -178,6 +178,64 @@ int cs_unpack_sgd(const cs_update_desc* descs, int n, const uint64_t* sources,
   return 0;
 }
 
+int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* d, const cs_sgd_hyper* h, void* stream) {
+  if (d == nullptr || h == nullptr) return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: NULL argument");
+  if (d->nranks < 1 || d->nranks > CS_MAX_SOURCES)
+    return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: nranks=%d outside [1, %d]", d->nranks,
+                     CS_MAX_SOURCES);
+  if (d->numel < 0 || (d->numel > 0 && d->param == nullptr))
+    return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: bad shard");
+  if (h->divisor != d->nranks)
+    return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: divisor %d != nranks %d", h->divisor, d->nranks);
+  if (!(h->lr > 0.0f)) return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: learning rate must be > 0");
+  if (h->rounding == CS_ROUND_REFERENCE && (h->momentum != 0.0f || h->weight_decay != 0.0f))
+    return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: reference rounding has no momentum / weight decay");
+  if (h->momentum != 0.0f && d->momentum_buf == nullptr)
+    return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: momentum buffer is NULL");
+  uintptr_t al = (uintptr_t)d->param | (uintptr_t)d->momentum_buf;
+  for (int r = 0; r < d->nranks; ++r) {
+    if (d->src[r] == 0 || d->dst[r] == 0)
+      return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: NULL peer address for rank %d", r);
+    al |= (uintptr_t)d->src[r] | (uintptr_t)d->dst[r];
+  }
+  if (al & 15u) return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: shards must be 16-byte aligned");
+  return cuda_status(launch_p2p(*d, *h, (cudaStream_t)stream), "cs_p2p_reduce_sgd_bcast launch");
+}
+
+int cs_device_alloc(size_t bytes, void** ptr) {
+  if (ptr == nullptr || bytes == 0) return set_error(CS_ERR_ARG, "cs_device_alloc: invalid arguments");
+  int rc = cuda_status(cudaMalloc(ptr, bytes), "cudaMalloc");
+  if (rc) return rc;
+  return cuda_status(cudaMemset(*ptr, 0, bytes), "cudaMemset");
+}
+
+int cs_device_free(void* ptr) {
+  if (ptr == nullptr) return 0;
+  return cuda_status(cudaFree(ptr), "cudaFree");
+}
+
+int cs_ipc_get_handle(void* ptr, uint8_t* out) {
+  if (ptr == nullptr || out == nullptr) return set_error(CS_ERR_ARG, "cs_ipc_get_handle: NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == CS_IPC_HANDLE_BYTES, "IPC handle size changed");
+  cudaIpcMemHandle_t h;
+  int rc = cuda_status(cudaIpcGetMemHandle(&h, ptr), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  std::memcpy(out, &h, sizeof(h));
+  return 0;
+}
+
+int cs_ipc_open_handle(const uint8_t* handle, void** ptr) {
+  if (ptr == nullptr || handle == nullptr) return set_error(CS_ERR_ARG, "cs_ipc_open_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int cs_ipc_close_handle(void* ptr) {
+  if (ptr == nullptr) return 0;
+  return cuda_status(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+}
+
 size_t cs_gradient_stats_workspace_bytes(int64_t numel) {
   return 256 + (size_t)stats_grid(numel) * 2 * sizeof(double);
 }

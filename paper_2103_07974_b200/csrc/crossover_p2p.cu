@@ -1,0 +1,125 @@
+// crossover_p2p.cu -- collective-fused update over NVLink peer memory.
+//
+// One kernel replaces reduce-scatter + K2 + all-gather.  Every rank owns one shard of the
+// app's flat parameter buffer.  For its shard it
+//   1. reads the shard of EVERY rank's bucket over NVLink (peer pointers opened with CUDA IPC)
+//      and sums them in rank order 0..W-1 -- the reference's left-to-right
+//      average_gradients order (equivalence.py:156-159), so the result is bit-identical to
+//      the fp32 oracle for any W (NCCL's ring order is not);
+//   2. divides by W and applies the SGD(-momentum) rule (same sgd_elem as K2);
+//   3. writes the new parameters into EVERY rank's flat buffer (local + W-1 remote stores),
+//      i.e. the all-gather is fused into the epilogue.
+// The host brackets the kernel with two stream-ordered NCCL barriers (all K1 packs done
+// before the first peer read; all peer writes done before any rank's next forward).
+// Memory: cs_device_alloc'd (cudaMalloc, IPC-capable) buffers only.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "crossover.h"
+#include "crossover_internal.h"
+#include "crossover_sgd.cuh"
+
+namespace cs {
+
+namespace {
+__device__ __forceinline__ float4 ld_peer(const float* p) {
+  // peer (NVLink) or local read-once data; L2-bypassed for peer apertures by the hardware
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+}  // namespace
+
+constexpr int kP2PUnroll = 2;
+constexpr int kP2PChunk = kThreads * 4 * kP2PUnroll;
+
+template <bool kMom>
+__global__ void __launch_bounds__(kThreads)
+p2p_reduce_sgd_bcast_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
+  const int64_t e0 = (int64_t)blockIdx.x * kP2PChunk;
+  const int64_t rem = d.numel - e0;
+  const int n = rem < kP2PChunk ? (int)rem : kP2PChunk;
+  const int tid = threadIdx.x;
+  const int W = d.nranks;
+  const Rule r = make_rule(h, kMom);
+  float* p = d.param + e0;
+  float* m = kMom ? d.momentum_buf + e0 : nullptr;
+  const int nvec = n >> 2;
+
+  float4 acc[kP2PUnroll], pv[kP2PUnroll], mv[kP2PUnroll];
+#pragma unroll
+  for (int u = 0; u < kP2PUnroll; ++u) {
+    const int idx = u * kThreads + tid;
+    acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mv[u] = acc[u];
+    pv[u] = acc[u];
+    if (idx < nvec) {
+      pv[u] = *(const float4*)(p + 4 * idx);
+      if (kMom) mv[u] = *(const float4*)(m + 4 * idx);
+    }
+  }
+  // all W x U peer loads in flight before the first add
+  float4 g[CS_MAX_SOURCES][kP2PUnroll];
+#pragma unroll
+  for (int s = 0; s < CS_MAX_SOURCES; ++s) {
+    if (s < W) {
+      const float* src = (const float*)d.src[s] + e0;
+#pragma unroll
+      for (int u = 0; u < kP2PUnroll; ++u) {
+        const int idx = u * kThreads + tid;
+        g[s][u] = idx < nvec ? ld_peer(src + 4 * idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < CS_MAX_SOURCES; ++s) {
+    if (s < W) {
+#pragma unroll
+      for (int u = 0; u < kP2PUnroll; ++u) {
+        acc[u].x = __fadd_rn(acc[u].x, g[s][u].x);
+        acc[u].y = __fadd_rn(acc[u].y, g[s][u].y);
+        acc[u].z = __fadd_rn(acc[u].z, g[s][u].z);
+        acc[u].w = __fadd_rn(acc[u].w, g[s][u].w);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kP2PUnroll; ++u) {
+    const int idx = u * kThreads + tid;
+    if (idx < nvec) {
+      float4 o;
+      o.x = sgd_elem(r, acc[u].x, pv[u].x, &mv[u].x);
+      o.y = sgd_elem(r, acc[u].y, pv[u].y, &mv[u].y);
+      o.z = sgd_elem(r, acc[u].z, pv[u].z, &mv[u].z);
+      o.w = sgd_elem(r, acc[u].w, pv[u].w, &mv[u].w);
+      if (kMom) st4(m + 4 * idx, mv[u]);
+      for (int s = 0; s < W; ++s) st4((float*)d.dst[s] + e0 + 4 * idx, o);   // fused all-gather
+    }
+  }
+  for (int k = 4 * nvec + tid; k < n; k += kThreads) {
+    float a = 0.0f;
+    for (int s = 0; s < W; ++s) a = __fadd_rn(a, ((const float*)d.src[s])[e0 + k]);
+    float b = kMom ? m[k] : 0.0f;
+    const float np = sgd_elem(r, a, p[k], &b);
+    if (kMom) m[k] = b;
+    for (int s = 0; s < W; ++s) ((float*)d.dst[s])[e0 + k] = np;
+  }
+  __threadfence_system();   // remote stores performed before the kernel retires
+}
+
+cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
+  if (d.numel == 0) return cudaSuccess;
+  const int64_t grid = (d.numel + kP2PChunk - 1) / kP2PChunk;
+  if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+  else p2p_reduce_sgd_bcast_kernel<false><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+  return cudaGetLastError();
+}
+
+}  // namespace cs

@@ -21,6 +21,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Sequence
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -29,7 +31,36 @@ from .comm import NcclCommunicator
 from .errors import ConfigError
 from .workload import BucketLayout
 
-__all__ = ["SgdSettings", "FusedGradientSync"]
+__all__ = ["SgdSettings", "FusedGradientSync", "flatten_parameters"]
+
+
+def flatten_parameters(params: Sequence[torch.Tensor], align: int = 32, shards: int = 1,
+                       ipc: bool = False):
+    """Move every parameter into one contiguous fp32 buffer laid out like the bucket.
+
+    Each parameter keeps its shape and strides (channels_last stays channels_last) but
+    its storage becomes a view of ``flat`` at ``layout.offsets[i]``; the total is padded
+    to ``align * shards`` so the buffer splits into equal aligned shards.  This is what
+    lets the sharded sync all-gather updated shards straight into the model's weights.
+    Call it before anything captures parameter addresses (CUDA graphs).  ``ipc=True``
+    allocates the buffer with cs_device_alloc so peers can map it (p2p sync mode).
+    """
+    lay = BucketLayout.build([p.numel() for p in params], align, multiple=align * shards)
+    dev = params[0].device
+    if ipc:
+        from .p2p import DeviceBuffer
+
+        flat = DeviceBuffer(lay.total, dev).tensor
+    else:
+        flat = torch.zeros(lay.total, dtype=torch.float32, device=dev)
+    with torch.no_grad():
+        for p, off in zip(params, lay.offsets):
+            if p.dtype != torch.float32 or not _dense(p):
+                raise ConfigError("flat parameters need dense fp32 tensors")
+            view = torch.as_strided(flat, p.shape, p.stride(), off)
+            view.copy_(p.data)
+            p.data = view
+    return flat, lay
 
 
 @dataclass(frozen=True)
@@ -73,7 +104,8 @@ class FusedGradientSync:
 
     def __init__(self, params: Sequence[torch.Tensor], settings: SgdSettings,
                  comm: NcclCommunicator | None = None, local_workers: int = 1,
-                 align: int = 32, mode: str = "auto", snapshot_rows: int = 0):
+                 align: int = 32, mode: str = "auto", snapshot_rows: int = 0,
+                 flat_params: torch.Tensor | None = None):
         if not params:
             raise ConfigError("an app needs at least one trainable parameter")
         dev = params[0].device
@@ -93,23 +125,54 @@ class FusedGradientSync:
             raise ConfigError("simulated local workers are only supported at world size 1")
         self.workers = self.ranks * self.local_workers
         if mode == "auto":
-            mode = "direct" if self.workers == 1 else "bucket"
-        if mode not in ("bucket", "direct"):
+            if self.workers == 1:
+                mode = "direct"
+            else:
+                mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
+        if mode not in ("bucket", "direct", "sharded", "p2p"):
             raise ConfigError(f"unknown sync mode {mode!r}")
         if mode == "direct" and self.workers != 1:
             raise ConfigError("direct mode has no bucket and needs exactly one worker")
+        if mode in ("sharded", "p2p") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
+            raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
+                              "and one worker per rank")
         self.mode = mode
-        self.layout = BucketLayout.build([p.numel() for p in self.params], align)
+        self.flat = flat_params
+        sharded = mode in ("sharded", "p2p")
+        multiple = align * self.ranks if sharded else None
+        self.layout = BucketLayout.build([p.numel() for p in self.params], align, multiple=multiple)
+        if sharded:
+            if flat_params.numel() != self.layout.total or flat_params.dtype != torch.float32:
+                raise ConfigError("flat parameter buffer does not match the sharded layout")
+            base = flat_params.data_ptr()
+            for p, off in zip(self.params, self.layout.offsets):
+                if p.data_ptr() != base + 4 * off:
+                    raise ConfigError("parameters are not views of the flat buffer at the layout offsets")
         n = len(self.params)
         lay = self.layout
         row_bytes = lay.bucket_bytes
 
         self.bucket = None
-        if mode == "bucket":
+        self._peer_maps = []
+        if mode == "p2p":
+            from .p2p import DeviceBuffer, buffer_of
+
+            if self.ranks > _lib.CS_MAX_SOURCES:
+                raise ConfigError(f"p2p sync supports up to {_lib.CS_MAX_SOURCES} ranks")
+            if buffer_of(flat_params) is None:
+                raise ConfigError("p2p sync needs IPC-capable flat parameters (flatten_parameters(ipc=True))")
+            self._bucket_buf = DeviceBuffer(lay.total, dev)
+            self.bucket = self._bucket_buf.tensor
+        elif mode in ("bucket", "sharded"):
             self.bucket = torch.zeros(self.local_workers * lay.total, dtype=torch.float32, device=dev)
         self.momentum_bufs = None
+        self.shard = lay.total // self.ranks
+        self.rank = comm.rank if comm is not None else 0
         if settings.momentum != 0:
-            self.momentum_bufs = [torch.zeros_like(p) for p in self.params]
+            if sharded:   # momentum only for this rank's shard: S / W per GPU
+                self.momentum_bufs = [torch.zeros(self.shard, dtype=torch.float32, device=dev)]
+            else:
+                self.momentum_bufs = [torch.zeros_like(p) for p in self.params]
         self.first_step = True
         self.snapshot = None
         if snapshot_rows:
@@ -126,6 +189,37 @@ class FusedGradientSync:
                 sl["dst"] = base + w * row_bytes + offs_bytes
                 sl["numel"] = numels
         # K2 descriptors: fixed except grad_offset in direct mode
+        if mode == "p2p":
+            from .p2p import buffer_of, exchange_peer_addresses
+
+            off = self.rank * self.shard * 4
+            bmap = exchange_peer_addresses(self._bucket_buf, self.rank, self.ranks)
+            fmap = exchange_peer_addresses(buffer_of(flat_params), self.rank, self.ranks)
+            self._peer_maps = [bmap, fmap]
+            self._p2p = _lib.P2PDesc()
+            for r in range(self.ranks):
+                self._p2p.src[r] = bmap.addresses[r] + off
+                self._p2p.dst[r] = fmap.addresses[r] + off
+            self._p2p.param = flat_params.data_ptr() + off
+            self._p2p.momentum_buf = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else None
+            self._p2p.numel = self.shard
+            self._p2p.nranks = self.ranks
+            self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
+            self._finish_init(settings)
+            return
+        if mode == "sharded":
+            # one flat range: this rank's shard of the parameters, bucket and momentum
+            off = self.rank * self.shard * 4
+            self._upd = np.zeros(1, dtype=_lib.UPDATE_DESC)
+            self._upd["param"] = flat_params.data_ptr() + off
+            if self.momentum_bufs is not None:
+                self._upd["momentum_buf"] = self.momentum_bufs[0].data_ptr()
+            self._upd["grad_offset"] = off
+            self._upd["snap_offset"] = off
+            self._upd["numel"] = self.shard
+            self._sources = np.asarray([self.bucket.data_ptr()], dtype=np.uint64)
+            self._finish_init(settings)
+            return
         self._upd = np.zeros(n, dtype=_lib.UPDATE_DESC)
         self._upd["param"] = [p.data_ptr() for p in self.params]
         if self.momentum_bufs is not None:
@@ -138,6 +232,9 @@ class FusedGradientSync:
                                         for w in range(self.local_workers)], dtype=np.uint64)
         else:
             self._sources = np.zeros(1, dtype=np.uint64)
+        self._finish_init(settings)
+
+    def _finish_init(self, settings: SgdSettings) -> None:
         self._hyper = _lib.SgdHyper(
             lr=settings.lr, momentum=settings.momentum,
             dampening_complement=float(1.0 - settings.dampening),
@@ -149,7 +246,7 @@ class FusedGradientSync:
     # -- per-iteration pieces (all asynchronous on `stream`) -----------------
     def pack(self, grads_per_worker: Sequence[Sequence[torch.Tensor]], stream: int) -> None:
         """K1: gather each worker's gradients into its bucket row."""
-        if self.mode != "bucket":
+        if self.mode not in ("bucket", "sharded"):
             raise ConfigError("pack() needs bucket mode")
         n = len(self.params)
         if len(grads_per_worker) != self.local_workers:
@@ -172,7 +269,7 @@ class FusedGradientSync:
                 raise ValueError("direct mode needs the gradient tensors")
             self._upd["grad_offset"] = _grad_ptrs(grads, self.params)
         snap = 0
-        if snapshot_row is not None:
+        if snapshot_row is not None and self.mode != "sharded":
             if self.snapshot is None:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
             snap = self.snapshot[snapshot_row].data_ptr()
@@ -196,6 +293,12 @@ class FusedGradientSync:
         self.pack(grads_per_worker, stream)
         if timer is not None:
             timer.end("k1_pack")
+        if self.mode == "sharded":
+            self._sharded_tail(stream, snapshot_row, timer)
+            return
+        if self.mode == "p2p":
+            self._p2p_tail(stream, snapshot_row, timer)
+            return
         if self.comm is not None and self.comm.active:
             if timer is not None:
                 timer.begin("c1_allreduce")
@@ -208,11 +311,65 @@ class FusedGradientSync:
         if timer is not None:
             timer.end("k2_update")
 
+    def _sharded_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
+        """reduce-scatter -> K2 on this rank's shard -> all-gather into the flat parameters."""
+        shard_bytes = self.shard * 4
+        b = self.bucket.data_ptr()
+        if timer is not None:
+            timer.begin("c1_reduce_scatter")
+        self.comm.reduce_scatter(b, b + self.rank * shard_bytes, self.shard, stream)
+        if timer is not None:
+            timer.end("c1_reduce_scatter")
+            timer.begin("k2_update")
+        self.update(stream, None, None)
+        if timer is not None:
+            timer.end("k2_update")
+            timer.begin("c1_all_gather")
+        f = self.flat.data_ptr()
+        self.comm.all_gather(f + self.rank * shard_bytes, f, self.shard, stream)
+        if timer is not None:
+            timer.end("c1_all_gather")
+        if snapshot_row is not None:
+            if self.snapshot is None:
+                raise ConfigError("no snapshot buffer (snapshot_rows=0)")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.snapshot[snapshot_row].copy_(self.flat)
+
+    def _p2p_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
+        """barrier -> fused reduce + update + all-gather over NVLink -> barrier."""
+        bar = self._barrier.data_ptr()
+        self.comm.all_reduce_(bar, 1, stream)          # every rank's K1 has landed
+        if timer is not None:
+            timer.begin("k2_p2p_fused")
+        self._hyper.first_step = int(self.first_step)
+        _lib.check("cs_p2p_reduce_sgd_bcast", _lib.lib.cs_p2p_reduce_sgd_bcast(
+            ctypes.byref(self._p2p), ctypes.byref(self._hyper), stream))
+        self.first_step = False
+        self.kernel_launches += 1
+        if timer is not None:
+            timer.end("k2_p2p_fused")
+        self.comm.all_reduce_(bar, 1, stream)          # every rank's parameter writes landed
+        if snapshot_row is not None:
+            if self.snapshot is None:
+                raise ConfigError("no snapshot buffer (snapshot_rows=0)")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.snapshot[snapshot_row].copy_(self.flat)
+
+    def close(self) -> None:
+        for m in self._peer_maps:
+            m.close()
+        self._peer_maps = []
+
     # -- algorithmic bytes per launch (SURVEY §8d) ---------------------------
     def k1_bytes(self) -> int:
         return 2 * self.local_workers * self.layout.payload_bytes
 
     def k2_bytes(self) -> int:
+        if self.mode == "p2p":
+            # W source shards + p read + W destination shards (+ momentum read/write)
+            return (2 * self.ranks + 1 + (2 if self.settings.momentum else 0)) * self.shard * 4
+        if self.mode == "sharded":
+            return (5 if self.settings.momentum else 3) * self.shard * 4
         s = self.layout.payload_bytes
         streams = self.local_workers if self.mode == "bucket" else 1
         per = (streams + 2) * s            # read sources + read p + write p
@@ -221,6 +378,7 @@ class FusedGradientSync:
         return per
 
     def c1_bus_bytes(self) -> float:
+        """All-reduce bus bytes 2(W-1)/W * S (== reduce-scatter + all-gather in sharded mode)."""
         w = self.ranks
         return 0.0 if w <= 1 else 2.0 * (w - 1) / w * self.layout.bucket_bytes
 

@@ -87,6 +87,7 @@ class App:
     params: list[torch.Tensor] | None = None
     samples_per_batch: int = 0   # for samples/s accounting (per worker)
     autocast_cache: bool = True  # must be False when the model replays CUDA graphs
+    flat_params: torch.Tensor | None = None   # set by fusion.flatten_parameters (sharded sync)
 
     def __post_init__(self):
         if self.iterations < 1:
@@ -241,7 +242,8 @@ class CrossoverScheduler:
             if p.device != self.device:
                 raise ConfigError(f"job {app.job_id!r}: parameters must be on {self.device}")
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
-                                 self.sync_mode, app.iterations if self.record_weights else 0)
+                                 self.sync_mode, app.iterations if self.record_weights else 0,
+                                 flat_params=app.flat_params)
         st = JobRuntimeState(app.job_id, app=app, sync=sync)
         self.states.append(st)
         return st
@@ -378,6 +380,11 @@ class CrossoverScheduler:
         if st.sync.snapshot is None:
             raise ConfigError("record_weights=False")
         return st.sync.snapshot
+
+    def close(self) -> None:
+        """Release peer mappings (p2p sync); call after the last drain()."""
+        for st in self.states:
+            st.sync.close()
 
     @property
     def kernel_launches(self) -> int:

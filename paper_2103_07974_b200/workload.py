@@ -127,7 +127,9 @@ class BucketLayout:
     align: int
 
     @staticmethod
-    def build(numels: Sequence[int], align: int = 32) -> "BucketLayout":
+    def build(numels: Sequence[int], align: int = 32, multiple: int | None = None) -> "BucketLayout":
+        """``multiple`` pads the total length (default ``align``), e.g. to align * W so the
+        bucket splits into W equal, aligned shards for reduce-scatter / sharded updates."""
         if align < 1:
             raise ValueError("align must be >= 1")
         if not numels:
@@ -140,7 +142,10 @@ class BucketLayout:
             cur = -(-cur // align) * align
             offs.append(cur)
             cur += int(n)
-        total = -(-cur // align) * align
+        mult = align if multiple is None else int(multiple)
+        if mult < 1 or mult % align:
+            raise ValueError("multiple must be a positive multiple of align")
+        total = -(-cur // mult) * mult
         return BucketLayout(tuple(int(n) for n in numels), tuple(offs), total, align)
 
     @property

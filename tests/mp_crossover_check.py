@@ -62,6 +62,41 @@ def main():
     s2.run()
     lin = [s2.weights(f"lin{k}")[:, :8].cpu().numpy().astype(np.float64) for k in range(2)]
 
+    # (3) sharded sync (reduce-scatter -> shard K2 -> all-gather into flat params) vs the
+    #     all-reduce bucket path, both with momentum: bitwise at W = 2, tolerance otherwise
+    mom_w = {}
+    for mode, flat in (("bucket", False), ("sharded", True)):
+        s4 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode=mode)
+        for k, (ds, rs) in enumerate(specs):
+            s4.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T,
+                                dev, local_workers=1, worker_count=world, flat=flat))
+        s4.run()
+        mom_w[mode] = [s4.weights(f"m{k}").cpu() for k in range(2)]
+        if mode == "sharded":
+            res["checks"].append({"name": "sharded_mode_used",
+                                  "ok": all(st.sync.mode == "sharded" for st in s4.states)})
+    n = mom_w["bucket"][0].shape[1]
+    if world == 2:
+        same = all(torch.equal(mom_w["bucket"][k], mom_w["sharded"][k][:, :n]) for k in range(2))
+        res["checks"].append({"name": "sharded_bitwise_eq_allreduce_w2", "ok": bool(same)})
+    else:
+        d = max(float((mom_w["bucket"][k] - mom_w["sharded"][k][:, :n]).abs().max()) for k in range(2))
+        res["checks"].append({"name": "sharded_close_to_allreduce", "ok": d < 1e-5, "max_abs": d})
+
+    # (4) collective-fused P2P sync (one kernel: NVLink reads of every rank's bucket shard in
+    #     rank order, / W, SGD-momentum, NVLink writes of the new shard to every rank)
+    s5 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode="p2p")
+    for k, (ds, rs) in enumerate(specs):
+        s5.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T,
+                            dev, local_workers=1, worker_count=world, flat="ipc"))
+    s5.run()
+    p2p_w = [s5.weights(f"m{k}").cpu() for k in range(2)]
+    s5.close()
+    res["checks"].append({"name": "p2p_mode_used", "ok": all(st.sync.mode == "p2p" for st in s5.states)})
+    if world == 2:
+        same = all(torch.equal(mom_w["bucket"][k], p2p_w[k][:, :n]) for k in range(2))
+        res["checks"].append({"name": "p2p_bitwise_eq_allreduce_w2", "ok": bool(same)})
+
     # every rank must hold identical weights after every iteration
     for k in range(2):
         gathered = [torch.empty_like(w_ranks[k]) for _ in range(world)] if rank == 0 else None
@@ -91,6 +126,15 @@ def main():
             r = np.stack(lref[k])
             lw = max(lw, float(np.max(np.abs(lin[k] - r) / (1e-5 + 1e-4 * np.abs(r)))))
         res["checks"].append({"name": "linear_vs_oracle", "ok": lw <= 1.0, "worst_ratio": lw})
+
+        # the P2P path sums in rank order 0..W-1 exactly like K2 over W simulated workers
+        # on one GPU (and like the reference's average_gradients): bitwise for ANY W
+        s6 = CrossoverScheduler(Policy.CROSSOVER, record_weights=True)
+        for k, (ds, rs) in enumerate(specs):
+            s6.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T, dev))
+        s6.run()
+        same = all(torch.equal(s6.weights(f"m{k}").cpu(), p2p_w[k][:, :n]) for k in range(2))
+        res["checks"].append({"name": f"p2p_w{world}_bitwise_eq_simulated_w{world}", "ok": bool(same)})
 
         if world == 2:
             # single-GPU run with 2 simulated workers, reduced left to right by K2

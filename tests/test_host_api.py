@@ -171,3 +171,30 @@ def test_chrome_and_json_exports(schedule_golden):
                        "start_ns": 0, "end_ns": 1}
     assert engine.schedule_key(tr)[:3] == [("gpu0", "j1", "forward", 1), ("gpu0", "j1", "backward", 1),
                                            ("nic0", "j1", "sync", 1)]
+
+
+def test_bucket_layout_multiple_for_shards():
+    lay = workload.BucketLayout.build([10, 33, 7], 32, multiple=32 * 4)
+    assert lay.total % 128 == 0 and lay.total >= lay.offsets[-1] + 7
+    with pytest.raises(ValueError):
+        workload.BucketLayout.build([1], 32, multiple=48)
+
+
+def test_flatten_parameters_keeps_values_and_strides():
+    import torch
+
+    from paper_2103_07974_b200.fusion import flatten_parameters
+
+    torch.manual_seed(0)
+    conv = torch.nn.Conv2d(3, 8, 3).to(memory_format=torch.channels_last)
+    lin = torch.nn.Linear(5, 3)
+    params = list(conv.parameters()) + list(lin.parameters())
+    before = [p.detach().clone() for p in params]
+    strides = [p.stride() for p in params]
+    flat, lay = flatten_parameters(params, 32, shards=4)
+    assert flat.numel() == lay.total and lay.total % 128 == 0
+    for p, b, st, off in zip(params, before, strides, lay.offsets):
+        assert torch.equal(p, b) and p.stride() == st
+        assert p.data_ptr() == flat.data_ptr() + 4 * off
+    y = conv(torch.randn(1, 3, 6, 6).contiguous(memory_format=torch.channels_last))
+    assert y.shape == (1, 8, 4, 4)
