@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--gemm-reps", type=int, default=3)
     ap.add_argument("--out", default="")
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"])
     args = ap.parse_args()
     from paper_2103_07974_b200.apps import synthetic_app
     from paper_2103_07974_b200.scheduler import Policy, overlap_roofline
@@ -31,15 +32,17 @@ def main():
     h = Harness()
     rows = []
     for mb in [int(x) for x in args.sizes_mb.split(",")]:
-        base = [synthetic_app(f"syn{j}", mb * 2**20, 1, h.dev, gemm_reps=args.gemm_reps, seed=j)
-                for j in range(2)]
-        cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps)
-        seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps)
+        flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if h.world > 1 else False
+        base = [synthetic_app(f"syn{j}", mb * 2**20, 1, h.dev, gemm_reps=args.gemm_reps, seed=j,
+                              flat=flat) for j in range(2)]
+        cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=args.sync_mode)
+        seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=args.sync_mode)
         comp, comm = phase_medians(seq["timed_spans"], [a.job_id for a in base])
         rho = sum(comm) / sum(comp)
         roof = overlap_roofline(comp, comm)
         rot_x, rot_s = cross["ms"] / args.steps, seq["ms"] / args.steps
-        row = {"bucket_MB": mb, "world": h.world, "rho": round(rho, 4),
+        row = {"bucket_MB": mb, "world": h.world, "sync_mode": cross["sched"].states[0].sync.mode,
+               "rho": round(rho, 4),
                "speedup": round(rot_s / rot_x, 4),
                "predicted": round((1 + rho) / max(1.0, rho), 4),
                "rotation_ms": {"crossover": round(rot_x, 4), "sequential": round(rot_s, 4)},
