@@ -246,7 +246,7 @@ class FusedGradientSync:
     # -- per-iteration pieces (all asynchronous on `stream`) -----------------
     def pack(self, grads_per_worker: Sequence[Sequence[torch.Tensor]], stream: int) -> None:
         """K1: gather each worker's gradients into its bucket row."""
-        if self.mode not in ("bucket", "sharded"):
+        if self.mode not in ("bucket", "sharded", "p2p"):
             raise ConfigError("pack() needs bucket mode")
         n = len(self.params)
         if len(grads_per_worker) != self.local_workers:
