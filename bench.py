@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
+    ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"],
@@ -328,6 +329,9 @@ def run_ours(args):
 
     h = Harness(args.nccl_max_ctas)
     rank, world, dev = h.rank, h.world, h.dev
+    if args.p2p_ctas:
+        from paper_2103_07974_b200 import _lib
+        _lib.tune("p2p_ctas", args.p2p_ctas)
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
     flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False

@@ -21,6 +21,8 @@
 
 namespace cs {
 
+int g_tune_p2p_ctas = 0;
+
 namespace {
 __device__ __forceinline__ float4 ld_peer(const float* p) {
   // peer (NVLink) or local read-once data; L2-bypassed for peer apertures by the hardware
@@ -41,14 +43,25 @@ constexpr int kP2PUnroll = 2;
 constexpr int kP2PChunk = kThreads * 4 * kP2PUnroll;
 
 template <bool kMom>
+__device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0);
+
+// Persistent when the grid is capped (cs_tune "p2p_ctas"): a comm kernel that overlaps another
+// app's compute should hold as few SMs as keep NVLink busy; each CTA walks chunks with stride.
+template <bool kMom>
 __global__ void __launch_bounds__(kThreads)
 p2p_reduce_sgd_bcast_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
-  const int64_t e0 = (int64_t)blockIdx.x * kP2PChunk;
+  const Rule r = make_rule(h, kMom);
+  const int64_t chunks = (d.numel + kP2PChunk - 1) / kP2PChunk;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) p2p_chunk<kMom>(d, r, c * kP2PChunk);
+  __threadfence_system();   // remote stores performed before the kernel retires
+}
+
+template <bool kMom>
+__device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0) {
   const int64_t rem = d.numel - e0;
   const int n = rem < kP2PChunk ? (int)rem : kP2PChunk;
   const int tid = threadIdx.x;
   const int W = d.nranks;
-  const Rule r = make_rule(h, kMom);
   float* p = d.param + e0;
   float* m = kMom ? d.momentum_buf + e0 : nullptr;
   const int nvec = n >> 2;
@@ -111,12 +124,12 @@ p2p_reduce_sgd_bcast_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_
     if (kMom) m[k] = b;
     for (int s = 0; s < W; ++s) ((float*)d.dst[s])[e0 + k] = np;
   }
-  __threadfence_system();   // remote stores performed before the kernel retires
 }
 
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
-  const int64_t grid = (d.numel + kP2PChunk - 1) / kP2PChunk;
+  int64_t grid = (d.numel + kP2PChunk - 1) / kP2PChunk;
+  if (g_tune_p2p_ctas > 0 && grid > g_tune_p2p_ctas) grid = g_tune_p2p_ctas;
   if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
   else p2p_reduce_sgd_bcast_kernel<false><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
   return cudaGetLastError();

@@ -146,6 +146,7 @@ def main():
             res["checks"].append({"name": "nccl_w2_bitwise_eq_simulated_w2", "ok": bool(same)})
         res["ok"] = all(c["ok"] for c in res["checks"])
         Path(out_path).write_text(json.dumps(res, indent=1))
+        print("MPCHECK " + json.dumps(res), flush=True)
     comm.close()
     dist.barrier()
     dist.destroy_process_group()

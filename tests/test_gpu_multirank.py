@@ -21,6 +21,7 @@ def test_multirank_crossover_parity(tmp_path, world):
            "--master-addr=127.0.0.1", f"--master-port={29600 + world}",
            str(ROOT / "tests" / "mp_crossover_check.py"), str(out)]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    checks = [ln for ln in proc.stdout.splitlines() if ln.startswith("MPCHECK ")]
+    assert proc.returncode == 0, (checks or [proc.stdout[-3000:]])[-1] + proc.stderr[-3000:]
     res = json.loads(out.read_text())
     assert res["ok"], res

@@ -25,11 +25,16 @@ def main():
     ap.add_argument("--gemm-reps", type=int, default=3)
     ap.add_argument("--out", default="")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"])
+    ap.add_argument("--p2p-ctas", type=int, default=0)
+    ap.add_argument("--nccl-max-ctas", type=int, default=0)
     args = ap.parse_args()
     from paper_2103_07974_b200.apps import synthetic_app
     from paper_2103_07974_b200.scheduler import Policy, overlap_roofline
 
-    h = Harness()
+    h = Harness(args.nccl_max_ctas)
+    if args.p2p_ctas:
+        from paper_2103_07974_b200 import _lib
+        _lib.tune("p2p_ctas", args.p2p_ctas)
     rows = []
     for mb in [int(x) for x in args.sizes_mb.split(",")]:
         flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if h.world > 1 else False
@@ -42,6 +47,7 @@ def main():
         roof = overlap_roofline(comp, comm)
         rot_x, rot_s = cross["ms"] / args.steps, seq["ms"] / args.steps
         row = {"bucket_MB": mb, "world": h.world, "sync_mode": cross["sched"].states[0].sync.mode,
+               "p2p_ctas": args.p2p_ctas, "nccl_max_ctas": args.nccl_max_ctas,
                "rho": round(rho, 4),
                "speedup": round(rot_s / rot_x, 4),
                "predicted": round((1 + rho) / max(1.0, rho), 4),
