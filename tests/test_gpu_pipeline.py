@@ -193,3 +193,18 @@ def test_resnet50_graphed_two_jobs(cuda_device):
     assert validate_trace(tr) == []
     assert all(torch.isfinite(l).all() for st in s.states for l in st.losses)
     assert not torch.equal(before, s.states[1].app.params[0])
+
+
+def test_mixed_models_bert_vgg(cuda_device):
+    """Config 5 shape: heterogeneous apps (VGG-16, BERT-base) co-located on one GPU."""
+    from paper_2103_07974_b200.apps import bert_app, vgg16_app
+    from paper_2103_07974_b200.engine import validate_trace
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
+
+    s = CrossoverScheduler(Policy.CROSSOVER)
+    s.register(vgg16_app("vgg", 4, 2, cuda_device))
+    s.register(bert_app("bert", 2, 32, 2, cuda_device))
+    tr = s.run()
+    assert validate_trace(tr) == []
+    assert [st.sync.layout.payload_bytes for st in s.states][0] == 553_430_176
+    assert all(torch.isfinite(l).all() for st in s.states for l in st.losses)
