@@ -160,13 +160,16 @@ def mlp_gradient(params, x, y):
 
 
 def run_mlp_crossover(job_specs, iterations: int, workers: int, batch: int = 64, lr: float = 0.05,
-                      dataset_size: int = 4096):
-    """job_specs: [(dataset_seed, rng_seed)]; returns per-job lists of per-iteration params."""
+                      dataset_size: int = 4096, momentum: float = 0.0):
+    """job_specs: [(dataset_seed, rng_seed)]; returns per-job lists of per-iteration params.
+
+    momentum > 0 applies torch.optim.SGD's momentum rule (torch_sgd_step) in fp64."""
     jobs = []
     for ds, rs in job_specs:
         x, y = mlp_dataset(ds, dataset_size)
         jobs.append((x, y, rs, mlp_init(rs)))
     params = [j[3] for j in jobs]
+    bufs = [[None] * 4 for _ in jobs]
     traj = [[] for _ in jobs]
     for t in range(1, iterations + 1):       # isolated == crossover order (neutrality)
         for k, (x, y, rs, _) in enumerate(jobs):
@@ -175,7 +178,15 @@ def run_mlp_crossover(job_specs, iterations: int, workers: int, batch: int = 64,
                 idx = batch_indices(rs, t, w, dataset_size, batch)
                 grads.append(mlp_gradient(params[k], x[idx], y[idx]))
             avg = [average_gradients([g[i] for g in grads]) for i in range(4)]
-            params[k] = [sgd_step(p, a, lr) for p, a in zip(params[k], avg)]
+            if momentum:
+                new = []
+                for i, (p, a) in enumerate(zip(params[k], avg)):
+                    q, bufs[k][i] = torch_sgd_step(p, a, bufs[k][i], lr, momentum=momentum,
+                                                   first=t == 1)
+                    new.append(q)
+                params[k] = new
+            else:
+                params[k] = [sgd_step(p, a, lr) for p, a in zip(params[k], avg)]
             traj[k].append(params[k])
     return traj
 

@@ -76,6 +76,7 @@ def main():
             res["checks"].append({"name": "sharded_mode_used",
                                   "ok": all(st.sync.mode == "sharded" for st in s4.states)})
     n = mom_w["bucket"][0].shape[1]
+    mom_ref = osgd.run_mlp_crossover(specs, T, workers=world, momentum=0.9) if rank == 0 else None
     if world == 2:
         same = all(torch.equal(mom_w["bucket"][k], mom_w["sharded"][k][:, :n]) for k in range(2))
         res["checks"].append({"name": "sharded_bitwise_eq_allreduce_w2", "ok": bool(same)})
@@ -137,6 +138,24 @@ def main():
         s6.run()
         same = all(torch.equal(s6.weights(f"m{k}").cpu(), p2p_w[k][:, :n]) for k in range(2))
         res["checks"].append({"name": f"p2p_w{world}_bitwise_eq_simulated_w{world}", "ok": bool(same)})
+
+        # every sync mode vs the fp64 oracle with torch-SGD momentum
+        from paper_2103_07974_b200.workload import BucketLayout as _BL
+
+        lay2 = _BL.build([256 * 784, 256, 10 * 256, 10], 32)
+
+        def vs_oracle(ws):
+            worst = 0.0
+            for k in range(2):
+                w = ws[k].numpy().astype(np.float64)
+                for t in range(T):
+                    for i, o in enumerate(lay2.offsets):
+                        r = mom_ref[k][t][i].reshape(-1)
+                        worst = max(worst, float(np.max(np.abs(w[t, o:o + r.size] - r) / (1e-5 + 1e-3 * np.abs(r)))))
+            return worst
+        for name, ws in (("bucket", mom_w["bucket"]), ("sharded", mom_w["sharded"]), ("p2p", p2p_w)):
+            wr = vs_oracle(ws)
+            res["checks"].append({"name": f"momentum_{name}_vs_oracle", "ok": wr <= 1.0, "worst_ratio": wr})
 
         if world == 2:
             # single-GPU run with 2 simulated workers, reduced left to right by K2
