@@ -95,6 +95,16 @@ def run_isolated(job: LinearJob, iterations: int) -> list[np.ndarray]:
     return out
 
 
+def run_isolated_momentum(job: LinearJob, iterations: int, momentum: float) -> list[np.ndarray]:
+    """run_isolated with torch.optim.SGD momentum (no reference counterpart; fp64)."""
+    p, buf, out = job.p0, None, []
+    for t in range(1, iterations + 1):
+        p, buf = torch_sgd_step(p, job.averaged_gradient(p, t), buf, job.lr, momentum=momentum,
+                                first=t == 1)
+        out.append(p)
+    return out
+
+
 def run_crossover(jobs: Sequence[LinearJob], iterations: int, perturb=None) -> list[list[np.ndarray]]:
     """Interleaved order of equivalence.py:224-231 (+ 1-ulp perturb hook, :214-219)."""
     params = [j.p0 for j in jobs]

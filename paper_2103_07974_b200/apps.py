@@ -150,18 +150,20 @@ class _GatherData:
 
 
 def linear_app(config: SgdConfig, job_id: str, rng_seed: int, iterations: int,
-               device: torch.device, local_workers: int | None = None) -> App:
-    """One of the reference's synthetic SGD jobs as a device app."""
+               device: torch.device, local_workers: int | None = None, momentum: float = 0.0,
+               flat=False) -> App:
+    """One of the reference's synthetic SGD jobs as a device app (momentum: torch-SGD rule)."""
     x, y = make_dataset(config)
     idx = _index_table(rng_seed, iterations, config.workers, config.dataset_size, config.batch_size)
     model = LinearModel(initial_parameters(config.dim, rng_seed)).to(device)
+    flat_params = _flatten(list(model.parameters()), flat)
     data = _GatherData(torch.as_tensor(x, dtype=torch.float32, device=device),
                        torch.as_tensor(y, dtype=torch.float32, device=device),
                        torch.as_tensor(idx, device=device))
     return App(job_id, model, _linear_loss(config.loss), data,
-               SgdSettings(config.learning_rate), iterations,
+               SgdSettings(config.learning_rate, momentum=momentum), iterations,
                local_workers=config.workers if local_workers is None else local_workers,
-               samples_per_batch=config.batch_size)
+               samples_per_batch=config.batch_size, flat_params=flat_params)
 
 
 # ---------------------------------------------------------------------------

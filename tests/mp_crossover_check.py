@@ -76,15 +76,23 @@ def main():
             res["checks"].append({"name": "sharded_mode_used",
                                   "ok": all(st.sync.mode == "sharded" for st in s4.states)})
     n = mom_w["bucket"][0].shape[1]
-    mom_ref = osgd.run_mlp_crossover(specs, T, workers=world, momentum=0.9) if rank == 0 else None
     if world == 2:
         same = all(torch.equal(mom_w["bucket"][k], mom_w["sharded"][k][:, :n]) for k in range(2))
         res["checks"].append({"name": "sharded_bitwise_eq_allreduce_w2", "ok": bool(same)})
-    else:
-        # NCCL's all-reduce and reduce-scatter sum in different orders: fp32 tolerance
-        d = max(float(((mom_w["bucket"][k] - mom_w["sharded"][k][:, :n]).abs()
-                       / (1e-5 + 1e-3 * mom_w["bucket"][k].abs())).max()) for k in range(2))
-        res["checks"].append({"name": "sharded_close_to_allreduce", "ok": d <= 1.0, "worst_ratio": d})
+    # (MLP trajectories are compared bitwise only: a ReLU whose pre-activation sits within an
+    #  ulp of zero flips with the reduction order, so ReLU nets are chaotic at the ulp level.
+    #  Tolerance checks of every mode use the smooth linear problems below.)
+
+    # (3b) momentum on the reference's linear problems, every sync mode vs the fp64 oracle
+    Tl = 20
+    lin_m = {}
+    for mode, flat in (("bucket", False), ("sharded", True), ("p2p", "ipc")):
+        s7 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode=mode)
+        for k, c in enumerate(lcfg):
+            s7.register(linear_app(c, f"lm{k}", 40 + k, Tl, dev, local_workers=1, momentum=0.9, flat=flat))
+        s7.run()
+        lin_m[mode] = [s7.weights(f"lm{k}")[:, :8].cpu().numpy().astype(np.float64) for k in range(2)]
+        s7.close()
 
     # (4) collective-fused P2P sync (one kernel: NVLink reads of every rank's bucket shard in
     #     rank order, / W, SGD-momentum, NVLink writes of the new shard to every rank)
@@ -139,23 +147,12 @@ def main():
         same = all(torch.equal(s6.weights(f"m{k}").cpu(), p2p_w[k][:, :n]) for k in range(2))
         res["checks"].append({"name": f"p2p_w{world}_bitwise_eq_simulated_w{world}", "ok": bool(same)})
 
-        # every sync mode vs the fp64 oracle with torch-SGD momentum
-        from paper_2103_07974_b200.workload import BucketLayout as _BL
-
-        lay2 = _BL.build([256 * 784, 256, 10 * 256, 10], 32)
-
-        def vs_oracle(ws):
-            worst = 0.0
-            for k in range(2):
-                w = ws[k].numpy().astype(np.float64)
-                for t in range(T):
-                    for i, o in enumerate(lay2.offsets):
-                        r = mom_ref[k][t][i].reshape(-1)
-                        worst = max(worst, float(np.max(np.abs(w[t, o:o + r.size] - r) / (1e-5 + 1e-3 * np.abs(r)))))
-            return worst
-        for name, ws in (("bucket", mom_w["bucket"]), ("sharded", mom_w["sharded"]), ("p2p", p2p_w)):
-            wr = vs_oracle(ws)
-            res["checks"].append({"name": f"momentum_{name}_vs_oracle", "ok": wr <= 1.0, "worst_ratio": wr})
+        ljobs = [osgd.LinearJob(0.05, world, c.loss.value, c.dataset_seed, 40 + k) for k, c in enumerate(lcfg)]
+        lref_m = [np.stack(osgd.run_isolated_momentum(j, Tl, 0.9)) for j in ljobs]
+        for mode, ws in lin_m.items():
+            wr = max(float(np.max(np.abs(ws[k] - lref_m[k]) / (1e-5 + 1e-4 * np.abs(lref_m[k]))))
+                     for k in range(2))
+            res["checks"].append({"name": f"momentum_{mode}_vs_oracle", "ok": wr <= 1.0, "worst_ratio": wr})
 
         if world == 2:
             # single-GPU run with 2 simulated workers, reduced left to right by K2

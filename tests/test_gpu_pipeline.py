@@ -208,3 +208,21 @@ def test_mixed_models_bert_vgg(cuda_device):
     assert validate_trace(tr) == []
     assert [st.sync.layout.payload_bytes for st in s.states][0] == 553_430_176
     assert all(torch.isfinite(l).all() for st in s.states for l in st.losses)
+
+
+@pytest.mark.parametrize("workers", [1, 3, 4])
+def test_momentum_linear_matches_oracle(cuda_device, workers):
+    """torch-SGD momentum through K2 (W simulated workers) vs the fp64 momentum oracle."""
+    from paper_2103_07974_b200.apps import LossKind, SgdConfig, linear_app
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
+
+    cfgs = [SgdConfig(0.05, workers, LossKind.LEAST_SQUARES, 51), SgdConfig(0.05, workers, LossKind.LOGISTIC, 52)]
+    s = CrossoverScheduler(Policy.CROSSOVER, record_weights=True)
+    for k, c in enumerate(cfgs):
+        s.register(linear_app(c, f"j{k}", 7 + k, 25, cuda_device, momentum=0.9))
+    s.run()
+    for k, c in enumerate(cfgs):
+        ref = np.stack(osgd.run_isolated_momentum(
+            osgd.LinearJob(0.05, workers, c.loss.value, c.dataset_seed, 7 + k), 25, 0.9))
+        got = s.weights(f"j{k}")[:, :8].cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(got - ref) <= ATOL + RTOL * np.abs(ref))
