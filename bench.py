@@ -54,7 +54,7 @@ def parse():
                                               "(configs 3/5); overrides --model/--jobs/--batch")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"],
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
                          "the fused NVLink P2P kernel; auto = bucket")
     return ap.parse_args()
@@ -310,6 +310,10 @@ def kernel_summary(kern: dict, sync) -> dict:
             t = statistics.mean(kern[name])
             out[name] = {"ms": round(t, 4), "bus_bytes": sync.c1_bus_bytes() / 2,
                          "busbw_GB/s": round(sync.c1_bus_bytes() / 2 / (t / 1e3) / 1e9, 1)}
+    if "c1_unfused" in kern:
+        t = statistics.mean(kern["c1_unfused"])
+        out["c1_unfused"] = {"ms": round(t, 4), "messages": len(sync.params),
+                             "busbw_GB/s": round(sync.c1_bus_bytes() / (t / 1e3) / 1e9, 1)}
     if "k2_p2p_fused" in kern:
         t = statistics.mean(kern["k2_p2p_fused"])
         nv = sync.c1_bus_bytes()

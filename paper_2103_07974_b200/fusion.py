@@ -129,10 +129,12 @@ class FusedGradientSync:
                 mode = "direct"
             else:
                 mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
-        if mode not in ("bucket", "direct", "sharded", "p2p"):
+        if mode not in ("bucket", "direct", "sharded", "p2p", "unfused"):
             raise ConfigError(f"unknown sync mode {mode!r}")
         if mode == "direct" and self.workers != 1:
             raise ConfigError("direct mode has no bucket and needs exactly one worker")
+        if mode == "unfused" and self.local_workers != 1:
+            raise ConfigError("unfused mode all-reduces each gradient tensor in place: one worker per rank")
         if mode in ("sharded", "p2p") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
             raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
                               "and one worker per rank")
@@ -226,11 +228,13 @@ class FusedGradientSync:
             self._upd["momentum_buf"] = [b.data_ptr() for b in self.momentum_bufs]
         self._upd["snap_offset"] = offs_bytes
         self._upd["numel"] = numels
-        if mode == "bucket":
+        if mode == "unfused":
+            self._sources = np.zeros(1, dtype=np.uint64)   # grad_offset = gradient pointer, per step
+        elif mode == "bucket":
             self._upd["grad_offset"] = offs_bytes
             self._sources = np.asarray([self.bucket.data_ptr() + w * row_bytes
                                         for w in range(self.local_workers)], dtype=np.uint64)
-        else:
+        elif mode == "direct":
             self._sources = np.zeros(1, dtype=np.uint64)
         self._finish_init(settings)
 
@@ -264,7 +268,7 @@ class FusedGradientSync:
     def update(self, stream: int, grads: Sequence[torch.Tensor] | None = None,
                snapshot_row: int | None = None) -> None:
         """K2: reduce the source rows left to right, / W, SGD step in place."""
-        if self.mode == "direct":
+        if self.mode in ("direct", "unfused"):
             if grads is None:
                 raise ValueError("direct mode needs the gradient tensors")
             self._upd["grad_offset"] = _grad_ptrs(grads, self.params)
@@ -281,6 +285,24 @@ class FusedGradientSync:
     def sync(self, grads_per_worker: Sequence[Sequence[torch.Tensor]], stream: int,
              snapshot_row: int | None = None, timer=None) -> None:
         """The whole sync phase of one iteration: K1 -> C1 -> K2 (or K2 alone in direct mode)."""
+        if self.mode == "unfused":
+            # per-tensor counterfactual (workload.unfused_messages, workload.py:104-110): one
+            # collective per gradient tensor, each paying the per-message latency
+            grads = grads_per_worker[0]
+            ptrs = _grad_ptrs(grads, self.params)
+            if timer is not None:
+                timer.begin("c1_unfused")
+            if self.comm is not None and self.comm.active:
+                for ptr, n in zip(ptrs, self.layout.numels):
+                    if n:
+                        self.comm.all_reduce_(ptr, n, stream)
+            if timer is not None:
+                timer.end("c1_unfused")
+                timer.begin("k2_update")
+            self.update(stream, grads, snapshot_row)
+            if timer is not None:
+                timer.end("k2_update")
+            return
         if self.mode == "direct":
             if timer is not None:
                 timer.begin("k2_update")

@@ -79,6 +79,18 @@ def main():
     if world == 2:
         same = all(torch.equal(mom_w["bucket"][k], mom_w["sharded"][k][:, :n]) for k in range(2))
         res["checks"].append({"name": "sharded_bitwise_eq_allreduce_w2", "ok": bool(same)})
+    # (3a) per-tensor (unfused) all-reduces == fused bucket at W = 2 (same two-operand sums)
+    s8 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode="unfused")
+    for k, (ds, rs) in enumerate(specs):
+        s8.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T,
+                            dev, local_workers=1, worker_count=world))
+    s8.run()
+    unf_w = [s8.weights(f"m{k}").cpu() for k in range(2)]
+    res["checks"].append({"name": "unfused_mode_used", "ok": all(st.sync.mode == "unfused" for st in s8.states)})
+    if world == 2:
+        same = all(torch.equal(mom_w["bucket"][k], unf_w[k]) for k in range(2))
+        res["checks"].append({"name": "unfused_bitwise_eq_fused_w2", "ok": bool(same)})
+
     # (MLP trajectories are compared bitwise only: a ReLU whose pre-activation sits within an
     #  ulp of zero flips with the reduction order, so ReLU nets are chaotic at the ulp level.
     #  Tolerance checks of every mode use the smooth linear problems below.)
@@ -86,7 +98,7 @@ def main():
     # (3b) momentum on the reference's linear problems, every sync mode vs the fp64 oracle
     Tl = 20
     lin_m = {}
-    for mode, flat in (("bucket", False), ("sharded", True), ("p2p", "ipc")):
+    for mode, flat in (("bucket", False), ("sharded", True), ("p2p", "ipc"), ("unfused", False)):
         s7 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode=mode)
         for k, c in enumerate(lcfg):
             s7.register(linear_app(c, f"lm{k}", 40 + k, Tl, dev, local_workers=1, momentum=0.9, flat=flat))
