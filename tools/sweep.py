@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--gemm-reps", type=int, default=3)
     ap.add_argument("--out", default="")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p"])
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"])
     ap.add_argument("--p2p-ctas", type=int, default=0)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     args = ap.parse_args()
