@@ -172,6 +172,7 @@ CS_API int cs_nccl_reduce_scatter_sum_f32(void* comm, const float* send, float* 
 CS_API int cs_nccl_all_gather_f32(void* comm, const float* send, float* recv,
                            size_t send_count, void* stream);
 CS_API int cs_nccl_async_error(void* comm);
+CS_API int cs_nccl_abort(void* comm);   /* failure path: unblocks work waiting on a dead peer */
 CS_API int cs_nccl_destroy(void* comm);
 
 #ifdef __cplusplus

@@ -85,6 +85,7 @@ EXPORTS = {
     "cs_nccl_all_gather_f32": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_async_error": ([ctypes.c_void_p], ctypes.c_int),
+    "cs_nccl_abort": ([ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_destroy": ([ctypes.c_void_p], ctypes.c_int),
 }
 

@@ -167,6 +167,12 @@ class NcclCommunicator:
         if self.world > 1:
             self._lib.check("cs_nccl_async_error", self._lib.lib.cs_nccl_async_error(self.handle))
 
+    def abort(self) -> None:
+        """Abort the communicator (unblocks kernels stuck waiting for a dead peer)."""
+        if self.world > 1 and self.handle:
+            self._lib.lib.cs_nccl_abort(self.handle)
+            self.handle = ctypes.c_void_p(None)
+
     def close(self) -> None:
         if self.world > 1 and self.handle:
             self._lib.check("cs_nccl_destroy", self._lib.lib.cs_nccl_destroy(self.handle))

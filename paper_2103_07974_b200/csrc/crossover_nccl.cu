@@ -90,6 +90,11 @@ int cs_nccl_async_error(void* comm) {
   return nccl_status(r, "NCCL async error");
 }
 
+int cs_nccl_abort(void* comm) {
+  if (comm == nullptr) return 0;
+  return nccl_status(ncclCommAbort((ncclComm_t)comm), "ncclCommAbort");
+}
+
 int cs_nccl_destroy(void* comm) {
   if (comm == nullptr) return 0;
   return nccl_status(ncclCommDestroy((ncclComm_t)comm), "ncclCommDestroy");

@@ -29,6 +29,7 @@ returned as a measured ``Trace``.
 from __future__ import annotations
 
 import contextlib
+import time
 from dataclasses import dataclass, field
 from enum import Enum
 from fractions import Fraction
@@ -205,7 +206,7 @@ class CrossoverScheduler:
                  comm: NcclCommunicator | None = None, record_spans: bool = True,
                  record_weights: bool = False, align: int = 32, sync_mode: str = "auto",
                  time_kernels: bool = False, comm_priority: int = -1,
-                 perturb: tuple[int, int] | None = None):
+                 perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -219,6 +220,7 @@ class CrossoverScheduler:
         self.sync_mode = sync_mode
         self.record_weights = record_weights
         self.perturb = perturb
+        self.watchdog_s = watchdog_s
         with torch.cuda.device(self.device):
             self.compute_stream = torch.cuda.Stream(self.device)
             lo, hi = torch.cuda.Stream.priority_range()
@@ -351,18 +353,42 @@ class CrossoverScheduler:
     def job_index(self, job_id: str) -> int:
         return self.job_order.index(job_id)
 
-    def drain(self) -> None:
-        """Wait for the final syncs (the drain of Alg. 1) and release gradients."""
+    def drain(self, timeout_s: float | None = None) -> None:
+        """Wait for the final syncs (the drain of Alg. 1) and release gradients.
+
+        Failure detection (SURVEY §5): while waiting, NCCL's asynchronous error state is polled;
+        an error, or no completion within ``timeout_s`` (default: ``self.watchdog_s``), aborts the
+        communicator and raises DeadlockError(job, iteration) for the oldest unfinished sync --
+        the device analogue of the reference's quiescence check (engine.py:168-173).
+        """
         join = torch.cuda.Event()
         join.record(self.comm_stream)
         self.compute_stream.wait_event(join)
-        self.compute_stream.synchronize()
-        self.comm_stream.synchronize()
+        done = torch.cuda.Event()
+        done.record(self.compute_stream)
+        limit = self.watchdog_s if timeout_s is None else timeout_s
+        t0 = time.monotonic()
+        while not done.query():
+            if self.comm is not None:
+                try:
+                    self.comm.check_async_error()
+                except RuntimeError as exc:
+                    self._fail(f"NCCL error: {exc}")
+            if limit is not None and time.monotonic() - t0 > limit:
+                self._fail(f"no progress within {limit:.0f} s")
+            time.sleep(0.0005)
         for st in self.states:
             st.held = None
             st.awaiting_sync = False
         if self.comm is not None:
             self.comm.check_async_error()
+
+    def _fail(self, detail: str) -> None:
+        waiting = [(st.job_id, st.sync_of_iteration) for st in self.states if st.awaiting_sync]
+        job, it = waiting[0] if waiting else (self.states[0].job_id, self.states[0].next_iteration)
+        if self.comm is not None:
+            self.comm.abort()
+        raise DeadlockError(job, it, f"policy={self.policy.value}; {detail}")
 
     def run(self) -> Trace:
         """Step every app through its budget; returns the measured trace."""

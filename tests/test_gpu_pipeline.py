@@ -226,3 +226,58 @@ def test_momentum_linear_matches_oracle(cuda_device, workers):
             osgd.LinearJob(0.05, workers, c.loss.value, c.dataset_seed, 7 + k), 25, 0.9))
         got = s.weights(f"j{k}")[:, :8].cpu().numpy().astype(np.float64)
         assert np.all(np.abs(got - ref) <= ATOL + RTOL * np.abs(ref))
+
+
+def test_simulate_measure_compare_on_device(cuda_device):
+    """Reference-shaped API end to end: SchedulePlan -> simulate (on the GPU) -> measure -> compare."""
+    from paper_2103_07974_b200.apps import MlpConfig, mlp_app
+    from paper_2103_07974_b200.metrics import compare, measure, report
+    from paper_2103_07974_b200.scheduler import Policy, SchedulePlan, simulate
+
+    mk = lambda: [mlp_app(MlpConfig(workers=1, dataset_seed=k), f"m{k}", k, 6, cuda_device)  # noqa: E731
+                  for k in range(2)]
+    px = SchedulePlan(Policy.CROSSOVER, mk())
+    ps = SchedulePlan(Policy.SEQUENTIAL, mk())
+    mx = measure(simulate(px), px, "mlp")
+    ms = measure(simulate(ps), ps, "mlp")
+    c = compare(mx, ms)
+    assert c.per_job_iterations == {"m0": 6, "m1": 6}
+    assert c.speedup_vs_baseline > 0 and 0 < c.gpu_utilization <= 1
+    assert "speedup" in report(c, "table")
+
+
+def test_e2e_host_batches_resnet(cuda_device):
+    """Pinned-host uint8 batches are copied on the H2D stream and normalised on the device."""
+    from paper_2103_07974_b200.apps import resnet50_app
+    from paper_2103_07974_b200.engine import validate_trace
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
+
+    s = CrossoverScheduler(Policy.CROSSOVER)
+    for k in range(2):
+        s.register(resnet50_app(f"h{k}", 8, 2, cuda_device, seed=k, host_data=True))
+    tr = s.run()
+    assert validate_trace(tr) == []
+    assert all(torch.isfinite(l).all() for st in s.states for l in st.losses)
+
+
+def test_watchdog_raises_deadlock_error(cuda_device):
+    """No completion within the watchdog limit -> DeadlockError naming the pending (job, iteration)."""
+    from paper_2103_07974_b200.apps import MlpConfig, mlp_app
+    from paper_2103_07974_b200.errors import DeadlockError
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
+
+    app = mlp_app(MlpConfig(workers=1), "slow", 0, 1, cuda_device)
+    inner = app.loss_fn
+
+    def slow_loss(model, batch):
+        torch.cuda._sleep(2_000_000_000)          # ~1 s of device time
+        return inner(model, batch)
+
+    app.loss_fn = slow_loss
+    s = CrossoverScheduler(Policy.CROSSOVER, watchdog_s=0.05)
+    s.register(app)
+    s.step()
+    with pytest.raises(DeadlockError) as ei:
+        s.drain()
+    assert ei.value.job_id == "slow" and ei.value.iteration == 1
+    torch.cuda.synchronize()
