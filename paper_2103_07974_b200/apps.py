@@ -302,7 +302,12 @@ class _GraphedImageModel(torch.nn.Module):
 
 def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
                device: torch.device, seed: int, host_data: bool, sgd: SgdSettings,
-               n_batches: int = 2, graphed: bool = False, flat: bool = False) -> App:
+               n_batches: int = 2, graphed: bool = False, flat: bool = False,
+               fast_bn: bool = False) -> App:
+    if fast_bn:   # NHWC BatchNorm kernels of libcrossover.so instead of ATen's (same semantics)
+        from .bn import swap_batchnorm
+
+        swap_batchnorm(model)
     model = model.to(device).to(memory_format=torch.channels_last)
     data = _CycleData(synthetic_image_batches(batch, n_batches, seed, device, host_uint8=host_data))
     params = [p for p in model.parameters() if p.requires_grad]
@@ -321,22 +326,22 @@ DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
 
 def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
-                 graphed: bool = False, flat: bool = False) -> App:
+                 graphed: bool = False, flat: bool = False, fast_bn: bool = False) -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed, flat=flat)
+                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn)
 
 
 def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
-                 graphed: bool = False, flat: bool = False) -> App:
+                 graphed: bool = False, flat: bool = False, fast_bn: bool = False) -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed, flat=flat)
+                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn)
 
 
 def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,

@@ -1,0 +1,112 @@
+"""channels_last BatchNorm2d for the apps' forward/backward, on libcrossover.so's BN kernels.
+
+``swap_batchnorm(model)`` replaces every ``nn.BatchNorm2d`` by :class:`CrossoverBatchNorm2d`
+(same parameters and buffers, same training semantics: batch statistics, biased variance for
+normalisation, unbiased variance in the running estimate, ``momentum``, ``num_batches_tracked``).
+In training mode on a bf16 CUDA input whose channel count the kernels support it runs
+``cs_bn_forward`` / ``cs_bn_backward``; everything else (eval mode, fp32 inputs, odd channel
+counts) goes through ``torch.nn.functional.batch_norm`` unchanged.  The kernels are graph-safe
+(no host synchronisation; the per-module workspace keeps a fixed address).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+
+__all__ = ["CrossoverBatchNorm2d", "swap_batchnorm", "bn_supported"]
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else t.data_ptr()
+
+
+def bn_supported(x: torch.Tensor) -> bool:
+    c = x.shape[1] if x.dim() == 4 else 0
+    return (x.is_cuda and x.dtype == torch.bfloat16 and x.dim() == 4 and c % 8 == 0
+            and (c <= 256 or c % 256 == 0))
+
+
+class _BnFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, weight, bias, running_mean, running_var, momentum, eps, ws):
+        n, c, h, w = x.shape
+        m = n * h * w
+        x = x.contiguous(memory_format=torch.channels_last)
+        y = torch.empty_like(x)
+        f32 = dict(dtype=torch.float32, device=x.device)
+        save_mean = torch.empty(c, **f32)
+        save_invstd = torch.empty(c, **f32)
+        scale_shift = torch.empty(2 * c, **f32)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        _lib.check("cs_bn_forward", _lib.lib.cs_bn_forward(
+            x.data_ptr(), m, c, _ptr(weight), _ptr(bias), _ptr(running_mean), _ptr(running_var),
+            ctypes.c_float(momentum), ctypes.c_float(eps), save_mean.data_ptr(), save_invstd.data_ptr(),
+            scale_shift.data_ptr(), y.data_ptr(), ws.data_ptr(), stream))
+        ctx.save_for_backward(x, weight, save_mean, save_invstd)
+        ctx.ws = ws
+        ctx.has_bias = bias is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, weight, save_mean, save_invstd = ctx.saved_tensors
+        n, c, h, w = x.shape
+        dy = dy.contiguous(memory_format=torch.channels_last)
+        dx = torch.empty_like(x)
+        f32 = dict(dtype=torch.float32, device=x.device)
+        gw = torch.empty(c, **f32) if weight is not None else None
+        gb = torch.empty(c, **f32) if ctx.has_bias else None
+        coef = torch.empty(3 * c, **f32)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        _lib.check("cs_bn_backward", _lib.lib.cs_bn_backward(
+            dy.data_ptr(), x.data_ptr(), n * h * w, c, save_mean.data_ptr(), save_invstd.data_ptr(),
+            _ptr(weight), _ptr(gw), _ptr(gb), coef.data_ptr(), dx.data_ptr(), ctx.ws.data_ptr(), stream))
+        return dx, gw, gb, None, None, None, None, None
+
+
+class CrossoverBatchNorm2d(torch.nn.BatchNorm2d):
+    """nn.BatchNorm2d whose training-mode bf16 path runs the fused NHWC kernels."""
+
+    def _workspace(self, x: torch.Tensor) -> torch.Tensor:
+        n, c, h, w = x.shape
+        need = int(_lib.lib.cs_bn_workspace_bytes(n * h * w, c))
+        ws = getattr(self, "_cs_ws", None)
+        if ws is None or ws.numel() < need or ws.device != x.device:
+            ws = torch.zeros(need, dtype=torch.uint8, device=x.device)   # zeroed once; kernels keep it zeroed
+            self._cs_ws = ws
+        return ws
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not (self.training and bn_supported(x)):
+            return super().forward(x)
+        momentum = self.momentum
+        if self.track_running_stats and self.num_batches_tracked is not None:
+            self.num_batches_tracked.add_(1)
+            if momentum is None:   # cumulative moving average, as nn.BatchNorm2d
+                raise NotImplementedError("momentum=None is not supported by the fused kernels")
+        rm = self.running_mean if self.track_running_stats else None
+        rv = self.running_var if self.track_running_stats else None
+        return _BnFunction.apply(x, self.weight, self.bias, rm, rv, float(momentum or 0.0),
+                                 float(self.eps), self._workspace(x))
+
+
+def swap_batchnorm(module: torch.nn.Module) -> int:
+    """Replace nn.BatchNorm2d children in place (parameters and buffers are shared); returns count."""
+    count = 0
+    for name, child in list(module.named_children()):
+        if type(child) is torch.nn.BatchNorm2d:
+            new = CrossoverBatchNorm2d(child.num_features, child.eps, child.momentum, child.affine,
+                                       child.track_running_stats, device=None)
+            new.weight, new.bias = child.weight, child.bias
+            new.running_mean, new.running_var = child.running_mean, child.running_var
+            new.num_batches_tracked = child.num_batches_tracked
+            new.train(child.training)
+            setattr(module, name, new)
+            count += 1
+        else:
+            count += swap_batchnorm(child)
+    return count

@@ -1,0 +1,96 @@
+"""NHWC BatchNorm kernels (apps' compute) vs torch.nn.functional.batch_norm in fp32."""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(8, 64, 56, 56), (4, 256, 14, 14), (2, 2048, 7, 7), (16, 24, 5, 5), (3, 512, 9, 9),
+          (1, 8, 1, 1), (64, 1024, 2, 3)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_bn_forward_backward_matches_torch(cuda_device, shape):
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d
+
+    torch.manual_seed(sum(shape))
+    n, c, h, w = shape
+    x = (torch.randn(shape, device=cuda_device) * 3 + 1.5).to(torch.bfloat16).contiguous(
+        memory_format=torch.channels_last)
+    dy = torch.randn(shape, device=cuda_device).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    bn = CrossoverBatchNorm2d(c).to(cuda_device)
+    with torch.no_grad():
+        bn.weight.copy_(torch.rand(c) + 0.5)
+        bn.bias.copy_(torch.randn(c))
+        bn.running_var.fill_(2.0)
+    ref = torch.nn.BatchNorm2d(c).to(cuda_device)
+    ref.load_state_dict(bn.state_dict())
+    xa = x.detach().clone().requires_grad_(True)
+    xb = x.detach().float().clone().requires_grad_(True)
+    y = bn(xa)
+    yr = ref(xb)
+    assert y.dtype == torch.bfloat16 and y.is_contiguous(memory_format=torch.channels_last)
+    torch.testing.assert_close(y.float(), yr.to(torch.bfloat16).float(), rtol=2e-2, atol=3e-2)
+    y.backward(dy)
+    yr.backward(dy.float())
+    scale = xb.grad.abs().max().item()
+    torch.testing.assert_close(xa.grad.float(), xb.grad, rtol=2e-2, atol=2e-2 * scale)
+    for a, b in ((bn.weight.grad, ref.weight.grad), (bn.bias.grad, ref.bias.grad)):
+        torch.testing.assert_close(a, b, rtol=2e-3, atol=1e-3 * b.abs().max().item() + 1e-4)
+    torch.testing.assert_close(bn.running_mean, ref.running_mean, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(bn.running_var, ref.running_var, rtol=1e-4, atol=1e-5)
+    assert int(bn.num_batches_tracked) == int(ref.num_batches_tracked) == 1
+
+
+def test_bn_deterministic_and_graph_capturable(cuda_device):
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d
+
+    bn = CrossoverBatchNorm2d(128).to(cuda_device)
+    x = torch.randn(32, 128, 28, 28, device=cuda_device).to(torch.bfloat16).contiguous(
+        memory_format=torch.channels_last)
+    y1 = bn(x)
+    y2 = bn(x)
+    assert torch.equal(y1, y2)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        bn(x)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        yg = bn(x)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(yg, y1)
+
+
+def test_bn_fallbacks(cuda_device):
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d, swap_batchnorm
+
+    bn = CrossoverBatchNorm2d(20).to(cuda_device)          # C % 8 != 0 -> ATen path
+    x = torch.randn(4, 20, 6, 6, device=cuda_device).to(torch.bfloat16)
+    ref = torch.nn.BatchNorm2d(20).to(cuda_device)
+    torch.testing.assert_close(bn(x).float(), ref(x).float(), rtol=1e-2, atol=1e-2)
+    bn.eval()
+    assert bn(x).shape == x.shape
+    import torchvision
+
+    m = torchvision.models.resnet50()
+    assert swap_batchnorm(m) == 53
+    assert isinstance(m.bn1, CrossoverBatchNorm2d)
+    assert sum(p.numel() for p in m.parameters()) == 25_557_032
+
+
+def test_resnet50_fast_bn_graphed_pipeline(cuda_device):
+    from paper_2103_07974_b200.apps import resnet50_app
+    from paper_2103_07974_b200.engine import validate_trace
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
+
+    s = CrossoverScheduler(Policy.CROSSOVER)
+    for k in range(2):
+        s.register(resnet50_app(f"b{k}", 16, 3, cuda_device, seed=k, graphed=True, fast_bn=True))
+    tr = s.run()
+    assert validate_trace(tr) == []
+    losses = [float(l) for st in s.states for l in st.losses]
+    assert all(0 < l < 20 for l in losses)

@@ -14,12 +14,16 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def run(model_name="resnet50", batch=256, fmt="cl", graph=False, iters=10):
+def run(model_name="resnet50", batch=256, fmt="cl", graph=False, iters=10, fast_bn=False):
     import torchvision
 
     dev = torch.device("cuda", 0)
     torch.backends.cudnn.benchmark = True
-    m = getattr(torchvision.models, model_name)().to(dev)
+    m = getattr(torchvision.models, model_name)()
+    if fast_bn:
+        from paper_2103_07974_b200.bn import swap_batchnorm
+        swap_batchnorm(m)
+    m = m.to(dev)
     mf = torch.channels_last if fmt == "cl" else torch.contiguous_format
     m = m.to(memory_format=mf)
     params = [p for p in m.parameters()]
@@ -60,11 +64,10 @@ def run(model_name="resnet50", batch=256, fmt="cl", graph=False, iters=10):
 
 if __name__ == "__main__":
     for model in sys.argv[1:] or ["resnet50"]:
-        for fmt in ("cl", "nchw"):
-            for graph in (False, True):
+        for fmt, graph, fast in (("cl", False, False), ("cl", True, False), ("cl", False, True), ("cl", True, True)):
                 try:
-                    gpu, cpu = run(model, fmt=fmt, graph=graph)
-                    print(f"{model} fmt={fmt} graph={graph}: {gpu:.2f} ms/iter GPU, {cpu:.2f} ms host issue, "
+                    gpu, cpu = run(model, fmt=fmt, graph=graph, fast_bn=fast)
+                    print(f"{model} fmt={fmt} graph={graph} fast_bn={fast}: {gpu:.2f} ms/iter GPU, {cpu:.2f} ms host issue, "
                           f"{256 / gpu * 1e3:.0f} img/s", flush=True)
                 except Exception as e:  # noqa: BLE001
                     print(f"{model} fmt={fmt} graph={graph}: FAILED {type(e).__name__}: {str(e)[:200]}", flush=True)
