@@ -54,6 +54,7 @@ def parse():
                                               "(configs 3/5); overrides --model/--jobs/--batch")
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
+    ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
                          "the fused NVLink P2P kernel; auto = bucket")
@@ -351,11 +352,12 @@ def run_ours(args):
             else:
                 fn = apps.resnet50_app if name == "resnet50" else apps.vgg16_app
                 base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j + rank,
-                               graphed=not args.no_graphs, flat=flat))
+                               graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn))
         args.no_e2e, args.no_cpu_baseline = True, True
     else:
         base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
-                      graphed=not args.no_graphs, flat=flat) for j in range(args.jobs)]
+                      graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn)
+            for j in range(args.jobs)]
     host_data = None if args.no_e2e else [
         apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + j, dev, host_uint8=True))
         for j in range(args.jobs)]
@@ -412,7 +414,8 @@ def run_ours(args):
                                     f"{args.jobs}x {args.model} co-located, crossover, batch "
                                     f"{args.batch}/GPU")
                                    + ", bf16 autocast, fp32 params/grads, SGD momentum 0.9"
-                                   + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs"),
+                                   + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs")
+                                   + ("" if args.aten_bn else ", NHWC BatchNorm kernels"),
                        "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": sync0.mode},

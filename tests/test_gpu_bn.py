@@ -35,7 +35,7 @@ def test_bn_forward_backward_matches_torch(cuda_device, shape):
     y.backward(dy)
     yr.backward(dy.float())
     scale = xb.grad.abs().max().item()
-    torch.testing.assert_close(xa.grad.float(), xb.grad, rtol=2e-2, atol=2e-2 * scale)
+    torch.testing.assert_close(xa.grad.float(), xb.grad, rtol=2e-2, atol=2e-2 * scale + 1e-6)
     for a, b in ((bn.weight.grad, ref.weight.grad), (bn.bias.grad, ref.bias.grad)):
         torch.testing.assert_close(a, b, rtol=2e-3, atol=1e-3 * b.abs().max().item() + 1e-4)
     torch.testing.assert_close(bn.running_mean, ref.running_mean, rtol=1e-4, atol=1e-5)
