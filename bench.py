@@ -384,6 +384,11 @@ def run_ours(args):
     value = samples_per_rot * K / (cross["ms"] / 1e3)
     seq_value = samples_per_rot * K / (seq["ms"] / 1e3)
 
+    # NHWC BN kernels: 3 forward + 3 backward launches per BN layer per iteration (they replay
+    # inside the CUDA graphs, so they are counted from the model structure, not from Python calls)
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d
+    n_bn = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverBatchNorm2d)) for a in base)
+    bn_launches = 6 * n_bn
     hbm_peak, peak_kind = peaks()
     sync0 = cross["sched"].states[0].sync
     kernels = kernel_summary(cross["kernels"], sync0)
@@ -434,7 +439,8 @@ def run_ours(args):
                          "peak_kind": peak_kind, "bytes_per_launch": sync0.k2_bytes()},
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
-            "gpu_launches": cross["launches"],
+            "gpu_launches": cross["launches"] + bn_launches * K,
+            "gpu_launches_breakdown": {"k1_k2_p2p": cross["launches"], "bn_kernels": bn_launches * K},
             "clocks": cross["clocks"],
             "e2e": e2e_line,
             "cpu_baseline": cpu,
