@@ -159,23 +159,31 @@ CS_API int cs_ipc_get_handle(void* ptr, uint8_t* out /* CS_IPC_HANDLE_BYTES */);
 CS_API int cs_ipc_open_handle(const uint8_t* handle, void** ptr);
 CS_API int cs_ipc_close_handle(void* ptr);
 
-/* channels_last BatchNorm2d (training) for the apps' compute: x / y / dy / dx are bf16 [M, C]
- * row-major (M = N*H*W, C % 8 == 0), weight / bias / running stats / saved stats fp32 [C].
+/* channels_last BatchNorm2d (training) for the apps' compute: x / y / dy / dx / residual are
+ * bf16 [M, C] row-major (M = N*H*W, C % 8 == 0, C <= 256 or C % 256 == 0), weight / bias /
+ * running stats / saved stats fp32 [C].
  * Forward: per-channel mean / biased var (Welford + fixed-order Chan merge), running stats
- * updated with the unbiased variance (torch semantics, momentum as in nn.BatchNorm2d),
- * y = (x - mean) * invstd * w + b.  scale_shift: fp32 [2C] scratch (scale, shift).
- * Backward: grad_weight = sum(dy * xhat), grad_bias = sum(dy), dx per torch's formula.
- * coef: fp32 [3C] scratch.  workspace: cs_bn_workspace_bytes(M, C) bytes, zeroed once
- * (the kernels leave it zeroed).  weight / bias / running stats / grads may be NULL. */
+ * updated with the unbiased variance (nn.BatchNorm2d momentum semantics), then the fused
+ * epilogue y = act((x - mean) * invstd * w + b [+ residual]) with flags
+ * CS_BN_RELU (act = max(., 0)) and CS_BN_RESIDUAL (add `residual` before the activation).
+ * scale_shift: fp32 [2C] written by the forward (scale, shift) and read by the backward.
+ * Backward: g = dy masked by the recomputed activation; grad_weight = sum(g * xhat),
+ * grad_bias = sum(g), dx per torch's formula, dresidual = g (CS_BN_RESIDUAL).
+ * coef: fp32 [3C] scratch.  workspace: cs_bn_workspace_bytes(M, C) bytes (caller-owned).
+ * weight / bias / running stats / grads may be NULL. */
+#define CS_BN_RELU 1
+#define CS_BN_RESIDUAL 2
 CS_API size_t cs_bn_workspace_bytes(int64_t M, int C);
-CS_API int cs_bn_forward(const void* x, int64_t M, int C, const float* weight, const float* bias,
-                         float* running_mean, float* running_var, float momentum, float eps,
-                         float* save_mean, float* save_invstd, float* scale_shift, void* y,
-                         void* workspace, void* stream);
-CS_API int cs_bn_backward(const void* dy, const void* x, int64_t M, int C,
-                          const float* save_mean, const float* save_invstd, const float* weight,
-                          float* grad_weight, float* grad_bias, float* coef, void* dx,
-                          void* workspace, void* stream);
+CS_API int cs_bn_forward(const void* x, const void* residual, int64_t M, int C,
+                         const float* weight, const float* bias, float* running_mean,
+                         float* running_var, float momentum, float eps, float* save_mean,
+                         float* save_invstd, float* scale_shift, void* y, void* workspace,
+                         int flags, void* stream);
+CS_API int cs_bn_backward(const void* dy, const void* x, const void* residual, int64_t M, int C,
+                          const float* save_mean, const float* save_invstd,
+                          const float* scale_shift, const float* weight, float* grad_weight,
+                          float* grad_bias, float* coef, void* dx, void* dresidual,
+                          void* workspace, int flags, void* stream);
 
 /* NCCL communicator over NVLink / NVSwitch (one per process, one per job set).
  * min_ctas / max_ctas <= 0 leave NCCL's defaults. */

@@ -305,9 +305,11 @@ def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
                n_batches: int = 2, graphed: bool = False, flat: bool = False,
                fast_bn: bool = False) -> App:
     if fast_bn:   # NHWC BatchNorm kernels of libcrossover.so instead of ATen's (same semantics)
-        from .bn import swap_batchnorm
+        from .bn import fuse_resnet, swap_batchnorm
 
         swap_batchnorm(model)
+        if hasattr(model, "layer1"):
+            fuse_resnet(model)      # BN + ReLU (+ residual add) in one pass
     model = model.to(device).to(memory_format=torch.channels_last)
     data = _CycleData(synthetic_image_batches(batch, n_batches, seed, device, host_uint8=host_data))
     params = [p for p in model.parameters() if p.requires_grad]

@@ -17,7 +17,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["CrossoverBatchNorm2d", "swap_batchnorm", "bn_supported"]
+__all__ = ["CrossoverBatchNorm2d", "swap_batchnorm", "fuse_resnet", "bn_supported"]
 
 
 def _ptr(t: torch.Tensor | None):
@@ -30,12 +30,18 @@ def bn_supported(x: torch.Tensor) -> bool:
             and (c <= 256 or c % 256 == 0))
 
 
+CS_BN_RELU = 1
+CS_BN_RESIDUAL = 2
+
+
 class _BnFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, weight, bias, running_mean, running_var, momentum, eps, ws):
+    def forward(ctx, x, weight, bias, running_mean, running_var, momentum, eps, ws, residual, flags):
         n, c, h, w = x.shape
         m = n * h * w
         x = x.contiguous(memory_format=torch.channels_last)
+        if residual is not None:
+            residual = residual.contiguous(memory_format=torch.channels_last)
         y = torch.empty_like(x)
         f32 = dict(dtype=torch.float32, device=x.device)
         save_mean = torch.empty(c, **f32)
@@ -43,46 +49,62 @@ class _BnFunction(torch.autograd.Function):
         scale_shift = torch.empty(2 * c, **f32)
         stream = torch.cuda.current_stream(x.device).cuda_stream
         _lib.check("cs_bn_forward", _lib.lib.cs_bn_forward(
-            x.data_ptr(), m, c, _ptr(weight), _ptr(bias), _ptr(running_mean), _ptr(running_var),
-            ctypes.c_float(momentum), ctypes.c_float(eps), save_mean.data_ptr(), save_invstd.data_ptr(),
-            scale_shift.data_ptr(), y.data_ptr(), ws.data_ptr(), stream))
-        ctx.save_for_backward(x, weight, save_mean, save_invstd)
-        ctx.ws = ws
+            x.data_ptr(), _ptr(residual), m, c, _ptr(weight), _ptr(bias), _ptr(running_mean),
+            _ptr(running_var), ctypes.c_float(momentum), ctypes.c_float(eps), save_mean.data_ptr(),
+            save_invstd.data_ptr(), scale_shift.data_ptr(), y.data_ptr(), ws.data_ptr(), flags, stream))
+        keep_res = residual if (flags & CS_BN_RELU and flags & CS_BN_RESIDUAL) else None
+        ctx.save_for_backward(x, weight, save_mean, save_invstd, scale_shift, keep_res)
+        ctx.ws, ctx.flags = ws, flags
         ctx.has_bias = bias is not None
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        x, weight, save_mean, save_invstd = ctx.saved_tensors
+        x, weight, save_mean, save_invstd, scale_shift, res = ctx.saved_tensors
         n, c, h, w = x.shape
         dy = dy.contiguous(memory_format=torch.channels_last)
         dx = torch.empty_like(x)
+        dres = torch.empty_like(x) if ctx.flags & CS_BN_RESIDUAL else None
         f32 = dict(dtype=torch.float32, device=x.device)
         gw = torch.empty(c, **f32) if weight is not None else None
         gb = torch.empty(c, **f32) if ctx.has_bias else None
         coef = torch.empty(3 * c, **f32)
         stream = torch.cuda.current_stream(x.device).cuda_stream
         _lib.check("cs_bn_backward", _lib.lib.cs_bn_backward(
-            dy.data_ptr(), x.data_ptr(), n * h * w, c, save_mean.data_ptr(), save_invstd.data_ptr(),
-            _ptr(weight), _ptr(gw), _ptr(gb), coef.data_ptr(), dx.data_ptr(), ctx.ws.data_ptr(), stream))
-        return dx, gw, gb, None, None, None, None, None
+            dy.data_ptr(), x.data_ptr(), _ptr(res), n * h * w, c, save_mean.data_ptr(),
+            save_invstd.data_ptr(), scale_shift.data_ptr(), _ptr(weight), _ptr(gw), _ptr(gb),
+            coef.data_ptr(), dx.data_ptr(), _ptr(dres), ctx.ws.data_ptr(), ctx.flags, stream))
+        return dx, gw, gb, None, None, None, None, None, dres, None
 
 
 class CrossoverBatchNorm2d(torch.nn.BatchNorm2d):
-    """nn.BatchNorm2d whose training-mode bf16 path runs the fused NHWC kernels."""
+    """nn.BatchNorm2d whose training-mode bf16 path runs the fused NHWC kernels.
+
+    ``forward_fused(x, relu, residual)`` also fuses the ReLU and the residual add that follow
+    the BN in ResNet blocks into the same passes (forward and backward).
+    """
 
     def _workspace(self, x: torch.Tensor) -> torch.Tensor:
         n, c, h, w = x.shape
         need = int(_lib.lib.cs_bn_workspace_bytes(n * h * w, c))
         ws = getattr(self, "_cs_ws", None)
         if ws is None or ws.numel() < need or ws.device != x.device:
-            ws = torch.zeros(need, dtype=torch.uint8, device=x.device)   # zeroed once; kernels keep it zeroed
+            ws = torch.zeros(need, dtype=torch.uint8, device=x.device)
             self._cs_ws = ws
         return ws
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        if not (self.training and bn_supported(x)):
-            return super().forward(x)
+        return self.forward_fused(x)
+
+    def forward_fused(self, x: torch.Tensor, relu: bool = False,
+                      residual: torch.Tensor | None = None) -> torch.Tensor:
+        fast = self.training and bn_supported(x) and (
+            residual is None or (residual.shape == x.shape and residual.dtype == x.dtype))
+        if not fast:
+            y = super().forward(x)
+            if residual is not None:
+                y = y + residual
+            return torch.relu(y) if relu else y
         momentum = self.momentum
         if self.track_running_stats and self.num_batches_tracked is not None:
             self.num_batches_tracked.add_(1)
@@ -90,8 +112,41 @@ class CrossoverBatchNorm2d(torch.nn.BatchNorm2d):
                 raise NotImplementedError("momentum=None is not supported by the fused kernels")
         rm = self.running_mean if self.track_running_stats else None
         rv = self.running_var if self.track_running_stats else None
+        flags = (CS_BN_RELU if relu else 0) | (CS_BN_RESIDUAL if residual is not None else 0)
         return _BnFunction.apply(x, self.weight, self.bias, rm, rv, float(momentum or 0.0),
-                                 float(self.eps), self._workspace(x))
+                                 float(self.eps), self._workspace(x), residual, flags)
+
+
+def _bn_relu_forward(self, x):
+    return self.forward_fused(x, relu=True)
+
+
+def _bottleneck_forward(self, x):
+    # torchvision Bottleneck.forward with bn+relu and bn3+residual+relu fused
+    identity = x if self.downsample is None else self.downsample(x)
+    out = self.bn1.forward_fused(self.conv1(x), relu=True)
+    out = self.bn2.forward_fused(self.conv2(out), relu=True)
+    return self.bn3.forward_fused(self.conv3(out), relu=True, residual=identity)
+
+
+def fuse_resnet(model: torch.nn.Module) -> int:
+    """Fuse BN+ReLU (and the bottleneck residual add) in a torchvision ResNet; returns #blocks.
+
+    Call after swap_batchnorm.  Parameters, buffers and state_dict keys are unchanged.
+    """
+    import types
+
+    from torchvision.models.resnet import Bottleneck
+
+    if isinstance(getattr(model, "bn1", None), CrossoverBatchNorm2d) and hasattr(model, "relu"):
+        model.bn1.forward = types.MethodType(_bn_relu_forward, model.bn1)   # stem BN + ReLU
+        model.relu = torch.nn.Identity()
+    n = 0
+    for m in model.modules():
+        if isinstance(m, Bottleneck) and isinstance(m.bn3, CrossoverBatchNorm2d):
+            m.forward = types.MethodType(_bottleneck_forward, m)
+            n += 1
+    return n
 
 
 def swap_batchnorm(module: torch.nn.Module) -> int:

@@ -242,30 +242,44 @@ size_t cs_bn_workspace_bytes(int64_t M, int C) {
   return bn_workspace_bytes(M, C);
 }
 
-int cs_bn_forward(const void* x, int64_t M, int C, const float* weight, const float* bias,
-                  float* running_mean, float* running_var, float momentum, float eps,
-                  float* save_mean, float* save_invstd, float* scale_shift, void* y,
-                  void* workspace, void* stream) {
+static bool bn_shape_ok(int64_t M, int C) {
+  return M > 0 && C > 0 && C % 8 == 0 && (C <= 256 || C % 256 == 0);
+}
+
+int cs_bn_forward(const void* x, const void* residual, int64_t M, int C, const float* weight,
+                  const float* bias, float* running_mean, float* running_var, float momentum,
+                  float eps, float* save_mean, float* save_invstd, float* scale_shift, void* y,
+                  void* workspace, int flags, void* stream) {
+  const bool resid = flags & CS_BN_RESIDUAL;
   if (x == nullptr || y == nullptr || save_mean == nullptr || save_invstd == nullptr ||
-      scale_shift == nullptr || workspace == nullptr || M <= 0 || C <= 0 || C % 8 ||
-      (C > 256 && C % 256) || ((uintptr_t)x & 15u) || ((uintptr_t)y & 15u) ||
+      scale_shift == nullptr || workspace == nullptr || !bn_shape_ok(M, C) ||
+      (flags & ~(CS_BN_RELU | CS_BN_RESIDUAL)) || (resid && residual == nullptr) ||
+      (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual) & 15u) ||
       ((running_mean == nullptr) != (running_var == nullptr)))
-    return set_error(CS_ERR_ARG, "cs_bn_forward: invalid arguments (M=%lld C=%d)", (long long)M, C);
-  return cuda_status(launch_bn_fwd(x, M, C, weight, bias, running_mean, running_var, momentum, eps,
-                                   save_mean, save_invstd, scale_shift, y, workspace,
-                                   (cudaStream_t)stream),
+    return set_error(CS_ERR_ARG, "cs_bn_forward: invalid arguments (M=%lld C=%d flags=%d)",
+                     (long long)M, C, flags);
+  return cuda_status(launch_bn_fwd(x, residual, M, C, weight, bias, running_mean, running_var,
+                                   momentum, eps, save_mean, save_invstd, scale_shift, y,
+                                   workspace, flags, (cudaStream_t)stream),
                      "cs_bn_forward launch");
 }
 
-int cs_bn_backward(const void* dy, const void* x, int64_t M, int C, const float* save_mean,
-                   const float* save_invstd, const float* weight, float* grad_weight,
-                   float* grad_bias, float* coef, void* dx, void* workspace, void* stream) {
+int cs_bn_backward(const void* dy, const void* x, const void* residual, int64_t M, int C,
+                   const float* save_mean, const float* save_invstd, const float* scale_shift,
+                   const float* weight, float* grad_weight, float* grad_bias, float* coef,
+                   void* dx, void* dresidual, void* workspace, int flags, void* stream) {
+  const bool relu = flags & CS_BN_RELU, resid = flags & CS_BN_RESIDUAL;
   if (dy == nullptr || x == nullptr || dx == nullptr || save_mean == nullptr ||
-      save_invstd == nullptr || coef == nullptr || workspace == nullptr || M <= 0 || C <= 0 ||
-      C % 8 || (C > 256 && C % 256) || (((uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx) & 15u))
-    return set_error(CS_ERR_ARG, "cs_bn_backward: invalid arguments (M=%lld C=%d)", (long long)M, C);
-  return cuda_status(launch_bn_bwd(dy, x, M, C, save_mean, save_invstd, weight, grad_weight,
-                                   grad_bias, coef, dx, workspace, (cudaStream_t)stream),
+      save_invstd == nullptr || coef == nullptr || workspace == nullptr || !bn_shape_ok(M, C) ||
+      (flags & ~(CS_BN_RELU | CS_BN_RESIDUAL)) || (relu && scale_shift == nullptr) ||
+      (resid && (dresidual == nullptr || (relu && residual == nullptr))) ||
+      (((uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx | (uintptr_t)residual |
+        (uintptr_t)dresidual) & 15u))
+    return set_error(CS_ERR_ARG, "cs_bn_backward: invalid arguments (M=%lld C=%d flags=%d)",
+                     (long long)M, C, flags);
+  return cuda_status(launch_bn_bwd(dy, x, residual, M, C, save_mean, save_invstd, scale_shift,
+                                   weight, grad_weight, grad_bias, coef, dx, dresidual, workspace,
+                                   flags, (cudaStream_t)stream),
                      "cs_bn_backward launch");
 }
 

@@ -199,64 +199,120 @@ bn_fwd_finalize_kernel(const float* __restrict__ partial, int blocks, int C,
   }
 }
 
-template <bool kBwd>
-__device__ __forceinline__ uint4 apply8(const uint4& ra, const uint4& rb, const float* q1,
-                                        const float* q2, const float* q3) {
-  float fa[8], o[8];
-  unpack8(ra, fa);
-  if (kBwd) {
-    float fb[8];
-    unpack8(rb, fb);
+// Fused epilogues: kRelu = max(., 0) after the affine map, kRes = + residual before it.
+template <bool kRelu, bool kRes>
+__device__ __forceinline__ void pre_act8(const uint4& rx, const uint4& rr, const float* sc,
+                                         const float* sh, float* pre) {
+  float fx[8];
+  unpack8(rx, fx);
+  if (kRes) {
+    float fr[8];
+    unpack8(rr, fr);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = fmaf(fa[i], q1[i], fmaf(fb[i], q2[i], q3[i]));
+    for (int i = 0; i < 8; ++i) pre[i] = fmaf(fx[i], sc[i], sh[i]) + fr[i];
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = fmaf(fa[i], q1[i], q2[i]);
+    for (int i = 0; i < 8; ++i) pre[i] = fmaf(fx[i], sc[i], sh[i]);
   }
-  return pack8(o);
 }
 
-// y = x * scale + shift  |  dx = dy * k1 + x * k2 + k3
-template <bool kBwd>
+// y = act(x * scale + shift [+ residual])
+template <bool kRelu, bool kRes>
 __global__ void __launch_bounds__(kBnThreads)
-bn_apply_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ b,
-                int64_t M, int C, const float* __restrict__ k1, const float* __restrict__ k2,
-                const float* __restrict__ k3, __nv_bfloat16* __restrict__ out) {
+bn_fwd_apply_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
+                    int64_t M, int C, const float* __restrict__ scale,
+                    const float* __restrict__ shift, __nv_bfloat16* __restrict__ y) {
   const int64_t vecs = M * (C / 8);
   const int cv = C / 8;
   const int64_t stride = (int64_t)gridDim.x * kBnThreads;   // multiple of cv (host guarantees)
   const int64_t v0 = (int64_t)blockIdx.x * kBnThreads + threadIdx.x;
   const int c = (int)(v0 % cv) * 8;
-  float q1[8], q2[8], q3[8];
+  float sc[8], sh[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    q1[i] = k1[c + i];
-    q2[i] = k2[c + i];
-    q3[i] = kBwd ? k3[c + i] : 0.f;
-  }
+  for (int i = 0; i < 8; ++i) { sc[i] = scale[c + i]; sh[i] = shift[c + i]; }
   const uint4 zero = make_uint4(0, 0, 0, 0);
   int64_t v = v0;
   for (; v + stride < vecs; v += 2 * stride) {
-    const uint4 ra0 = ld_nc16(a + v * 8), ra1 = ld_nc16(a + (v + stride) * 8);
-    const uint4 rb0 = kBwd ? ld_nc16(b + v * 8) : zero;
-    const uint4 rb1 = kBwd ? ld_nc16(b + (v + stride) * 8) : zero;
-    *reinterpret_cast<uint4*>(out + v * 8) = apply8<kBwd>(ra0, rb0, q1, q2, q3);
-    *reinterpret_cast<uint4*>(out + (v + stride) * 8) = apply8<kBwd>(ra1, rb1, q1, q2, q3);
+    const uint4 rx0 = ld_nc16(x + v * 8), rx1 = ld_nc16(x + (v + stride) * 8);
+    const uint4 rr0 = kRes ? ld_nc16(res + v * 8) : zero;
+    const uint4 rr1 = kRes ? ld_nc16(res + (v + stride) * 8) : zero;
+    float p[8];
+    pre_act8<kRelu, kRes>(rx0, rr0, sc, sh, p);
+    if (kRelu) for (int i = 0; i < 8; ++i) p[i] = fmaxf(p[i], 0.f);
+    *reinterpret_cast<uint4*>(y + v * 8) = pack8(p);
+    pre_act8<kRelu, kRes>(rx1, rr1, sc, sh, p);
+    if (kRelu) for (int i = 0; i < 8; ++i) p[i] = fmaxf(p[i], 0.f);
+    *reinterpret_cast<uint4*>(y + (v + stride) * 8) = pack8(p);
   }
   for (; v < vecs; v += stride) {
-    const uint4 ra = ld_nc16(a + v * 8);
-    const uint4 rb = kBwd ? ld_nc16(b + v * 8) : zero;
-    *reinterpret_cast<uint4*>(out + v * 8) = apply8<kBwd>(ra, rb, q1, q2, q3);
+    const uint4 rx = ld_nc16(x + v * 8);
+    const uint4 rr = kRes ? ld_nc16(res + v * 8) : zero;
+    float p[8];
+    pre_act8<kRelu, kRes>(rx, rr, sc, sh, p);
+    if (kRelu) for (int i = 0; i < 8; ++i) p[i] = fmaxf(p[i], 0.f);
+    *reinterpret_cast<uint4*>(y + v * 8) = pack8(p);
+  }
+}
+
+// g = dy masked by the forward activation (recomputed from x [, residual]; nothing stored)
+template <bool kRelu, bool kRes>
+__device__ __forceinline__ void masked_grad8(const uint4& rg, const uint4& rx, const uint4& rr,
+                                             const float* sc, const float* sh, float* g) {
+  unpack8(rg, g);
+  if (kRelu) {
+    float p[8];
+    pre_act8<kRelu, kRes>(rx, rr, sc, sh, p);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = p[i] > 0.f ? g[i] : 0.f;
+  }
+}
+
+// dx = g * k1 + x * k2 + k3 ; dres = g (kRes)
+template <bool kRelu, bool kRes>
+__global__ void __launch_bounds__(kBnThreads)
+bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                    const __nv_bfloat16* __restrict__ res, int64_t M, int C,
+                    const float* __restrict__ coef, const float* __restrict__ scale,
+                    const float* __restrict__ shift, __nv_bfloat16* __restrict__ dx,
+                    __nv_bfloat16* __restrict__ dres) {
+  const int64_t vecs = M * (C / 8);
+  const int cv = C / 8;
+  const int64_t stride = (int64_t)gridDim.x * kBnThreads;
+  const int64_t v0 = (int64_t)blockIdx.x * kBnThreads + threadIdx.x;
+  const int c = (int)(v0 % cv) * 8;
+  float q1[8], q2[8], q3[8], sc[8], sh[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    q1[i] = coef[c + i];
+    q2[i] = coef[C + c + i];
+    q3[i] = coef[2 * C + c + i];
+    sc[i] = kRelu ? scale[c + i] : 0.f;
+    sh[i] = kRelu ? shift[c + i] : 0.f;
+  }
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  for (int64_t v = v0; v < vecs; v += stride) {
+    const uint4 rg = ld_nc16(dy + v * 8);
+    const uint4 rx = ld_nc16(x + v * 8);
+    const uint4 rr = (kRes && kRelu) ? ld_nc16(res + v * 8) : zero;
+    float g[8], fx[8], o[8];
+    masked_grad8<kRelu, kRes>(rg, rx, rr, sc, sh, g);
+    unpack8(rx, fx);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = fmaf(g[i], q1[i], fmaf(fx[i], q2[i], q3[i]));
+    *reinterpret_cast<uint4*>(dx + v * 8) = pack8(o);
+    if (kRes) *reinterpret_cast<uint4*>(dres + v * 8) = pack8(g);
   }
 }
 
 // ---------------------------------------------------------------------------
 // backward: sum(dy), sum(dy * (x - mean)) per channel
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void bwd_acc8(const uint4& rg, const uint4& rx, const float* mu,
+template <bool kRelu, bool kRes>
+__device__ __forceinline__ void bwd_acc8(const uint4& rg, const uint4& rx, const uint4& rr,
+                                         const float* mu, const float* sc, const float* sh,
                                          float* sdy, float* sdx) {
   float g[8], v[8];
-  unpack8(rg, g);
+  masked_grad8<kRelu, kRes>(rg, rx, rr, sc, sh, g);
   unpack8(rx, v);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -265,31 +321,42 @@ __device__ __forceinline__ void bwd_acc8(const uint4& rg, const uint4& rx, const
   }
 }
 
+template <bool kRelu, bool kRes>
 __global__ void __launch_bounds__(kBnThreads)
 bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                      int64_t M, int C, const float* __restrict__ save_mean,
-                      float* __restrict__ partial) {
+                      const __nv_bfloat16* __restrict__ res, int64_t M, int C,
+                      const float* __restrict__ save_mean, const float* __restrict__ scale,
+                      const float* __restrict__ shift, float* __restrict__ partial) {
   const TileShape s = tile_shape(C);
   const int tx = threadIdx.x % s.tx, ty = threadIdx.x / s.tx;
   const int c0 = blockIdx.y * s.tile + tx * 8;
   const int64_t rows_per = (M + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
-  float mu[8], sdy[8], sdx[8];
+  float mu[8], sdy[8], sdx[8], sc[8], sh[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { mu[i] = save_mean[c0 + i]; sdy[i] = 0.f; sdx[i] = 0.f; }
+  for (int i = 0; i < 8; ++i) {
+    mu[i] = save_mean[c0 + i]; sdy[i] = 0.f; sdx[i] = 0.f;
+    sc[i] = kRelu ? scale[c0 + i] : 0.f;
+    sh[i] = kRelu ? shift[c0 + i] : 0.f;
+  }
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  constexpr bool kLoadRes = kRes && kRelu;
   int64_t r = r0 + ty;
   for (; r + (kRowUnroll - 1) * s.ty < r1; r += kRowUnroll * s.ty) {
-    uint4 rg[kRowUnroll], rx[kRowUnroll];
+    uint4 rg[kRowUnroll], rx[kRowUnroll], rr[kRowUnroll];
 #pragma unroll
     for (int u = 0; u < kRowUnroll; ++u) {
       rg[u] = ld_nc16(dy + (r + u * s.ty) * C + c0);
       rx[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
+      rr[u] = kLoadRes ? ld_nc16(res + (r + u * s.ty) * C + c0) : zero;
     }
 #pragma unroll
-    for (int u = 0; u < kRowUnroll; ++u) bwd_acc8(rg[u], rx[u], mu, sdy, sdx);
+    for (int u = 0; u < kRowUnroll; ++u) bwd_acc8<kRelu, kRes>(rg[u], rx[u], rr[u], mu, sc, sh, sdy, sdx);
   }
-  for (; r < r1; r += s.ty) bwd_acc8(ld_nc16(dy + r * C + c0), ld_nc16(x + r * C + c0), mu, sdy, sdx);
+  for (; r < r1; r += s.ty)
+    bwd_acc8<kRelu, kRes>(ld_nc16(dy + r * C + c0), ld_nc16(x + r * C + c0),
+                          kLoadRes ? ld_nc16(res + r * C + c0) : zero, mu, sc, sh, sdy, sdx);
 
   __shared__ float s_dy[kBnThreads * 8], s_dx[kBnThreads * 8];
 #pragma unroll
@@ -389,10 +456,17 @@ static unsigned apply_grid(int64_t M, int C) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
-cudaError_t launch_bn_fwd(const void* x, int64_t M, int C, const float* w, const float* b,
-                          float* rm, float* rv, float momentum, float eps, float* save_mean,
-                          float* save_invstd, float* scale_shift, void* y, void* ws,
-                          cudaStream_t s) {
+template <bool kRelu, bool kRes>
+static void fwd_apply(const void* x, const void* res, int64_t M, int C, const float* scale,
+                      const float* shift, void* y, cudaStream_t s) {
+  bn_fwd_apply_kernel<kRelu, kRes><<<apply_grid(M, C), kBnThreads, 0, s>>>(
+      (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C, scale, shift, (__nv_bfloat16*)y);
+}
+
+cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, const float* w,
+                          const float* b, float* rm, float* rv, float momentum, float eps,
+                          float* save_mean, float* save_invstd, float* scale_shift, void* y,
+                          void* ws, int flags, cudaStream_t s) {
   const TileShape sh = tile_shape(C);
   const int blocks = bn_row_blocks(M, C);
   float* partial = (float*)((char*)ws + 256);
@@ -407,19 +481,27 @@ cudaError_t launch_bn_fwd(const void* x, int64_t M, int C, const float* w, const
                                                              scale, shift);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  bn_apply_kernel<false><<<apply_grid(M, C), kBnThreads, 0, s>>>(
-      (const __nv_bfloat16*)x, nullptr, M, C, scale, shift, nullptr, (__nv_bfloat16*)y);
+  const bool relu = flags & CS_BN_RELU, resid = flags & CS_BN_RESIDUAL;
+  if (relu && resid) fwd_apply<true, true>(x, res, M, C, scale, shift, y, s);
+  else if (relu) fwd_apply<true, false>(x, res, M, C, scale, shift, y, s);
+  else if (resid) fwd_apply<false, true>(x, res, M, C, scale, shift, y, s);
+  else fwd_apply<false, false>(x, res, M, C, scale, shift, y, s);
   return cudaGetLastError();
 }
 
-cudaError_t launch_bn_bwd(const void* dy, const void* x, int64_t M, int C, const float* save_mean,
-                          const float* save_invstd, const float* w, float* gw, float* gb,
-                          float* coef, void* dx, void* ws, cudaStream_t s) {
+template <bool kRelu, bool kRes>
+static cudaError_t bwd_impl(const void* dy, const void* x, const void* res, int64_t M, int C,
+                            const float* save_mean, const float* save_invstd,
+                            const float* scale_shift, const float* w, float* gw, float* gb,
+                            float* coef, void* dx, void* dres, void* ws, cudaStream_t s) {
   const TileShape sh = tile_shape(C);
   const int blocks = bn_row_blocks(M, C);
   float* partial = (float*)((char*)ws + 256);
-  bn_bwd_partial_kernel<<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, M, C, save_mean, partial);
+  const float* scale = scale_shift;
+  const float* shift = scale_shift ? scale_shift + C : nullptr;
+  bn_bwd_partial_kernel<kRelu, kRes><<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C,
+      save_mean, scale, shift, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   bn_bwd_finalize_kernel<<<(C + 7) / 8, kBnThreads, 0, s>>>(partial, blocks, M, C, save_mean,
@@ -427,10 +509,24 @@ cudaError_t launch_bn_bwd(const void* dy, const void* x, int64_t M, int C, const
                                                              coef + C, coef + 2 * C);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  bn_apply_kernel<true><<<apply_grid(M, C), kBnThreads, 0, s>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, M, C, coef, coef + C, coef + 2 * C,
-      (__nv_bfloat16*)dx);
+  bn_bwd_apply_kernel<kRelu, kRes><<<apply_grid(M, C), kBnThreads, 0, s>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C, coef,
+      scale, shift, (__nv_bfloat16*)dx, (__nv_bfloat16*)dres);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bn_bwd(const void* dy, const void* x, const void* res, int64_t M, int C,
+                          const float* save_mean, const float* save_invstd,
+                          const float* scale_shift, const float* w, float* gw, float* gb,
+                          float* coef, void* dx, void* dres, void* ws, int flags, cudaStream_t s) {
+  const bool relu = flags & CS_BN_RELU, resid = flags & CS_BN_RESIDUAL;
+  if (relu && resid)
+    return bwd_impl<true, true>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+  if (relu)
+    return bwd_impl<true, false>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+  if (resid)
+    return bwd_impl<false, true>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+  return bwd_impl<false, false>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
 }
 
 }  // namespace cs

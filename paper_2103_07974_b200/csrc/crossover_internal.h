@@ -72,13 +72,14 @@ int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s);
 int bn_row_blocks(int64_t M, int C);
 size_t bn_workspace_bytes(int64_t M, int C);
-cudaError_t launch_bn_fwd(const void* x, int64_t M, int C, const float* w, const float* b,
-                          float* rm, float* rv, float momentum, float eps, float* save_mean,
-                          float* save_invstd, float* scale_shift, void* y, void* ws,
-                          cudaStream_t s);
-cudaError_t launch_bn_bwd(const void* dy, const void* x, int64_t M, int C, const float* save_mean,
-                          const float* save_invstd, const float* w, float* gw, float* gb,
-                          float* coef, void* dx, void* ws, cudaStream_t s);
+cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, const float* w,
+                          const float* b, float* rm, float* rv, float momentum, float eps,
+                          float* save_mean, float* save_invstd, float* scale_shift, void* y,
+                          void* ws, int flags, cudaStream_t s);
+cudaError_t launch_bn_bwd(const void* dy, const void* x, const void* res, int64_t M, int C,
+                          const float* save_mean, const float* save_invstd,
+                          const float* scale_shift, const float* w, float* gw, float* gb,
+                          float* coef, void* dx, void* dres, void* ws, int flags, cudaStream_t s);
 cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
                          cudaStream_t s);
 int stats_grid(int64_t numel);

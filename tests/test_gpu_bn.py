@@ -94,3 +94,59 @@ def test_resnet50_fast_bn_graphed_pipeline(cuda_device):
     assert validate_trace(tr) == []
     losses = [float(l) for st in s.states for l in st.losses]
     assert all(0 < l < 20 for l in losses)
+
+
+@pytest.mark.parametrize("relu,residual", [(True, False), (True, True), (False, True)])
+def test_bn_fused_epilogues_match_torch(cuda_device, relu, residual):
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d
+
+    torch.manual_seed(3)
+    shape = (8, 256, 14, 14)
+    c = shape[1]
+    cl = dict(memory_format=torch.channels_last)
+    x = torch.randn(shape, device=cuda_device).to(torch.bfloat16).contiguous(**cl)
+    r = torch.randn(shape, device=cuda_device).to(torch.bfloat16).contiguous(**cl)
+    dy = torch.randn(shape, device=cuda_device).to(torch.bfloat16).contiguous(**cl)
+    bn = CrossoverBatchNorm2d(c).to(cuda_device)
+    ref = torch.nn.BatchNorm2d(c).to(cuda_device)
+    xa, ra = x.clone().requires_grad_(True), r.clone().requires_grad_(True)
+    xb, rb = x.float().requires_grad_(True), r.float().requires_grad_(True)
+    y = bn.forward_fused(xa, relu=relu, residual=ra if residual else None)
+    yr = ref(xb) + (rb if residual else 0)
+    if relu:
+        yr = torch.relu(yr)
+    torch.testing.assert_close(y.float(), yr.to(torch.bfloat16).float(), rtol=2e-2, atol=3e-2)
+    y.backward(dy)
+    yr.backward(dy.float())
+    sc = xb.grad.abs().max().item()
+    torch.testing.assert_close(xa.grad.float(), xb.grad, rtol=2e-2, atol=2e-2 * sc + 1e-6)
+    if residual:
+        torch.testing.assert_close(ra.grad.float(), rb.grad, rtol=1e-2, atol=1e-2)
+    torch.testing.assert_close(bn.weight.grad, ref.weight.grad, rtol=5e-3,
+                               atol=2e-3 * ref.weight.grad.abs().max().item() + 1e-4)
+
+
+def test_fused_resnet_matches_unfused(cuda_device):
+    """fuse_resnet changes kernels, not math: same loss and close grads as the unfused swap."""
+    import copy
+
+    import torchvision
+
+    from paper_2103_07974_b200.bn import fuse_resnet, swap_batchnorm
+
+    torch.manual_seed(0)
+    m0 = torchvision.models.resnet50()
+    swap_batchnorm(m0)
+    m1 = copy.deepcopy(m0)
+    assert fuse_resnet(m1) == 16
+    x = torch.randn(4, 3, 64, 64, device=cuda_device).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    outs = []
+    for m in (m0, m1):
+        m = m.to(cuda_device).to(memory_format=torch.channels_last)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = m(x).float().square().mean()
+        g = torch.autograd.grad(loss, [m.conv1.weight, m.fc.weight])
+        outs.append((loss.detach(), g))
+    torch.testing.assert_close(outs[0][0], outs[1][0], rtol=2e-2, atol=1e-3)
+    for a, b in zip(outs[0][1], outs[1][1]):
+        torch.testing.assert_close(a, b, rtol=5e-2, atol=5e-2 * b.abs().max().item())
