@@ -75,14 +75,14 @@ EXPORTS = {
     "cs_ipc_open_handle": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "cs_ipc_close_handle": ([ctypes.c_void_p], ctypes.c_int),
     "cs_bn_workspace_bytes": ([ctypes.c_int64, ctypes.c_int], ctypes.c_size_t),
-    "cs_bn_forward": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float, ctypes.c_float,
+    "cs_bn_forward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float, ctypes.c_float,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                       ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
-    "cs_bn_backward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                       ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "cs_bn_backward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                        ctypes.c_void_p], ctypes.c_int),
+                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_version": ([], ctypes.c_int),
     "cs_nccl_get_unique_id": ([ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_init": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int,

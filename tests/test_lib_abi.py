@@ -46,6 +46,7 @@ def test_struct_layouts():
     from paper_2103_07974_b200 import _lib
 
     assert _lib.PACK_DESC.itemsize == 24
+    assert ctypes.sizeof(_lib.P2PDesc) == 8 * 8 * 2 + 8 + 8 + 8 + 8
     assert _lib.UPDATE_DESC.itemsize == 40
     assert ctypes.sizeof(_lib.SgdHyper) == 32
     assert _lib.lib.cs_abi_version() == 1
@@ -71,6 +72,15 @@ def test_argument_errors_without_gpu():
     assert _lib.lib.cs_unpack_sgd(u.ctypes.data, 1, np.zeros(9, dtype=np.uint64).ctypes.data, 9,
                                   None, ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=1)), None) == _lib.CS_ERR_ARG
     assert _lib.lib.cs_nccl_init(None, 0, 0, None, 0, 0) == _lib.CS_ERR_ARG
+    # BN: channel counts the kernels do not support are rejected before any launch
+    assert _lib.lib.cs_bn_workspace_bytes(100, 7) == 0
+    assert _lib.lib.cs_bn_forward(16, None, 100, 7, None, None, None, None, 0.1, 1e-5, 16, 16, 16, 16,
+                                  16, 0, None) == _lib.CS_ERR_ARG
+    assert b"cs_bn_forward" in _lib.lib.cs_last_error()
+    p2p = _lib.P2PDesc()
+    p2p.nranks = 9
+    assert _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(p2p), ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=9)),
+                                            None) == _lib.CS_ERR_ARG
 
 
 def test_nccl_version_is_torchs():
