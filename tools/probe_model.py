@@ -14,15 +14,17 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def run(model_name="resnet50", batch=256, fmt="cl", graph=False, iters=10, fast_bn=False):
+def run(model_name="resnet50", batch=256, fmt="cl", graph=False, iters=10, fast_bn=False, fuse=False):
     import torchvision
 
     dev = torch.device("cuda", 0)
     torch.backends.cudnn.benchmark = True
     m = getattr(torchvision.models, model_name)()
     if fast_bn:
-        from paper_2103_07974_b200.bn import swap_batchnorm
+        from paper_2103_07974_b200.bn import fuse_resnet, swap_batchnorm
         swap_batchnorm(m)
+        if fuse:
+            fuse_resnet(m)
     m = m.to(dev)
     mf = torch.channels_last if fmt == "cl" else torch.contiguous_format
     m = m.to(memory_format=mf)
@@ -64,10 +66,10 @@ def run(model_name="resnet50", batch=256, fmt="cl", graph=False, iters=10, fast_
 
 if __name__ == "__main__":
     for model in sys.argv[1:] or ["resnet50"]:
-        for fmt, graph, fast in (("cl", False, False), ("cl", True, False), ("cl", False, True), ("cl", True, True)):
+        for fmt, graph, fast, fuse in (("cl", True, False, False), ("cl", True, True, False), ("cl", True, True, True)):
                 try:
-                    gpu, cpu = run(model, fmt=fmt, graph=graph, fast_bn=fast)
-                    print(f"{model} fmt={fmt} graph={graph} fast_bn={fast}: {gpu:.2f} ms/iter GPU, {cpu:.2f} ms host issue, "
+                    gpu, cpu = run(model, fmt=fmt, graph=graph, fast_bn=fast, fuse=fuse)
+                    print(f"{model} graph={graph} fast_bn={fast} fused={fuse}: {gpu:.2f} ms/iter GPU, {cpu:.2f} ms host issue, "
                           f"{256 / gpu * 1e3:.0f} img/s", flush=True)
                 except Exception as e:  # noqa: BLE001
                     print(f"{model} fmt={fmt} graph={graph}: FAILED {type(e).__name__}: {str(e)[:200]}", flush=True)
