@@ -126,8 +126,10 @@ def test_bn_fused_epilogues_match_torch(cuda_device, relu, residual):
                                atol=2e-3 * ref.weight.grad.abs().max().item() + 1e-4)
 
 
-def test_fused_resnet_matches_unfused(cuda_device):
-    """fuse_resnet changes kernels, not math: same loss and close grads as the unfused swap."""
+def test_fused_resnet_no_less_accurate_than_aten(cuda_device):
+    """Whole ResNet-50 in bf16: a random-init net's early-layer gradients are ill-conditioned
+    (ATen bf16 itself is O(1) off the fp32 gradients there), so the bar is relative: our
+    swapped and fused BN models must be as close to the fp32 reference as ATen's bf16 run."""
     import copy
 
     import torchvision
@@ -135,18 +137,29 @@ def test_fused_resnet_matches_unfused(cuda_device):
     from paper_2103_07974_b200.bn import fuse_resnet, swap_batchnorm
 
     torch.manual_seed(0)
-    m0 = torchvision.models.resnet50()
-    swap_batchnorm(m0)
-    m1 = copy.deepcopy(m0)
-    assert fuse_resnet(m1) == 16
-    x = torch.randn(4, 3, 64, 64, device=cuda_device).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
-    outs = []
-    for m in (m0, m1):
+    m_swap = torchvision.models.resnet50()
+    swap_batchnorm(m_swap)
+    m_fused = copy.deepcopy(m_swap)
+    assert fuse_resnet(m_fused) == 16
+    aten = torchvision.models.resnet50()
+    aten.load_state_dict(m_swap.state_dict())
+    aten32 = copy.deepcopy(aten)
+    x = torch.randn(16, 3, 224, 224, device=cuda_device).to(torch.bfloat16).contiguous(
+        memory_format=torch.channels_last)
+    keys = ["conv1.weight", "layer1.0.conv1.weight", "layer3.0.bn1.weight", "layer4.2.bn3.weight",
+            "fc.weight", "fc.bias"]
+    res = []
+    for m, amp in ((aten32, False), (aten, True), (m_swap, True), (m_fused, True)):
         m = m.to(cuda_device).to(memory_format=torch.channels_last)
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            loss = m(x).float().square().mean()
-        g = torch.autograd.grad(loss, [m.conv1.weight, m.fc.weight])
-        outs.append((loss.detach(), g))
-    torch.testing.assert_close(outs[0][0], outs[1][0], rtol=2e-2, atol=1e-3)
-    for a, b in zip(outs[0][1], outs[1][1]):
-        torch.testing.assert_close(a, b, rtol=5e-2, atol=5e-2 * b.abs().max().item())
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=amp):
+            loss = m(x if amp else x.float()).float().square().mean()
+        named = dict(m.named_parameters())
+        g = torch.autograd.grad(loss, [named[k] for k in keys])
+        res.append((loss.item(), g))
+    for k in range(len(keys)):
+        ref = res[0][1][k].float()
+        sc = ref.abs().max().item()
+        err = [((r[1][k].float() - ref).abs().max().item()) / sc for r in res[1:]]
+        assert err[1] <= 1.5 * err[0] + 0.05 and err[2] <= 1.5 * err[0] + 0.05, (keys[k], err)
+    assert abs(res[2][0] - res[0][0]) <= 2 * abs(res[1][0] - res[0][0]) + 1e-3
+    assert abs(res[3][0] - res[0][0]) <= 2 * abs(res[1][0] - res[0][0]) + 1e-3
