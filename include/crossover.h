@@ -185,6 +185,14 @@ CS_API int cs_bn_backward(const void* dy, const void* x, const void* residual, i
                           float* grad_bias, float* coef, void* dx, void* dresidual,
                           void* workspace, int flags, void* stream);
 
+/* channels_last max pooling (bf16, C % 8 == 0, no dilation / ceil mode).
+ * shape = {N, H, W, C, OH, OW, kh, kw, sh, sw, ph, pw}; argmax: uint8 [N*OH*OW*C] window
+ * offsets (kh*kw <= 256) written by the forward, read by the backward (dx is fully written). */
+CS_API int cs_maxpool2d_forward(const void* x, void* y, uint8_t* argmax, const int* shape,
+                                void* stream);
+CS_API int cs_maxpool2d_backward(const void* dy, const uint8_t* argmax, void* dx,
+                                 const int* shape, void* stream);
+
 /* NCCL communicator over NVLink / NVSwitch (one per process, one per job set).
  * min_ctas / max_ctas <= 0 leave NCCL's defaults. */
 CS_API int cs_nccl_version(void);

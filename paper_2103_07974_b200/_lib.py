@@ -83,6 +83,10 @@ EXPORTS = {
                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "cs_maxpool2d_forward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p], ctypes.c_int),
+    "cs_maxpool2d_backward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_version": ([], ctypes.c_int),
     "cs_nccl_get_unique_id": ([ctypes.c_void_p], ctypes.c_int),
     "cs_nccl_init": ([ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int,

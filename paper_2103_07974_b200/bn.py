@@ -17,7 +17,8 @@ import torch
 
 from . import _lib
 
-__all__ = ["CrossoverBatchNorm2d", "swap_batchnorm", "fuse_resnet", "bn_supported"]
+__all__ = ["CrossoverBatchNorm2d", "CrossoverMaxPool2d", "swap_batchnorm", "fuse_resnet",
+           "bn_supported"]
 
 
 def _ptr(t: torch.Tensor | None):
@@ -129,6 +130,50 @@ def _bottleneck_forward(self, x):
     return self.bn3.forward_fused(self.conv3(out), relu=True, residual=identity)
 
 
+class _MaxPoolFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, k, s, p):
+        n, c, h, w = x.shape
+        oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        x = x.contiguous(memory_format=torch.channels_last)
+        y = torch.empty((n, c, oh, ow), dtype=x.dtype, device=x.device,
+                        memory_format=torch.channels_last)
+        arg = torch.empty(n * oh * ow * c, dtype=torch.uint8, device=x.device)
+        shape = (ctypes.c_int * 12)(n, h, w, c, oh, ow, k, k, s, s, p, p)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        _lib.check("cs_maxpool2d_forward", _lib.lib.cs_maxpool2d_forward(
+            x.data_ptr(), y.data_ptr(), arg.data_ptr(), shape, stream))
+        ctx.save_for_backward(arg)
+        ctx.meta = (n, c, h, w, oh, ow, k, s, p)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (arg,) = ctx.saved_tensors
+        n, c, h, w, oh, ow, k, s, p = ctx.meta
+        dy = dy.contiguous(memory_format=torch.channels_last)
+        dx = torch.empty((n, c, h, w), dtype=dy.dtype, device=dy.device,
+                         memory_format=torch.channels_last)
+        shape = (ctypes.c_int * 12)(n, h, w, c, oh, ow, k, k, s, s, p, p)
+        stream = torch.cuda.current_stream(dy.device).cuda_stream
+        _lib.check("cs_maxpool2d_backward", _lib.lib.cs_maxpool2d_backward(
+            dy.data_ptr(), arg.data_ptr(), dx.data_ptr(), shape, stream))
+        return dx, None, None, None
+
+
+class CrossoverMaxPool2d(torch.nn.MaxPool2d):
+    """nn.MaxPool2d (square kernel, no dilation / ceil mode) with the NHWC kernels on bf16 CUDA input."""
+
+    def forward(self, x):
+        k, s, p = self.kernel_size, self.stride, self.padding
+        simple = (isinstance(k, int) and isinstance(s, int) and isinstance(p, int)
+                  and self.dilation == 1 and not self.ceil_mode and not self.return_indices)
+        if not (simple and x.is_cuda and x.dtype == torch.bfloat16 and x.dim() == 4
+                and x.shape[1] % 8 == 0 and k * k <= 256):
+            return super().forward(x)
+        return _MaxPoolFunction.apply(x, k, s, p)
+
+
 def fuse_resnet(model: torch.nn.Module) -> int:
     """Fuse BN+ReLU (and the bottleneck residual add) in a torchvision ResNet; returns #blocks.
 
@@ -141,6 +186,10 @@ def fuse_resnet(model: torch.nn.Module) -> int:
     if isinstance(getattr(model, "bn1", None), CrossoverBatchNorm2d) and hasattr(model, "relu"):
         model.bn1.forward = types.MethodType(_bn_relu_forward, model.bn1)   # stem BN + ReLU
         model.relu = torch.nn.Identity()
+    mp = getattr(model, "maxpool", None)
+    if type(mp) is torch.nn.MaxPool2d:
+        model.maxpool = CrossoverMaxPool2d(mp.kernel_size, mp.stride, mp.padding, mp.dilation,
+                                           mp.return_indices, mp.ceil_mode)
     n = 0
     for m in model.modules():
         if isinstance(m, Bottleneck) and isinstance(m.bn3, CrossoverBatchNorm2d):

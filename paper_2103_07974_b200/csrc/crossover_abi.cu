@@ -283,6 +283,31 @@ int cs_bn_backward(const void* dy, const void* x, const void* residual, int64_t 
                      "cs_bn_backward launch");
 }
 
+static bool pool_shape_ok(const int* s) {
+  if (s == nullptr) return false;
+  for (int i = 0; i < 10; ++i)
+    if (s[i] <= 0) return false;
+  if (s[10] < 0 || s[11] < 0 || s[3] % 8 || s[6] * s[7] > 256) return false;
+  return s[4] == (s[1] + 2 * s[10] - s[6]) / s[8] + 1 && s[5] == (s[2] + 2 * s[11] - s[7]) / s[9] + 1;
+}
+
+int cs_maxpool2d_forward(const void* x, void* y, uint8_t* argmax, const int* shape, void* stream) {
+  if (x == nullptr || y == nullptr || argmax == nullptr || !pool_shape_ok(shape) ||
+      (((uintptr_t)x | (uintptr_t)y) & 15u) || ((uintptr_t)argmax & 7u))
+    return set_error(CS_ERR_ARG, "cs_maxpool2d_forward: invalid arguments");
+  return cuda_status(launch_maxpool_fwd(x, y, argmax, shape, (cudaStream_t)stream),
+                     "cs_maxpool2d_forward launch");
+}
+
+int cs_maxpool2d_backward(const void* dy, const uint8_t* argmax, void* dx, const int* shape,
+                          void* stream) {
+  if (dy == nullptr || dx == nullptr || argmax == nullptr || !pool_shape_ok(shape) ||
+      (((uintptr_t)dy | (uintptr_t)dx) & 15u) || ((uintptr_t)argmax & 7u))
+    return set_error(CS_ERR_ARG, "cs_maxpool2d_backward: invalid arguments");
+  return cuda_status(launch_maxpool_bwd(dy, argmax, dx, shape, (cudaStream_t)stream),
+                     "cs_maxpool2d_backward launch");
+}
+
 size_t cs_gradient_stats_workspace_bytes(int64_t numel) {
   return 256 + (size_t)stats_grid(numel) * 2 * sizeof(double);
 }

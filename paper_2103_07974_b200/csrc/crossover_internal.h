@@ -80,6 +80,9 @@ cudaError_t launch_bn_bwd(const void* dy, const void* x, const void* res, int64_
                           const float* save_mean, const float* save_invstd,
                           const float* scale_shift, const float* w, float* gw, float* gb,
                           float* coef, void* dx, void* dres, void* ws, int flags, cudaStream_t s);
+cudaError_t launch_maxpool_fwd(const void* x, void* y, void* arg, const int* shape, cudaStream_t st);
+cudaError_t launch_maxpool_bwd(const void* dy, const void* arg, void* dx, const int* shape,
+                               cudaStream_t st);
 cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
                          cudaStream_t s);
 int stats_grid(int64_t numel);

@@ -1,0 +1,154 @@
+// crossover_pool.cu -- channels_last max pooling for the apps' compute (ResNet stem).
+//
+// ATen's NHWC max_pool2d kernels took ~2.5 ms of every ResNet-50 bs256 iteration
+// (profiles/r01_launches_fastbn.md) and save int64 indices (8 bytes per output element).
+// Here the forward stores the argmax as a uint8 window offset (kh*kw <= 255) and the backward
+// is a gather: every input element sums dy over the (at most ceil(k/s)^2) windows that
+// selected it.  Scan order and comparison match ATen (row-major window scan, first strictly
+// greater value wins, NaN propagates), so the selected positions -- and therefore dx -- are
+// identical.  8 channels (16 bytes of bf16) per thread.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "crossover.h"
+#include "crossover_internal.h"
+
+namespace cs {
+
+namespace {
+constexpr int kPoolThreads = 256;
+
+__device__ __forceinline__ void unpack8p(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 v = __bfloat1622float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8p(const float* f) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+}  // namespace
+
+struct PoolShape {
+  int N, H, W, C, OH, OW, kh, kw, sh, sw, ph, pw;
+};
+
+__global__ void __launch_bounds__(kPoolThreads)
+maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                   uint8_t* __restrict__ arg, PoolShape s) {
+  const int cv = s.C / 8;
+  const int64_t total = (int64_t)s.N * s.OH * s.OW * cv;
+  for (int64_t i = (int64_t)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * kPoolThreads) {
+    const int c8 = (int)(i % cv);
+    int64_t t = i / cv;
+    const int ow = (int)(t % s.OW);
+    t /= s.OW;
+    const int oh = (int)(t % s.OH);
+    const int n = (int)(t / s.OH);
+    float best[8];
+    uint8_t idx[8];
+    const int h0 = oh * s.sh - s.ph, w0 = ow * s.sw - s.pw;
+    // ATen starts from the first in-bounds position of the window
+    const uint8_t first = (uint8_t)(max(0, -h0) * s.kw + max(0, -w0));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { best[k] = -INFINITY; idx[k] = first; }
+    for (int a = 0; a < s.kh; ++a) {
+      const int ih = h0 + a;
+      if (ih < 0 || ih >= s.H) continue;
+      for (int b = 0; b < s.kw; ++b) {
+        const int iw = w0 + b;
+        if (iw < 0 || iw >= s.W) continue;
+        float v[8];
+        unpack8p(*reinterpret_cast<const uint4*>(x + (((int64_t)n * s.H + ih) * s.W + iw) * s.C + c8 * 8), v);
+        const uint8_t o = (uint8_t)(a * s.kw + b);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (v[k] > best[k] || isnan(v[k])) { best[k] = v[k]; idx[k] = o; }   // ATen's rule
+      }
+    }
+    *reinterpret_cast<uint4*>(y + i * 8) = pack8p(best);
+    uint2 packed;
+    packed.x = idx[0] | (idx[1] << 8) | (idx[2] << 16) | ((uint32_t)idx[3] << 24);
+    packed.y = idx[4] | (idx[5] << 8) | (idx[6] << 16) | ((uint32_t)idx[7] << 24);
+    *reinterpret_cast<uint2*>(arg + i * 8) = packed;
+  }
+}
+
+__global__ void __launch_bounds__(kPoolThreads)
+maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
+                   __nv_bfloat16* __restrict__ dx, PoolShape s) {
+  const int cv = s.C / 8;
+  const int64_t total = (int64_t)s.N * s.H * s.W * cv;
+  for (int64_t i = (int64_t)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * kPoolThreads) {
+    const int c8 = (int)(i % cv);
+    int64_t t = i / cv;
+    const int iw = (int)(t % s.W);
+    t /= s.W;
+    const int ih = (int)(t % s.H);
+    const int n = (int)(t / s.H);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    // output windows containing (ih, iw): oh*sh - ph <= ih < oh*sh - ph + kh
+    const int oh_lo = max(0, (ih + s.ph - s.kh + s.sh) / s.sh);
+    const int oh_hi = min(s.OH - 1, (ih + s.ph) / s.sh);
+    const int ow_lo = max(0, (iw + s.pw - s.kw + s.sw) / s.sw);
+    const int ow_hi = min(s.OW - 1, (iw + s.pw) / s.sw);
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      const int a = ih - (oh * s.sh - s.ph);
+      if (a < 0 || a >= s.kh) continue;
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int b = iw - (ow * s.sw - s.pw);
+        if (b < 0 || b >= s.kw) continue;
+        const int64_t o = (((int64_t)n * s.OH + oh) * s.OW + ow) * cv + c8;
+        const uint2 packed = *reinterpret_cast<const uint2*>(arg + o * 8);
+        const uint8_t me = (uint8_t)(a * s.kw + b);
+        float g[8];
+        unpack8p(*reinterpret_cast<const uint4*>(dy + o * 8), g);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t word = k < 4 ? packed.x : packed.y;
+          if (((word >> (8 * (k & 3))) & 0xffu) == me) acc[k] += g[k];
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(dx + i * 8) = pack8p(acc);
+  }
+}
+
+static unsigned pool_grid(int64_t total) {
+  int64_t g = (total + kPoolThreads - 1) / kPoolThreads;
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_maxpool_fwd(const void* x, void* y, void* arg, const int* shape, cudaStream_t st) {
+  PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5],
+              shape[6], shape[7], shape[8], shape[9], shape[10], shape[11]};
+  const int64_t total = (int64_t)s.N * s.OH * s.OW * (s.C / 8);
+  maxpool_fwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
+      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool_bwd(const void* dy, const void* arg, void* dx, const int* shape,
+                               cudaStream_t st) {
+  PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5],
+              shape[6], shape[7], shape[8], shape[9], shape[10], shape[11]};
+  const int64_t total = (int64_t)s.N * s.H * s.W * (s.C / 8);
+  maxpool_bwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
+      (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
+  return cudaGetLastError();
+}
+
+}  // namespace cs

@@ -141,6 +141,8 @@ def test_fused_resnet_no_less_accurate_than_aten(cuda_device):
     swap_batchnorm(m_swap)
     m_fused = copy.deepcopy(m_swap)
     assert fuse_resnet(m_fused) == 16
+    from paper_2103_07974_b200.bn import CrossoverMaxPool2d
+    assert isinstance(m_fused.maxpool, CrossoverMaxPool2d)
     aten = torchvision.models.resnet50()
     aten.load_state_dict(m_swap.state_dict())
     aten32 = copy.deepcopy(aten)
@@ -163,3 +165,24 @@ def test_fused_resnet_no_less_accurate_than_aten(cuda_device):
         assert err[1] <= 1.5 * err[0] + 0.05 and err[2] <= 1.5 * err[0] + 0.05, (keys[k], err)
     assert abs(res[2][0] - res[0][0]) <= 2 * abs(res[1][0] - res[0][0]) + 1e-3
     assert abs(res[3][0] - res[0][0]) <= 2 * abs(res[1][0] - res[0][0]) + 1e-3
+
+
+@pytest.mark.parametrize("shape,k,s,p", [((8, 64, 112, 112), 3, 2, 1), ((4, 16, 9, 7), 3, 2, 1),
+                                         ((2, 8, 10, 10), 2, 2, 0), ((3, 24, 11, 13), 3, 1, 1)])
+def test_maxpool_matches_aten_exactly(cuda_device, shape, k, s, p):
+    from paper_2103_07974_b200.bn import CrossoverMaxPool2d
+
+    torch.manual_seed(1)
+    x = torch.randn(shape, device=cuda_device).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    x[0, 0, 0, :4] = 0.0          # ties: the first maximum in scan order wins (ATen's rule)
+    x[0, 1, :3, :3] = 1.0
+    dy = torch.randn((shape[0], shape[1], (shape[2] + 2 * p - k) // s + 1, (shape[3] + 2 * p - k) // s + 1),
+                     device=cuda_device).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    xa, xb = x.clone().requires_grad_(True), x.clone().requires_grad_(True)
+    ya = CrossoverMaxPool2d(k, s, p)(xa)
+    yb = torch.nn.functional.max_pool2d(xb, k, s, p)
+    assert torch.equal(ya, yb)
+    ya.backward(dy)
+    yb.backward(dy)
+    torch.testing.assert_close(xa.grad.float(), xb.grad.float(), rtol=1e-2, atol=1e-2)
+    assert torch.equal(xa.grad != 0, xb.grad != 0)      # same selected positions
