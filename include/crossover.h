@@ -105,6 +105,20 @@ CS_API int cs_get_kernel_variant(void);
  * Results never depend on them. */
 CS_API int cs_tune(const char* key, int value);
 
+/* Streams and events -- the crossover pipeline's primitives for hosts without torch
+ * (reference lanes / events, engine.py:62-86): gpu0 = compute stream, nic0 = comm stream,
+ * COMPUTE_DONE / COMM_DONE = recorded events, span times = cs_event_elapsed_ns against an
+ * origin event.  cs_event_query returns 1 (complete), 0 (pending) or an error code. */
+CS_API int cs_stream_create(int priority, void** stream);
+CS_API int cs_stream_destroy(void* stream);
+CS_API int cs_stream_synchronize(void* stream);
+CS_API int cs_event_create(int timing, void** event);
+CS_API int cs_event_destroy(void* event);
+CS_API int cs_event_record(void* event, void* stream);
+CS_API int cs_stream_wait_event(void* stream, void* event);
+CS_API int cs_event_query(void* event);
+CS_API int cs_event_elapsed_ns(void* start, void* end, int64_t* ns);
+
 /* K1: gather n tensors into the bucket (128-bit vector path when src and dst
  * are 16-byte aligned, scalar otherwise).  Bit-exact copy. */
 CS_API int cs_pack(const cs_pack_desc* descs, int n, void* stream);

@@ -61,6 +61,15 @@ EXPORTS = {
     "cs_set_kernel_variant": ([ctypes.c_int], ctypes.c_int),
     "cs_get_kernel_variant": ([], ctypes.c_int),
     "cs_tune": ([ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
+    "cs_stream_create": ([ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cs_stream_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "cs_stream_synchronize": ([ctypes.c_void_p], ctypes.c_int),
+    "cs_event_create": ([ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cs_event_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "cs_event_record": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "cs_stream_wait_event": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "cs_event_query": ([ctypes.c_void_p], ctypes.c_int),
+    "cs_event_elapsed_ns": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "cs_pack": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "cs_unpack_sgd": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                        ctypes.c_void_p, ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),

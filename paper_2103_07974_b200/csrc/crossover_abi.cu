@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -306,6 +307,71 @@ int cs_maxpool2d_backward(const void* dy, const uint8_t* argmax, void* dx, const
     return set_error(CS_ERR_ARG, "cs_maxpool2d_backward: invalid arguments");
   return cuda_status(launch_maxpool_bwd(dy, argmax, dx, shape, (cudaStream_t)stream),
                      "cs_maxpool2d_backward launch");
+}
+
+// ---- streams and events: the pipeline primitives for hosts without torch ----
+int cs_stream_create(int priority, void** stream) {
+  if (stream == nullptr) return set_error(CS_ERR_ARG, "cs_stream_create: NULL argument");
+  cudaStream_t s = nullptr;
+  int rc = cuda_status(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority),
+                       "cudaStreamCreateWithPriority");
+  if (rc) return rc;
+  *stream = (void*)s;
+  return 0;
+}
+
+int cs_stream_destroy(void* stream) {
+  if (stream == nullptr) return 0;
+  return cuda_status(cudaStreamDestroy((cudaStream_t)stream), "cudaStreamDestroy");
+}
+
+int cs_stream_synchronize(void* stream) {
+  return cuda_status(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize");
+}
+
+int cs_event_create(int timing, void** event) {
+  if (event == nullptr) return set_error(CS_ERR_ARG, "cs_event_create: NULL argument");
+  cudaEvent_t e = nullptr;
+  int rc = cuda_status(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming),
+                       "cudaEventCreateWithFlags");
+  if (rc) return rc;
+  *event = (void*)e;
+  return 0;
+}
+
+int cs_event_destroy(void* event) {
+  if (event == nullptr) return 0;
+  return cuda_status(cudaEventDestroy((cudaEvent_t)event), "cudaEventDestroy");
+}
+
+int cs_event_record(void* event, void* stream) {
+  if (event == nullptr) return set_error(CS_ERR_ARG, "cs_event_record: NULL event");
+  return cuda_status(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream), "cudaEventRecord");
+}
+
+int cs_stream_wait_event(void* stream, void* event) {
+  if (event == nullptr) return set_error(CS_ERR_ARG, "cs_stream_wait_event: NULL event");
+  return cuda_status(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0),
+                     "cudaStreamWaitEvent");
+}
+
+int cs_event_query(void* event) {
+  if (event == nullptr) return set_error(CS_ERR_ARG, "cs_event_query: NULL event");
+  const cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+  if (e == cudaSuccess) return 1;
+  if (e == cudaErrorNotReady) { cudaGetLastError(); return 0; }
+  return cuda_status(e, "cudaEventQuery");
+}
+
+int cs_event_elapsed_ns(void* start, void* end, int64_t* ns) {
+  if (start == nullptr || end == nullptr || ns == nullptr)
+    return set_error(CS_ERR_ARG, "cs_event_elapsed_ns: NULL argument");
+  float ms = 0.f;
+  int rc = cuda_status(cudaEventElapsedTime(&ms, (cudaEvent_t)start, (cudaEvent_t)end),
+                       "cudaEventElapsedTime");
+  if (rc) return rc;
+  *ns = (int64_t)llround((double)ms * 1e6);
+  return 0;
 }
 
 size_t cs_gradient_stats_workspace_bytes(int64_t numel) {
