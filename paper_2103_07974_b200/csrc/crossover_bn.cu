@@ -85,16 +85,18 @@ __host__ __device__ inline TileShape tile_shape(int C) {
   return s;
 }
 
-__device__ __forceinline__ void welford8(const uint4& raw, float& n, float* mean, float* m2) {
+// Shifted sums: per thread, s1 = sum(x - k), s2 = sum((x - k)^2) with k = the thread's first
+// value of each channel (2 FMA-class ops per element instead of a Welford update); converted to
+// (n, mean, M2) before the Chan merges.  |mean - k| ~ std for BN inputs, so s2 - s1^2/n keeps
+// its precision.
+__device__ __forceinline__ void shifted8(const uint4& raw, const float* k, float* s1, float* s2) {
   float v[8];
   unpack8(raw, v);
-  n += 1.f;
-  const float inv = 1.0f / n;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float d = v[i] - mean[i];
-    mean[i] = fmaf(d, inv, mean[i]);
-    m2[i] = fmaf(d, v[i] - mean[i], m2[i]);
+    const float d = v[i] - k[i];
+    s1[i] += d;
+    s2[i] = fmaf(d, d, s2[i]);
   }
 }
 
@@ -113,18 +115,28 @@ bn_fwd_partial_kernel(const __nv_bfloat16* __restrict__ x, int64_t M, int C,
   const int64_t r0 = blockIdx.x * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
 
-  float n = 0.f, mean[8], m2[8];
+  constexpr int U = 2 * kRowUnroll;
+  float k[8], s1[8], s2[8], mean[8], m2[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { mean[i] = 0.f; m2[i] = 0.f; }
+  for (int i = 0; i < 8; ++i) { k[i] = 0.f; s1[i] = 0.f; s2[i] = 0.f; }
   int64_t r = r0 + ty;
-  for (; r + (kRowUnroll - 1) * s.ty < r1; r += kRowUnroll * s.ty) {
-    uint4 raw[kRowUnroll];
+  if (r < r1) unpack8(ld_nc16(x + r * C + c0), k);   // the shift
+  for (; r + (U - 1) * s.ty < r1; r += U * s.ty) {
+    uint4 raw[U];
 #pragma unroll
-    for (int u = 0; u < kRowUnroll; ++u) raw[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
+    for (int u = 0; u < U; ++u) raw[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
 #pragma unroll
-    for (int u = 0; u < kRowUnroll; ++u) welford8(raw[u], n, mean, m2);
+    for (int u = 0; u < U; ++u) shifted8(raw[u], k, s1, s2);
   }
-  for (; r < r1; r += s.ty) welford8(ld_nc16(x + r * C + c0), n, mean, m2);
+  for (; r < r1; r += s.ty) shifted8(ld_nc16(x + r * C + c0), k, s1, s2);
+  const int64_t my_rows = r1 > r0 + ty ? (r1 - (r0 + ty) + s.ty - 1) / s.ty : 0;
+  float n = (float)my_rows;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float mu = n > 0.f ? s1[i] / n : 0.f;
+    mean[i] = k[i] + mu;
+    m2[i] = n > 0.f ? fmaxf(s2[i] - s1[i] * mu, 0.f) : 0.f;
+  }
 
   // merge the ty row lanes of every channel (fixed order)
   __shared__ float s_n[kBnThreads], s_mean[kBnThreads * 8], s_m2[kBnThreads * 8];

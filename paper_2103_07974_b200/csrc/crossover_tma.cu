@@ -84,9 +84,6 @@ __device__ __forceinline__ void st_v4(float* p, float4 v) {
                "f"(v.w)
                : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 // Descriptor tables live in __grid_constant__ kernel parameters (constant bank).
 // A persistent CTA touches every descriptor many times, and dependent constant-
