@@ -386,9 +386,10 @@ def run_ours(args):
 
     # NHWC BN kernels: 3 forward + 3 backward launches per BN layer per iteration (they replay
     # inside the CUDA graphs, so they are counted from the model structure, not from Python calls)
-    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d, CrossoverMaxPool2d
     n_bn = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverBatchNorm2d)) for a in base)
-    bn_launches = 6 * n_bn
+    n_pool = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverMaxPool2d)) for a in base)
+    bn_launches = 6 * n_bn + 2 * n_pool
     hbm_peak, peak_kind = peaks()
     sync0 = cross["sched"].states[0].sync
     kernels = kernel_summary(cross["kernels"], sync0)
@@ -420,7 +421,7 @@ def run_ours(args):
                                     f"{args.batch}/GPU")
                                    + ", bf16 autocast, fp32 params/grads, SGD momentum 0.9"
                                    + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs")
-                                   + ("" if args.aten_bn else ", NHWC BatchNorm kernels"),
+                                   + ("" if args.aten_bn else ", NHWC BN(+ReLU/+residual) and max-pool kernels"),
                        "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": sync0.mode},
@@ -440,7 +441,8 @@ def run_ours(args):
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
             "gpu_launches": cross["launches"] + bn_launches * K,
-            "gpu_launches_breakdown": {"k1_k2_p2p": cross["launches"], "bn_kernels": bn_launches * K},
+            "gpu_launches_breakdown": {"k1_k2_p2p": cross["launches"],
+                                       "bn_and_pool_kernels": bn_launches * K},
             "clocks": cross["clocks"],
             "e2e": e2e_line,
             "cpu_baseline": cpu,
