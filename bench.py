@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
+    ap.add_argument("--sync-ctas", type=int, default=0, help="persistent grid cap of K1/K2")
+    ap.add_argument("--comm-priority", default="high", choices=["high", "low"],
+                    help="comm stream priority (low: the sync fills gaps left by the compute)")
     ap.add_argument("--mix", default="", help="co-located mix, e.g. resnet50:256,vgg16:32,bert:16 "
                                               "(configs 3/5); overrides --model/--jobs/--batch")
     ap.add_argument("--trace-out", default="")
@@ -229,7 +232,7 @@ class Harness:
 
 
 def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
-              time_kernels: bool = True, sync_mode: str = "auto"):
+              time_kernels: bool = True, sync_mode: str = "auto", comm_priority: int = -1):
     """W untimed rotations, drain + barrier, then K timed rotations (CUDA events, max over ranks).
 
     A rotation = every app in `base` steps once.  With `host_data` every step's batch is copied
@@ -240,7 +243,8 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     from paper_2103_07974_b200.scheduler import CrossoverScheduler
 
     mode = sync_mode if h.world > 1 else "auto"
-    sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode)
+    sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
+                               comm_priority=comm_priority)
     for j, a in enumerate(base):
         sched.register(dataclasses.replace(a, iterations=W + K,
                                            data=host_data[j] if host_data else a.data))
@@ -336,9 +340,11 @@ def run_ours(args):
 
     h = Harness(args.nccl_max_ctas)
     rank, world, dev = h.rank, h.world, h.dev
+    from paper_2103_07974_b200 import _lib
     if args.p2p_ctas:
-        from paper_2103_07974_b200 import _lib
         _lib.tune("p2p_ctas", args.p2p_ctas)
+    if args.sync_ctas:
+        _lib.tune("sync_ctas", args.sync_ctas)
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
     flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False
@@ -364,12 +370,11 @@ def run_ours(args):
     samples_per_rot = sum(a.samples_per_batch for a in base) * world
 
     sm = args.sync_mode
-    if args.mix:  # one table per app: samples/s below sums images and sequences
-        pass
-    cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm)
-    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm)
+    prio = -1 if args.comm_priority == "high" else 0
+    cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio)
+    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
-                                             time_kernels=False, sync_mode=sm)
+                                             time_kernels=False, sync_mode=sm, comm_priority=prio)
 
     # legality + bit-exact schedule of the measured runs
     order = [a.job_id for a in base]

@@ -117,6 +117,7 @@ int cs_tune(const char* key, int value) {
   else if (k == "k2_debug" && value <= 2) g_tune_k2_debug = value;  // ablation only: wrong results
   else if (k == "reg_shape" && value <= 4) g_tune_reg_shape = value;
   else if (k == "p2p_ctas" && value <= 65536) g_tune_p2p_ctas = value;
+  else if (k == "sync_ctas" && value <= 65536) g_tune_sync_ctas = value;
   else return set_error(CS_ERR_ARG, "cs_tune: unknown key or bad value (%s=%d)", key, value);
   return 0;
 }

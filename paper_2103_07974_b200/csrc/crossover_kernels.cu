@@ -26,7 +26,12 @@
 
 namespace cs {
 
-int g_tune_reg_shape = 1;  // U=4, 3 CTAs/SM: best measured K2 shape (kbench sweep)
+int g_tune_reg_shape = 1;
+int g_tune_sync_ctas = 0;   // 0: one CTA per chunk; >0: persistent grid capped at this many CTAs
+
+static int sync_grid(int chunks) {
+  return g_tune_sync_ctas > 0 && chunks > g_tune_sync_ctas ? g_tune_sync_ctas : chunks;
+}  // U=4, 3 CTAs/SM: best measured K2 shape (kbench sweep)
 
 // ---------------------------------------------------------------------------
 // 128-bit memory helpers (inline PTX so the cache policy is explicit)
@@ -67,10 +72,18 @@ __device__ __forceinline__ int find_segment(const int* chunk_begin, int n, int c
 // K1: pack
 // ---------------------------------------------------------------------------
 template <int CAP, int U>
+__device__ __forceinline__ void pack_chunk(const PackArgs<CAP>& a, int c);
+
+// grid = #chunks (one chunk per CTA) or capped (cs_tune "sync_ctas"): persistent over chunks
+template <int CAP, int U>
 __global__ void __launch_bounds__(kThreads)
 pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
+  for (int c = blockIdx.x; c < a.total_chunks; c += gridDim.x) pack_chunk<CAP, U>(a, c);
+}
+
+template <int CAP, int U>
+__device__ __forceinline__ void pack_chunk(const PackArgs<CAP>& a, int c) {
   constexpr int CH = kThreads * 4 * U;
-  const int c = blockIdx.x;
   const int i = find_segment(a.chunk_begin, a.n, c);
   const int64_t e0 = (int64_t)(c - a.chunk_begin[i]) * CH;
   const float* __restrict__ src = a.src[i] + e0;
@@ -102,17 +115,24 @@ pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
 // ---------------------------------------------------------------------------
 // K2: fixed-order reduce over sources, average, SGD update
 // ---------------------------------------------------------------------------
+template <int CAP, bool kMom, int U>
+__device__ __forceinline__ void unpack_sgd_chunk(const UpdateArgs<CAP>& a, const Rule& r, int c);
+
 template <int CAP, bool kMom, int U, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 unpack_sgd_kernel(const __grid_constant__ UpdateArgs<CAP> a) {
+  const Rule r = make_rule(a.h, kMom);
+  for (int c = blockIdx.x; c < a.total_chunks; c += gridDim.x) unpack_sgd_chunk<CAP, kMom, U>(a, r, c);
+}
+
+template <int CAP, bool kMom, int U>
+__device__ __forceinline__ void unpack_sgd_chunk(const UpdateArgs<CAP>& a, const Rule& r, int c) {
   constexpr int CH = kThreads * 4 * U;
-  const int c = blockIdx.x;
   const int i = find_segment(a.chunk_begin, a.n, c);
   const int64_t e0 = (int64_t)(c - a.chunk_begin[i]) * CH;
   const int64_t rem = a.numel[i] - e0;
   const int n = rem < CH ? (int)rem : CH;
   const int tid = threadIdx.x;
-  const Rule r = make_rule(a.h, kMom);
 
   float* __restrict__ p = a.param[i] + e0;
   float* __restrict__ m = kMom ? a.mom[i] + e0 : nullptr;
@@ -272,14 +292,15 @@ int reg_update_chunk() { return kThreads * 4 * shape_unroll(g_tune_reg_shape); }
 template <int CAP>
 cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
-  if (g_tune_reg_shape == 3) pack_kernel<CAP, 8><<<a.total_chunks, kThreads, 0, s>>>(a);
-  else pack_kernel<CAP, 4><<<a.total_chunks, kThreads, 0, s>>>(a);
+  const int g = sync_grid(a.total_chunks);
+  if (g_tune_reg_shape == 3) pack_kernel<CAP, 8><<<g, kThreads, 0, s>>>(a);
+  else pack_kernel<CAP, 4><<<g, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int CAP, bool kMom>
 static void launch_update_shape(const UpdateArgs<CAP>& a, cudaStream_t s) {
-  const int g = a.total_chunks;
+  const int g = sync_grid(a.total_chunks);
   switch (g_tune_reg_shape) {
     case 1: unpack_sgd_kernel<CAP, kMom, 4, 3><<<g, kThreads, 0, s>>>(a); break;
     case 2: unpack_sgd_kernel<CAP, kMom, 2, 4><<<g, kThreads, 0, s>>>(a); break;
