@@ -206,7 +206,8 @@ class CrossoverScheduler:
                  comm: NcclCommunicator | None = None, record_spans: bool = True,
                  record_weights: bool = False, align: int = 32, sync_mode: str = "auto",
                  time_kernels: bool = False, comm_priority: int = -1,
-                 perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0):
+                 perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0,
+                 nvtx: bool = False):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -221,6 +222,7 @@ class CrossoverScheduler:
         self.record_weights = record_weights
         self.perturb = perturb
         self.watchdog_s = watchdog_s
+        self.nvtx = nvtx
         with torch.cuda.device(self.device):
             self.compute_stream = torch.cuda.Stream(self.device)
             lo, hi = torch.cuda.Stream.priority_range()
@@ -318,13 +320,14 @@ class CrossoverScheduler:
             amp = (torch.autocast("cuda", dtype=app.autocast_dtype, cache_enabled=app.autocast_cache)
                    if app.autocast_dtype else contextlib.nullcontext())
             losses = []
-            with amp:
+            with amp, self._range(f"{st.job_id} forward t{t}"):
                 for b in batches:
                     losses.append(app.loss_fn(app.model, b))
             e_f1 = ev()
             e_f1.record(cs)
-            grads = [list(torch.autograd.grad(loss, app.params, allow_unused=True))
-                     for loss in losses]
+            with self._range(f"{st.job_id} backward t{t}"):
+                grads = [list(torch.autograd.grad(loss, app.params, allow_unused=True))
+                         for loss in losses]
             e_b1 = ev()
             e_b1.record(cs)
         st.losses.append(losses[0].detach())
@@ -335,7 +338,8 @@ class CrossoverScheduler:
             ms.wait_event(e_b1)
             e_s0 = ev()
             e_s0.record(ms)
-            st.sync.sync(grads, ms.cuda_stream, t - 1 if self.record_weights else None, self.timer)
+            with self._range(f"{st.job_id} sync t{t}"):
+                st.sync.sync(grads, ms.cuda_stream, t - 1 if self.record_weights else None, self.timer)
             if self.perturb is not None and self.perturb == (self.job_index(st.job_id), t):
                 _nudge_first_coordinate(app.params[0], st.sync, t - 1 if self.record_weights else None)
             e_s1 = ev()
@@ -349,6 +353,10 @@ class CrossoverScheduler:
         st.next_iteration = t + 1
         self.cursor = (self.cursor + 1) % len(self.states)
         return True
+
+    def _range(self, name: str):
+        """NVTX range around a phase (visible in Nsight Systems) when nvtx=True."""
+        return torch.cuda.nvtx.range(name) if self.nvtx else contextlib.nullcontext()
 
     def job_index(self, job_id: str) -> int:
         return self.job_order.index(job_id)
