@@ -79,6 +79,15 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def ncu_traffic(key: str):
+    """dram read + write bytes per launch from a committed ncu --set full capture (or None)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(key)
+    return None if d is None else d["dram_read_bytes"] + d["dram_write_bytes"]
+
+
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle port): rotation + torch-CPU fwd/bwd + numpy fusion/average/SGD
 # ---------------------------------------------------------------------------
@@ -441,7 +450,8 @@ def run_ours(args):
                                  "comm_ms": [round(c, 4) for c in comm_t]},
             "roofline": {"kernel": "k2_update (fused 1/W average + SGD-momentum)", "bound": "hbm",
                          "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(k2_gbs / hbm_peak, 4), "traffic": None,
+                         "frac": round(k2_gbs / hbm_peak, 4),
+                         "traffic": ncu_traffic(f"k2_update/{args.model}/{sync0.mode}/momentum"),
                          "peak_kind": peak_kind, "bytes_per_launch": sync0.k2_bytes()},
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
