@@ -443,7 +443,9 @@ static int sm_count_bn() {
 int bn_row_blocks(int64_t M, int C) {
   const TileShape s = tile_shape(C);
   const int tiles = C / s.tile;
-  int64_t want = (int64_t)sm_count_bn() * 6 / tiles;                              // ~6 CTAs / SM
+  // ~3 CTAs / SM: with 8 rows of 16-byte loads in flight per thread that keeps >= 64 KB per SM
+  // outstanding, and halves the partials the finalize kernels must merge (vs 6 / SM)
+  int64_t want = (int64_t)sm_count_bn() * 3 / tiles;
   const int64_t max_by_rows = (M + s.ty * 4 * kRowUnroll - 1) / (s.ty * 4 * kRowUnroll);
   if (want > max_by_rows) want = max_by_rows;
   if (want < 1) want = 1;

@@ -41,6 +41,55 @@ struct PoolShape {
   int N, H, W, C, OH, OW, kh, kw, sh, sw, ph, pw;
 };
 
+// 3x3 windows (the ResNet stem): all nine 16-byte loads issued before the first compare
+__global__ void __launch_bounds__(kPoolThreads)
+maxpool3_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                    uint8_t* __restrict__ arg, PoolShape s) {
+  const int cv = s.C / 8;
+  const int64_t total = (int64_t)s.N * s.OH * s.OW * cv;
+  for (int64_t i = (int64_t)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * kPoolThreads) {
+    const int c8 = (int)(i % cv);
+    int64_t t = i / cv;
+    const int ow = (int)(t % s.OW);
+    t /= s.OW;
+    const int oh = (int)(t % s.OH);
+    const int n = (int)(t / s.OH);
+    const int h0 = oh * s.sh - s.ph, w0 = ow * s.sw - s.pw;
+    uint4 raw[9];
+    bool ok[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int ih = h0 + a, iw = w0 + b;
+        ok[a * 3 + b] = ih >= 0 && ih < s.H && iw >= 0 && iw < s.W;
+        raw[a * 3 + b] = ok[a * 3 + b]
+            ? __ldg(reinterpret_cast<const uint4*>(x + (((int64_t)n * s.H + ih) * s.W + iw) * s.C + c8 * 8))
+            : make_uint4(0, 0, 0, 0);
+      }
+    float best[8];
+    uint8_t idx[8];
+    const uint8_t first = (uint8_t)(max(0, -h0) * 3 + max(0, -w0));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { best[k] = -INFINITY; idx[k] = first; }
+#pragma unroll
+    for (int o = 0; o < 9; ++o) {
+      if (!ok[o]) continue;
+      float v[8];
+      unpack8p(raw[o], v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (v[k] > best[k] || isnan(v[k])) { best[k] = v[k]; idx[k] = (uint8_t)o; }   // ATen's rule
+    }
+    *reinterpret_cast<uint4*>(y + i * 8) = pack8p(best);
+    uint2 packed;
+    packed.x = idx[0] | (idx[1] << 8) | (idx[2] << 16) | ((uint32_t)idx[3] << 24);
+    packed.y = idx[4] | (idx[5] << 8) | (idx[6] << 16) | ((uint32_t)idx[7] << 24);
+    *reinterpret_cast<uint2*>(arg + i * 8) = packed;
+  }
+}
+
 __global__ void __launch_bounds__(kPoolThreads)
 maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                    uint8_t* __restrict__ arg, PoolShape s) {
@@ -104,21 +153,50 @@ maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restri
     const int oh_hi = min(s.OH - 1, (ih + s.ph) / s.sh);
     const int ow_lo = max(0, (iw + s.pw - s.kw + s.sw) / s.sw);
     const int ow_hi = min(s.OW - 1, (iw + s.pw) / s.sw);
-    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
-      const int a = ih - (oh * s.sh - s.ph);
-      if (a < 0 || a >= s.kh) continue;
-      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
-        const int b = iw - (ow * s.sw - s.pw);
-        if (b < 0 || b >= s.kw) continue;
+    if (oh_hi - oh_lo <= 1 && ow_hi - ow_lo <= 1) {
+      // common case (kernel <= 2 * stride): up to 2x2 windows, loads issued together
+      uint4 rg[4];
+      uint2 ra[4];
+      uint8_t me[4];
+      bool use[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int oh = oh_lo + (q >> 1), ow = ow_lo + (q & 1);
+        const int a = ih - (oh * s.sh - s.ph), b = iw - (ow * s.sw - s.pw);
+        use[q] = oh <= oh_hi && ow <= ow_hi && a >= 0 && a < s.kh && b >= 0 && b < s.kw;
+        me[q] = (uint8_t)(a * s.kw + b);
         const int64_t o = (((int64_t)n * s.OH + oh) * s.OW + ow) * cv + c8;
-        const uint2 packed = *reinterpret_cast<const uint2*>(arg + o * 8);
-        const uint8_t me = (uint8_t)(a * s.kw + b);
+        rg[q] = use[q] ? __ldg(reinterpret_cast<const uint4*>(dy + o * 8)) : make_uint4(0, 0, 0, 0);
+        ra[q] = use[q] ? __ldg(reinterpret_cast<const uint2*>(arg + o * 8)) : make_uint2(0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!use[q]) continue;
         float g[8];
-        unpack8p(*reinterpret_cast<const uint4*>(dy + o * 8), g);
+        unpack8p(rg[q], g);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const uint32_t word = k < 4 ? packed.x : packed.y;
-          if (((word >> (8 * (k & 3))) & 0xffu) == me) acc[k] += g[k];
+          const uint32_t word = k < 4 ? ra[q].x : ra[q].y;
+          if (((word >> (8 * (k & 3))) & 0xffu) == me[q]) acc[k] += g[k];
+        }
+      }
+    } else {
+      for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+        const int a = ih - (oh * s.sh - s.ph);
+        if (a < 0 || a >= s.kh) continue;
+        for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+          const int b = iw - (ow * s.sw - s.pw);
+          if (b < 0 || b >= s.kw) continue;
+          const int64_t o = (((int64_t)n * s.OH + oh) * s.OW + ow) * cv + c8;
+          const uint2 packed = *reinterpret_cast<const uint2*>(arg + o * 8);
+          const uint8_t mine = (uint8_t)(a * s.kw + b);
+          float g[8];
+          unpack8p(*reinterpret_cast<const uint4*>(dy + o * 8), g);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t word = k < 4 ? packed.x : packed.y;
+            if (((word >> (8 * (k & 3))) & 0xffu) == mine) acc[k] += g[k];
+          }
         }
       }
     }
@@ -136,8 +214,12 @@ cudaError_t launch_maxpool_fwd(const void* x, void* y, void* arg, const int* sha
   PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5],
               shape[6], shape[7], shape[8], shape[9], shape[10], shape[11]};
   const int64_t total = (int64_t)s.N * s.OH * s.OW * (s.C / 8);
-  maxpool_fwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
-      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
+  if (s.kh == 3 && s.kw == 3)
+    maxpool3_fwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
+        (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
+  else
+    maxpool_fwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
+        (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
   return cudaGetLastError();
 }
 
