@@ -185,3 +185,38 @@ def test_gradient_stats(cuda_device):
     _lib.gradient_stats(x.data_ptr(), x.numel(), out2.data_ptr(), ws.data_ptr(), _stream())
     torch.cuda.synchronize()
     assert torch.equal(out2.cpu(), outs[0])        # deterministic
+
+
+def test_guard_bands_untouched(cuda_device):
+    """Out-of-bounds write detector (compute-sanitizer is closed on this pool): every tensor,
+    the bucket and the momentum buffers live inside one sentinel-filled arena with gaps; after
+    K1 + K2 the gaps must still hold the sentinel bit pattern."""
+    from paper_2103_07974_b200.fusion import FusedGradientSync, SgdSettings
+
+    sizes = [1, 3, 5, 4095, 4097, 12345, 10, 0, 7]
+    gap = 37
+    total = sum(sizes) * 4 + gap * (4 * len(sizes) + 2)
+    arena = torch.full((total,), float("nan"), device=cuda_device)
+    sentinel = arena.clone()
+    views, cur = {"p": [], "g": []}, gap
+    for kind in ("p", "g"):
+        for n in sizes:
+            v = arena[cur:cur + n]
+            v.copy_(torch.randn(n, device=cuda_device))
+            views[kind].append(v)
+            cur += n + gap
+    used = torch.zeros(total, dtype=torch.bool, device=cuda_device)
+    for kind in ("p", "g"):
+        for v in views[kind]:
+            off = (v.data_ptr() - arena.data_ptr()) // 4
+            used[off:off + v.numel()] = True
+    s = FusedGradientSync(views["p"], SgdSettings(0.01, momentum=0.9, weight_decay=1e-3), mode="direct")
+    for _ in range(2):
+        s.sync([views["g"]], _stream())
+    sb = FusedGradientSync(views["p"], SgdSettings(0.01), mode="bucket", align=1)
+    sb.sync([views["g"]], _stream())
+    torch.cuda.synchronize()
+    a = arena.view(torch.int32)[~used]
+    b = sentinel.view(torch.int32)[~used]
+    assert torch.equal(a, b)
+    assert torch.isfinite(torch.cat([v for v in views["p"] if v.numel()])).all()
