@@ -55,7 +55,8 @@ def parse():
                     help="comm stream priority (low: the sync fills gaps left by the compute)")
     ap.add_argument("--mix", default="", help="co-located mix, e.g. resnet50:256,vgg16:32,bert:16 "
                                               "(configs 3/5); overrides --model/--jobs/--batch")
-    ap.add_argument("--trace-out", default="")
+    ap.add_argument("--trace-out", default="", help="Chrome trace (JSON) of the measured crossover run")
+    ap.add_argument("--metrics-out", default="", help="colosim.metrics/v1 JSON + CSV of the measured runs")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"],
@@ -464,6 +465,16 @@ def run_ours(args):
         }
         if args.trace_out:
             Path(args.trace_out).write_text(trace_to_chrome_json(cross["trace"]))
+        if args.metrics_out:
+            # the reference's own measure / compare / report (metrics.py:62-200) on measured traces
+            from paper_2103_07974_b200.metrics import compare, measure, report
+            from paper_2103_07974_b200.scheduler import SchedulePlan
+
+            mx = measure(cross["trace"], SchedulePlan(Policy.CROSSOVER, base), "bench")
+            ms_ = measure(seq["trace"], SchedulePlan(Policy.SEQUENTIAL, base), "bench")
+            c = compare(mx, ms_)
+            Path(args.metrics_out).write_text(report(c, "json"))
+            Path(args.metrics_out).with_suffix(".csv").write_text(report(c, "csv") + report(ms_, "csv"))
     h.close()
     if out is not None:
         print(json.dumps(out), flush=True)
