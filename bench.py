@@ -415,11 +415,12 @@ def run_ours(args):
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cv, cores, wall = cpu_crossover(args.model, args.jobs, args.cpu_batch, 2, 1)
+            rot = 20   # ~10 s of host work on the pool's boxes
+            cv, cores, wall = cpu_crossover(args.model, args.jobs, args.cpu_batch, rot, 1)
             cpu = {"value": round(cv, 3), "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"{args.jobs} x {args.model}, batch {args.cpu_batch}/job, 2 rotations "
-                             f"after 1 warm-up, torch-CPU fwd/bwd + oracle fusion/average/SGD "
-                             f"({wall:.1f} s)"}
+                   "sample": f"{args.jobs} x {args.model}, batch {args.cpu_batch}/job (bounded sample of "
+                             f"batch {args.batch}), {rot} rotations after 1 warm-up, torch-CPU fwd/bwd + "
+                             f"oracle rotation / fusion / average / SGD-momentum ({wall:.1f} s)"}
         e2e_line = None
         if e2e is not None:
             ev = samples_per_rot * K / (e2e["ms"] / 1e3)
