@@ -39,25 +39,28 @@ __device__ __forceinline__ void st4(float* p, float4 v) {
 }
 }  // namespace
 
-constexpr int kP2PUnroll = 2;
-constexpr int kP2PChunk = kThreads * 4 * kP2PUnroll;
+// U float4 per thread per source: W * U = 8 peer loads in flight per thread for W = 2, 4, 8
+template <int U>
+constexpr int p2p_chunk_elems() { return kThreads * 4 * U; }
 
-template <bool kMom>
+template <bool kMom, int U>
 __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0);
 
 // Persistent when the grid is capped (cs_tune "p2p_ctas"): a comm kernel that overlaps another
 // app's compute should hold as few SMs as keep NVLink busy; each CTA walks chunks with stride.
-template <bool kMom>
+template <bool kMom, int U>
 __global__ void __launch_bounds__(kThreads)
 p2p_reduce_sgd_bcast_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
+  constexpr int CH = p2p_chunk_elems<U>();
   const Rule r = make_rule(h, kMom);
-  const int64_t chunks = (d.numel + kP2PChunk - 1) / kP2PChunk;
-  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) p2p_chunk<kMom>(d, r, c * kP2PChunk);
+  const int64_t chunks = (d.numel + CH - 1) / CH;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) p2p_chunk<kMom, U>(d, r, c * CH);
   __threadfence_system();   // remote stores performed before the kernel retires
 }
 
-template <bool kMom>
+template <bool kMom, int kP2PUnroll>
 __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0) {
+  constexpr int kP2PChunk = p2p_chunk_elems<kP2PUnroll>();
   const int64_t rem = d.numel - e0;
   const int n = rem < kP2PChunk ? (int)rem : kP2PChunk;
   const int tid = threadIdx.x;
@@ -126,12 +129,19 @@ __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, i
   }
 }
 
+template <int U>
+static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
+  int64_t grid = (d.numel + p2p_chunk_elems<U>() - 1) / p2p_chunk_elems<U>();
+  if (g_tune_p2p_ctas > 0 && grid > g_tune_p2p_ctas) grid = g_tune_p2p_ctas;
+  if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true, U><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+  else p2p_reduce_sgd_bcast_kernel<false, U><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+}
+
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
-  int64_t grid = (d.numel + kP2PChunk - 1) / kP2PChunk;
-  if (g_tune_p2p_ctas > 0 && grid > g_tune_p2p_ctas) grid = g_tune_p2p_ctas;
-  if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
-  else p2p_reduce_sgd_bcast_kernel<false><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+  if (d.nranks <= 2) launch_p2p_u<4>(d, h, s);
+  else if (d.nranks <= 4) launch_p2p_u<2>(d, h, s);
+  else launch_p2p_u<1>(d, h, s);
   return cudaGetLastError();
 }
 

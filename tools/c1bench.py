@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--sizes-mb", default="1,16,102,256,1024")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", default="")
+    ap.add_argument("--p2p-caps", default="64", help="comma list of p2p_ctas values to time")
     args = ap.parse_args()
     from paper_2103_07974_b200.fusion import FusedGradientSync, SgdSettings, flatten_parameters
 
@@ -58,20 +59,24 @@ def main():
         flat, _ = flatten_parameters(p, 32, W, ipc=True)
         sync = FusedGradientSync(p, SgdSettings(0.01, momentum=0.9), h.comm, mode="p2p", flat_params=flat)
         g = [torch.randn_like(p[0])]
-        ts = []
-        for it in range(args.iters + 2):
-            sync.pack([g], s.cuda_stream)
-            h.barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            sync._p2p_tail(s.cuda_stream, None, None)
-            b.record(s); b.synchronize()
-            if it >= 2:
-                ts.append(h.max_over_ranks(a.elapsed_time(b)))
-        t = statistics.median(ts)
-        nv = 2.0 * (W - 1) / W * n * 4
-        row["p2p_fused_with_barriers"] = {"ms": round(t, 4), "busbw_equiv_GB/s": round(nv / (t / 1e3) / 1e9, 1),
-                                          "hbm_bytes": sync.k2_bytes()}
+        from paper_2103_07974_b200 import _lib
+        for cap in [int(c) for c in args.p2p_caps.split(",")]:
+            _lib.tune("p2p_ctas", cap)
+            ts = []
+            for it in range(args.iters + 2):
+                sync.pack([g], s.cuda_stream)
+                h.barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                sync._p2p_tail(s.cuda_stream, None, None)
+                b.record(s); b.synchronize()
+                if it >= 2:
+                    ts.append(h.max_over_ranks(a.elapsed_time(b)))
+            t = statistics.median(ts)
+            nv = 2.0 * (W - 1) / W * n * 4
+            row[f"p2p_fused_with_barriers[ctas={cap}]"] = {
+                "ms": round(t, 4), "busbw_equiv_GB/s": round(nv / (t / 1e3) / 1e9, 1), "hbm_bytes": sync.k2_bytes()}
+        _lib.tune("p2p_ctas", 64)
         sync.close()
         rows.append(row)
         if h.rank == 0:
