@@ -101,7 +101,7 @@ CS_API int cs_get_kernel_variant(void);
 /* Launch-shape knobs of the TMA variant (0 restores the built-in heuristic):
  * "k1_chunk", "k2_chunk" (fp32 elements per stream per stage), "k2_stages",
  * "ctas_per_sm"; of the register variant: "reg_shape" (0..4: unroll x CTAs/SM); of the
- * fused P2P kernel: "p2p_ctas" (persistent grid cap, default 64; 0 = one CTA per chunk); of
+ * fused P2P kernel: "p2p_ctas" (persistent grid cap, 0 = default 2 CTAs per SM); of
  * the register K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
  * sync that overlaps another app's compute with slack can trade speed for fewer SMs.
  * Results never depend on them. */

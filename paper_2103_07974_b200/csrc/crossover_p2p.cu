@@ -21,7 +21,9 @@
 
 namespace cs {
 
-int g_tune_p2p_ctas = 64;  // persistent grid cap: measured best at W=4 (profiles/r01_multi_gpu.md)
+// persistent grid cap; 0 = 2 CTAs per SM (measured best in isolation at W = 2 and 4,
+// profiles/r01_c1/); a smaller cap trades sync speed for fewer SMs under a concurrent GEMM
+int g_tune_p2p_ctas = 0;
 
 namespace {
 __device__ __forceinline__ float4 ld_peer(const float* p) {
@@ -41,7 +43,7 @@ __device__ __forceinline__ void st4(float* p, float4 v) {
 
 // U float4 per thread per source: W * U = 8 peer loads in flight per thread for W = 2, 4, 8
 template <int U>
-constexpr int p2p_chunk_elems() { return kThreads * 4 * U; }
+__host__ __device__ constexpr int p2p_chunk_elems() { return kThreads * 4 * U; }
 
 template <bool kMom, int U>
 __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0);
@@ -132,7 +134,14 @@ __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, i
 template <int U>
 static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   int64_t grid = (d.numel + p2p_chunk_elems<U>() - 1) / p2p_chunk_elems<U>();
-  if (g_tune_p2p_ctas > 0 && grid > g_tune_p2p_ctas) grid = g_tune_p2p_ctas;
+  int cap = g_tune_p2p_ctas;
+  if (cap <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = 2 * sms;
+  }
+  if (grid > cap) grid = cap;
   if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true, U><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
   else p2p_reduce_sgd_bcast_kernel<false, U><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
 }

@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--sizes-mb", default="1,16,102,256,1024")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", default="")
-    ap.add_argument("--p2p-caps", default="64", help="comma list of p2p_ctas values to time")
+    ap.add_argument("--p2p-caps", default="0", help="comma list of p2p_ctas values to time (0 = default)")
     args = ap.parse_args()
     from paper_2103_07974_b200.fusion import FusedGradientSync, SgdSettings, flatten_parameters
 
@@ -76,7 +76,7 @@ def main():
             nv = 2.0 * (W - 1) / W * n * 4
             row[f"p2p_fused_with_barriers[ctas={cap}]"] = {
                 "ms": round(t, 4), "busbw_equiv_GB/s": round(nv / (t / 1e3) / 1e9, 1), "hbm_bytes": sync.k2_bytes()}
-        _lib.tune("p2p_ctas", 64)
+        _lib.tune("p2p_ctas", 0)
         sync.close()
         rows.append(row)
         if h.rank == 0:
