@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
-                         "the fused NVLink P2P kernel; auto = bucket")
+                         "the fused NVLink P2P kernel; auto = p2p (bucket if peers cannot be mapped)")
     return ap.parse_args()
 
 
@@ -357,6 +357,8 @@ def run_ours(args):
         _lib.tune("sync_ctas", args.sync_ctas)
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
+    if args.sync_mode == "auto":
+        args.sync_mode = "p2p" if world > 1 else "auto"
     flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False
     if args.mix:
         base = []
@@ -381,6 +383,16 @@ def run_ours(args):
 
     sm = args.sync_mode
     prio = -1 if args.comm_priority == "high" else 0
+    if sm == "p2p":
+        # probe once (collective): if any rank cannot map its peers, everyone falls back to bucket
+        from paper_2103_07974_b200.errors import ConfigError
+        try:
+            probe = timed_run(h, base, Policy.CROSSOVER, 0, 1, sync_mode="p2p", comm_priority=prio)
+            del probe
+        except ConfigError as exc:
+            if rank == 0:
+                print(f"p2p sync unavailable ({exc}); using the bucket all-reduce", file=sys.stderr)
+            sm = args.sync_mode = "bucket"
     cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio)
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,

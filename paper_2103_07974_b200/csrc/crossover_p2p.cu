@@ -45,22 +45,22 @@ __device__ __forceinline__ void st4(float* p, float4 v) {
 template <int U>
 __host__ __device__ constexpr int p2p_chunk_elems() { return kThreads * 4 * U; }
 
-template <bool kMom, int U>
+template <bool kMom, int U, int MAXW>
 __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0);
 
 // Persistent when the grid is capped (cs_tune "p2p_ctas"): a comm kernel that overlaps another
 // app's compute should hold as few SMs as keep NVLink busy; each CTA walks chunks with stride.
-template <bool kMom, int U>
+template <bool kMom, int U, int MAXW>
 __global__ void __launch_bounds__(kThreads)
 p2p_reduce_sgd_bcast_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
   constexpr int CH = p2p_chunk_elems<U>();
   const Rule r = make_rule(h, kMom);
   const int64_t chunks = (d.numel + CH - 1) / CH;
-  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) p2p_chunk<kMom, U>(d, r, c * CH);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) p2p_chunk<kMom, U, MAXW>(d, r, c * CH);
   __threadfence_system();   // remote stores performed before the kernel retires
 }
 
-template <bool kMom, int kP2PUnroll>
+template <bool kMom, int kP2PUnroll, int MAXW>
 __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, int64_t e0) {
   constexpr int kP2PChunk = p2p_chunk_elems<kP2PUnroll>();
   const int64_t rem = d.numel - e0;
@@ -84,9 +84,9 @@ __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, i
     }
   }
   // all W x U peer loads in flight before the first add
-  float4 g[CS_MAX_SOURCES][kP2PUnroll];
+  float4 g[MAXW][kP2PUnroll];
 #pragma unroll
-  for (int s = 0; s < CS_MAX_SOURCES; ++s) {
+  for (int s = 0; s < MAXW; ++s) {
     if (s < W) {
       const float* src = (const float*)d.src[s] + e0;
 #pragma unroll
@@ -97,7 +97,7 @@ __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, i
     }
   }
 #pragma unroll
-  for (int s = 0; s < CS_MAX_SOURCES; ++s) {
+  for (int s = 0; s < MAXW; ++s) {
     if (s < W) {
 #pragma unroll
       for (int u = 0; u < kP2PUnroll; ++u) {
@@ -131,7 +131,7 @@ __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, i
   }
 }
 
-template <int U>
+template <int U, int MAXW>
 static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   int64_t grid = (d.numel + p2p_chunk_elems<U>() - 1) / p2p_chunk_elems<U>();
   int cap = g_tune_p2p_ctas;
@@ -142,15 +142,15 @@ static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream
     cap = 2 * sms;
   }
   if (grid > cap) grid = cap;
-  if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true, U><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
-  else p2p_reduce_sgd_bcast_kernel<false, U><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+  if (h.momentum != 0.0f) p2p_reduce_sgd_bcast_kernel<true, U, MAXW><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
+  else p2p_reduce_sgd_bcast_kernel<false, U, MAXW><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
 }
 
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
-  if (d.nranks <= 2) launch_p2p_u<4>(d, h, s);
-  else if (d.nranks <= 4) launch_p2p_u<2>(d, h, s);
-  else launch_p2p_u<1>(d, h, s);
+  if (d.nranks <= 2) launch_p2p_u<4, 2>(d, h, s);
+  else if (d.nranks <= 4) launch_p2p_u<2, 4>(d, h, s);
+  else launch_p2p_u<1, CS_MAX_SOURCES>(d, h, s);
   return cudaGetLastError();
 }
 

@@ -71,12 +71,18 @@ class PeerMapping:
 
 
 def exchange_peer_addresses(buf: DeviceBuffer, rank: int, world: int) -> PeerMapping:
-    """All-gather IPC handles and open every peer's buffer (collective over torch.distributed)."""
+    """All-gather IPC handles and open every peer's buffer (collective over torch.distributed).
+
+    Failure is agreed on collectively: if any rank cannot map any peer, every rank closes what
+    it opened and raises ConfigError -- no rank is left waiting in a later collective.
+    """
     import torch.distributed as dist
+
+    from .errors import ConfigError
 
     handles: list = [None] * world
     dist.all_gather_object(handles, buf.ipc_handle())
-    addrs, opened = [], []
+    addrs, opened, error = [], [], ""
     with torch.cuda.device(buf.device):
         for r in range(world):
             if r == rank:
@@ -84,7 +90,16 @@ def exchange_peer_addresses(buf: DeviceBuffer, rank: int, world: int) -> PeerMap
                 continue
             h = (ctypes.c_uint8 * _lib.CS_IPC_HANDLE_BYTES).from_buffer_copy(handles[r])
             p = ctypes.c_void_p()
-            _lib.check("cs_ipc_open_handle", _lib.lib.cs_ipc_open_handle(h, ctypes.byref(p)))
+            rc = _lib.lib.cs_ipc_open_handle(h, ctypes.byref(p))
+            if rc:
+                error = f"rank {rank}: cannot map rank {r}: {_lib.lib.cs_last_error().decode()}"
+                break
             addrs.append(int(p.value))
             opened.append(int(p.value))
-    return PeerMapping(addrs, opened)
+    ok = torch.tensor([0 if error else 1], dtype=torch.int32)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    mapping = PeerMapping(addrs, opened)
+    if int(ok.item()) == 0:
+        mapping.close()
+        raise ConfigError("p2p peer mapping failed on some rank" + (f" ({error})" if error else ""))
+    return mapping
