@@ -80,6 +80,34 @@ def peaks():
     return 6650.0, "fallback"
 
 
+NVLINK_P2P_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
+
+
+def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: str) -> dict:
+    """Roofline of the path's dominant kernel: K2 (HBM) or, in p2p mode, the fused NVLink kernel."""
+    if "k2_p2p_fused" in kernels:
+        k = kernels["k2_p2p_fused"]
+        per_dir = sync.c1_bus_bytes()          # 2(W-1)/W * S through each GPU's links per direction
+        ach = per_dir / (k["ms"] / 1e3) / 1e9
+        out = {"kernel": "k2_p2p_fused (NVLink reads of every rank's bucket shard, rank-order sum, "
+                         "/W, SGD-momentum, NVLink writes of the new shard to every rank)",
+               "bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
+               "frac": round(ach / NVLINK_P2P_GBS, 4), "traffic": None,
+               "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+               "bytes_per_launch": per_dir}
+        if "k1_pack" in kernels:
+            k1 = kernels["k1_pack"]
+            out["hbm_kernel"] = {"kernel": "k1_pack", "achieved": k1["GB/s"], "peak": hbm_peak,
+                                 "frac": round(k1["GB/s"] / hbm_peak, 4), "bytes_per_launch": k1["bytes"]}
+        return out
+    k2 = kernels.get("k2_update", {"GB/s": 0.0})
+    return {"kernel": "k2_update (fused 1/W average + SGD-momentum)", "bound": "hbm",
+            "achieved": k2["GB/s"], "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(k2["GB/s"] / hbm_peak, 4),
+            "traffic": ncu_traffic(f"k2_update/{model}/{sync.mode}/momentum"),
+            "peak_kind": peak_kind, "bytes_per_launch": sync.k2_bytes()}
+
+
 def ncu_traffic(key: str):
     """dram read + write bytes per launch from a committed ncu --set full capture (or None)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
@@ -421,7 +449,6 @@ def run_ours(args):
     sync0 = cross["sched"].states[0].sync
     kernels = kernel_summary(cross["kernels"], sync0)
     kernels_isolated = kernel_summary(seq["kernels"], sync0)
-    k2_gbs = kernels.get("k2_update", kernels.get("k2_p2p_fused", {})).get("GB/s", 0.0)
 
     out = None
     if rank == 0:
@@ -462,11 +489,7 @@ def run_ours(args):
                                  "frac_tight": round(roof["tight"] / rot_cross, 4),
                                  "comp_ms": [round(c, 4) for c in comp],
                                  "comm_ms": [round(c, 4) for c in comm_t]},
-            "roofline": {"kernel": "k2_update (fused 1/W average + SGD-momentum)", "bound": "hbm",
-                         "achieved": k2_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(k2_gbs / hbm_peak, 4),
-                         "traffic": ncu_traffic(f"k2_update/{args.model}/{sync0.mode}/momentum"),
-                         "peak_kind": peak_kind, "bytes_per_launch": sync0.k2_bytes()},
+            "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind, args.model),
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
             "gpu_launches": cross["launches"] + bn_launches * K,
