@@ -220,3 +220,46 @@ def test_guard_bands_untouched(cuda_device):
     b = sentinel.view(torch.int32)[~used]
     assert torch.equal(a, b)
     assert torch.isfinite(torch.cat([v for v in views["p"] if v.numel()])).all()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum):
+    """The fused P2P kernel with every 'peer' address pointing at local memory (one GPU emulates
+    W ranks): rank-order sum, /W, SGD, and the broadcast into all W destinations, bit-exact
+    against the same arithmetic (reference rounding) / torch-SGD rounding on the CPU."""
+    import ctypes
+
+    from paper_2103_07974_b200 import _lib
+
+    torch.manual_seed(world)
+    shard = 4096 * 3 + 8                                  # not a multiple of the chunk: tail path
+    srcs = [torch.randn(shard, device=cuda_device) for _ in range(world)]
+    p = torch.randn(shard, device=cuda_device)
+    dsts = [torch.zeros(shard, device=cuda_device) for _ in range(world)]
+    mom = torch.randn(shard, device=cuda_device) if momentum else None
+    d = _lib.P2PDesc()
+    for r in range(world):
+        d.src[r] = srcs[r].data_ptr()
+        d.dst[r] = dsts[r].data_ptr()
+    d.param, d.numel, d.nranks = p.data_ptr(), shard, world
+    d.momentum_buf = mom.data_ptr() if mom is not None else None
+    h = _lib.SgdHyper(lr=0.05, momentum=momentum, dampening_complement=1.0, divisor=world,
+                      first_step=0, rounding=_lib.CS_ROUND_TORCH if momentum else _lib.CS_ROUND_REFERENCE)
+    p0, m0 = p.cpu().clone(), (mom.cpu().clone() if mom is not None else None)
+    _lib.check("p2p", _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(d), ctypes.byref(h), _stream()))
+    torch.cuda.synchronize()
+    acc = torch.zeros(shard)
+    for sr in srcs:
+        acc = acc + sr.cpu()                              # rank order, fp32, one rounding per add
+    avg = acc / world
+    if momentum:
+        buf = m0 * 0.9 + avg                              # mul rounded, then the add (fma(1, g, t))
+        want = torch.addcmul(p0, buf, torch.full_like(buf, -0.05))   # fused p - lr * buf
+        assert torch.equal(mom.cpu(), buf)
+        torch.testing.assert_close(dsts[0].cpu(), want, rtol=0, atol=1e-6)
+    else:
+        want = p0 - torch.tensor(0.05, dtype=torch.float32) * avg
+        assert torch.equal(dsts[0].cpu(), want)
+    for r in range(1, world):
+        assert torch.equal(dsts[r], dsts[0])              # the fused all-gather wrote every rank
