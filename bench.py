@@ -83,8 +83,13 @@ def peaks():
 NVLINK_P2P_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
 
 
-def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: str) -> dict:
-    """Roofline of the path's dominant kernel: K2 (HBM) or, in p2p mode, the fused NVLink kernel."""
+def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: str,
+                  isolated: dict | None = None) -> dict:
+    """Roofline of the path's dominant kernel: K2 (HBM) or, in p2p mode, the fused NVLink kernel.
+
+    Under crossover the P2P kernel is launched on a deliberately small grid (it overlaps the
+    other app's compute and only has to finish inside it), so its live fraction is low by
+    design; ``isolated`` is the same kernel at the full grid in the sequential arm."""
     if "k2_p2p_fused" in kernels:
         k = kernels["k2_p2p_fused"]
         per_dir = sync.c1_bus_bytes()          # 2(W-1)/W * S through each GPU's links per direction
@@ -94,7 +99,13 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
                "bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
                "frac": round(ach / NVLINK_P2P_GBS, 4), "traffic": None,
                "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-               "bytes_per_launch": per_dir}
+               "bytes_per_launch": per_dir,
+               "grid_cap_ctas": int(sync._p2p.max_ctas) or "2 per SM"}
+        ki = (isolated or {}).get("k2_p2p_fused")
+        if ki:
+            ach_i = per_dir / (ki["ms"] / 1e3) / 1e9
+            out["isolated"] = {"achieved": round(ach_i, 1), "frac": round(ach_i / NVLINK_P2P_GBS, 4),
+                               "grid_cap_ctas": "2 per SM", "arm": "sequential"}
         if "k1_pack" in kernels:
             k1 = kernels["k1_pack"]
             out["hbm_kernel"] = {"kernel": "k1_pack", "achieved": k1["GB/s"], "peak": hbm_peak,
@@ -269,6 +280,9 @@ class Harness:
             self.dist.destroy_process_group()
 
 
+P2P_CTAS: int | None = None   # --p2p-ctas; None = the scheduler's per-policy default
+
+
 def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
               time_kernels: bool = True, sync_mode: str = "auto", comm_priority: int = -1):
     """W untimed rotations, drain + barrier, then K timed rotations (CUDA events, max over ranks).
@@ -282,7 +296,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
 
     mode = sync_mode if h.world > 1 else "auto"
     sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
-                               comm_priority=comm_priority)
+                               comm_priority=comm_priority, p2p_ctas=P2P_CTAS)
     for j, a in enumerate(base):
         sched.register(dataclasses.replace(a, iterations=W + K,
                                            data=host_data[j] if host_data else a.data))
@@ -379,8 +393,9 @@ def run_ours(args):
     h = Harness(args.nccl_max_ctas)
     rank, world, dev = h.rank, h.world, h.dev
     from paper_2103_07974_b200 import _lib
-    if args.p2p_ctas:
-        _lib.tune("p2p_ctas", args.p2p_ctas)
+    if args.p2p_ctas:   # override the scheduler's policy-dependent cap, both arms
+        global P2P_CTAS
+        P2P_CTAS = args.p2p_ctas
     if args.sync_ctas:
         _lib.tune("sync_ctas", args.sync_ctas)
     K, W = args.steps, args.warmup
@@ -489,7 +504,8 @@ def run_ours(args):
                                  "frac_tight": round(roof["tight"] / rot_cross, 4),
                                  "comp_ms": [round(c, 4) for c in comp],
                                  "comm_ms": [round(c, 4) for c in comm_t]},
-            "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind, args.model),
+            "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind, args.model,
+                                      kernels_isolated),
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
             "gpu_launches": cross["launches"] + bn_launches * K,

@@ -162,7 +162,9 @@ typedef struct cs_p2p_desc {
   float* momentum_buf;   /* this rank's momentum shard, NULL when momentum == 0 */
   int64_t numel;         /* shard length (fp32 elements) */
   int32_t nranks;        /* W, 2..CS_MAX_SOURCES */
-  int32_t pad_;
+  int32_t max_ctas;      /* persistent grid cap for this launch; 0 = cs_tune("p2p_ctas") or
+                            2 CTAs per SM.  A sync that overlaps another app's compute with slack
+                            should hold few SMs (the scheduler uses 32 under crossover). */
 } cs_p2p_desc;
 CS_API int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* desc, const cs_sgd_hyper* hyper,
                                    void* stream);

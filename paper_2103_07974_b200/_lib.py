@@ -43,7 +43,7 @@ CS_IPC_HANDLE_BYTES = 64
 class P2PDesc(ctypes.Structure):
     _fields_ = [("src", ctypes.c_uint64 * CS_MAX_SOURCES), ("dst", ctypes.c_uint64 * CS_MAX_SOURCES),
                 ("param", ctypes.c_void_p), ("momentum_buf", ctypes.c_void_p),
-                ("numel", ctypes.c_int64), ("nranks", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("numel", ctypes.c_int64), ("nranks", ctypes.c_int32), ("max_ctas", ctypes.c_int32)]
 
 
 class CrossoverLibError(RuntimeError):

@@ -188,6 +188,7 @@ int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* d, const cs_sgd_hyper* h, void* s
                      CS_MAX_SOURCES);
   if (d->numel < 0 || (d->numel > 0 && d->param == nullptr))
     return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: bad shard");
+  if (d->max_ctas < 0) return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: max_ctas < 0");
   if (h->divisor != d->nranks)
     return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: divisor %d != nranks %d", h->divisor, d->nranks);
   if (!(h->lr > 0.0f)) return set_error(CS_ERR_ARG, "cs_p2p_reduce_sgd_bcast: learning rate must be > 0");

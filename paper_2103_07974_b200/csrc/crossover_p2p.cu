@@ -134,7 +134,7 @@ __device__ __forceinline__ void p2p_chunk(const cs_p2p_desc& d, const Rule& r, i
 template <int U, int MAXW>
 static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   int64_t grid = (d.numel + p2p_chunk_elems<U>() - 1) / p2p_chunk_elems<U>();
-  int cap = g_tune_p2p_ctas;
+  int cap = d.max_ctas > 0 ? d.max_ctas : g_tune_p2p_ctas;
   if (cap <= 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

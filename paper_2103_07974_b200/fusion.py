@@ -105,7 +105,7 @@ class FusedGradientSync:
     def __init__(self, params: Sequence[torch.Tensor], settings: SgdSettings,
                  comm: NcclCommunicator | None = None, local_workers: int = 1,
                  align: int = 32, mode: str = "auto", snapshot_rows: int = 0,
-                 flat_params: torch.Tensor | None = None):
+                 flat_params: torch.Tensor | None = None, p2p_ctas: int = 0):
         if not params:
             raise ConfigError("an app needs at least one trainable parameter")
         dev = params[0].device
@@ -206,6 +206,7 @@ class FusedGradientSync:
             self._p2p.momentum_buf = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else None
             self._p2p.numel = self.shard
             self._p2p.nranks = self.ranks
+            self._p2p.max_ctas = int(p2p_ctas)
             self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
             self._finish_init(settings)
             return

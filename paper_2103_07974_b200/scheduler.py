@@ -207,7 +207,7 @@ class CrossoverScheduler:
                  record_weights: bool = False, align: int = 32, sync_mode: str = "auto",
                  time_kernels: bool = False, comm_priority: int = -1,
                  perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0,
-                 nvtx: bool = False):
+                 nvtx: bool = False, p2p_ctas: int | None = None):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -223,6 +223,7 @@ class CrossoverScheduler:
         self.perturb = perturb
         self.watchdog_s = watchdog_s
         self.nvtx = nvtx
+        self.p2p_ctas = p2p_ctas
         with torch.cuda.device(self.device):
             self.compute_stream = torch.cuda.Stream(self.device)
             lo, hi = torch.cuda.Stream.priority_range()
@@ -245,9 +246,14 @@ class CrossoverScheduler:
         for p in app.params:
             if p.device != self.device:
                 raise ConfigError(f"job {app.job_id!r}: parameters must be on {self.device}")
+        # SM footprint of the fused P2P sync: under crossover it overlaps another app's compute
+        # and has that compute as slack, so it holds few SMs (32 CTAs, ~NCCL's channel count);
+        # the sequential baseline runs it alone and uses the whole GPU (2 CTAs per SM).
+        p2p_ctas = self.p2p_ctas if self.p2p_ctas is not None else (
+            32 if self.policy is Policy.CROSSOVER else 0)
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
                                  self.sync_mode, app.iterations if self.record_weights else 0,
-                                 flat_params=app.flat_params)
+                                 flat_params=app.flat_params, p2p_ctas=p2p_ctas)
         st = JobRuntimeState(app.job_id, app=app, sync=sync)
         self.states.append(st)
         return st

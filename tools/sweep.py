@@ -33,8 +33,8 @@ def main():
 
     h = Harness(args.nccl_max_ctas)
     if args.p2p_ctas:
-        from paper_2103_07974_b200 import _lib
-        _lib.tune("p2p_ctas", args.p2p_ctas)
+        import bench
+        bench.P2P_CTAS = args.p2p_ctas
     rows = []
     for mb in [int(x) for x in args.sizes_mb.split(",")]:
         flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if h.world > 1 else False
