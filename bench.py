@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-batch", type=int, default=2)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
+    ap.add_argument("--scenario", default="", help="run a reference scenario JSON file's jobs")
+    ap.add_argument("--scenario-time-scale", type=float, default=0.02,
+                    help="multiplier on inline scenario jobs' forward/backward ms")
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
     ap.add_argument("--sync-ctas", type=int, default=0, help="persistent grid cap of K1/K2")
     ap.add_argument("--comm-priority", default="high", choices=["high", "low"],
@@ -403,7 +406,18 @@ def run_ours(args):
     if args.sync_mode == "auto":
         args.sync_mode = "p2p" if world > 1 else "auto"
     flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False
-    if args.mix:
+    if args.scenario:
+        # a reference scenario file (colosim JSON) as device apps: profile jobs -> the model,
+        # inline jobs -> exact tensor split + calibrated GEMM compute (paper_2103_07974_b200.scenario)
+        from paper_2103_07974_b200.scenario import load_config
+        sc = load_config(args.scenario)
+        base = list(sc.device_plan(dev, 1, batch={"resnet50": args.batch, "vgg16": args.batch},
+                                   time_scale=args.scenario_time_scale, workers=world, flat=flat,
+                                   graphed=not args.no_graphs, fast_bn=not args.aten_bn,
+                                   seed=1000 * rank).jobs)
+        args.mix = f"scenario {sc.name}"
+        args.no_e2e, args.no_cpu_baseline = True, True
+    elif args.mix:
         base = []
         for j, item in enumerate(args.mix.split(",")):
             name, b = item.split(":")
@@ -486,7 +500,8 @@ def run_ours(args):
             "steps": K, "warmup": W, "ms_per_step": round(rot_cross, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights, N(0,1) images / random labels)",
-            "config": {"workload": (f"mix {args.mix} co-located, crossover" if args.mix else
+            "config": {"workload": (f"{args.mix} co-located, crossover" if args.scenario else
+                                    f"mix {args.mix} co-located, crossover" if args.mix else
                                     f"{args.jobs}x {args.model} co-located, crossover, batch "
                                     f"{args.batch}/GPU")
                                    + ", bf16 autocast, fp32 params/grads, SGD momentum 0.9"

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass
+from typing import Sequence
 from enum import Enum
 
 import numpy as np
@@ -391,13 +392,19 @@ class _SyntheticModel(torch.nn.Module):
 
 def synthetic_app(job_id: str, bucket_bytes: int, iterations: int, device: torch.device,
                   gemm_n: int = 8192, gemm_reps: int = 3, n_tensors: int = 16, seed: int = 0,
-                  sgd: SgdSettings = SgdSettings(lr=1e-3), flat: bool = False) -> App:
+                  sgd: SgdSettings = SgdSettings(lr=1e-3), flat: bool = False,
+                  tensor_bytes: Sequence[int] | None = None) -> App:
     """An app whose compute is a fixed bf16 GEMM chain (gemm_reps x [n,n]@[n,n]) and whose
     fused gradient is `bucket_bytes` of fp32 (mirrors cli._payload_for_ratio, cli.py:79-98:
-    the sweep dials the payload against a fixed compute time)."""
-    numel = max(bucket_bytes // 4, n_tensors)
-    sizes = [numel // n_tensors] * n_tensors
-    sizes[-1] += numel - sum(sizes)
+    the sweep dials the payload against a fixed compute time).  ``tensor_bytes`` gives the
+    exact per-tensor payload instead (a scenario job's split, scenario.py:114-119); each
+    tensor holds ceil(bytes / 4) fp32 elements, at least one."""
+    if tensor_bytes is not None:
+        sizes = [max(1, (int(b) + 3) // 4) for b in tensor_bytes]
+    else:
+        numel = max(bucket_bytes // 4, n_tensors)
+        sizes = [numel // n_tensors] * n_tensors
+        sizes[-1] += numel - sum(sizes)
     model = _SyntheticModel(sizes, seed, device)
     g = torch.Generator(device=device).manual_seed(seed)
     a = torch.randn(gemm_n, gemm_n, device=device, dtype=torch.bfloat16, generator=g)

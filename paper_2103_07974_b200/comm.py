@@ -24,6 +24,7 @@ from .workload import FusedGradient, JobProfile, comp_time, fuse_gradients
 
 __all__ = [
     "Architecture",
+    "comm_time_ps",
     "ClusterSpec",
     "SyncRequest",
     "comm_time_allreduce",
@@ -40,22 +41,27 @@ NVLINK5_GBPS = 900.0  # per direction per GPU, nominal
 
 
 class Architecture(Enum):
+    """Predictor topologies (comm.py:39-41).  The device always syncs over NVLink collectives;
+    ``parameter_server`` exists so the reference's scenario files price the same way."""
+
+    PARAMETER_SERVER = "parameter_server"
     RING_ALLREDUCE = "ring_allreduce"
 
 
 @dataclass(frozen=True)
 class ClusterSpec:
-    """Cluster description for the predictor (comm.py:44-71); ring all-reduce only."""
+    """Cluster description for the predictor (comm.py:44-71)."""
 
     workers: int
     bandwidth_bytes_per_sec: int
     latency_per_message: int = 0
     architecture: Architecture = Architecture.RING_ALLREDUCE
     gpus_per_worker: int = 1
+    ps_servers: int = 1
 
     def __post_init__(self):
         if not isinstance(self.architecture, Architecture):
-            raise ConfigError("only ring_allreduce is supported on the NVSwitch path")
+            raise ConfigError(f"cluster.architecture: {self.architecture!r} is not an Architecture")
         if self.workers < 1:
             raise ConfigError("cluster.workers must be >= 1")
         if self.gpus_per_worker < 1:
@@ -64,6 +70,8 @@ class ClusterSpec:
             raise ConfigError("cluster.bandwidth must be > 0")
         if self.latency_per_message < 0:
             raise ConfigError("cluster.latency must be >= 0")
+        if self.architecture is Architecture.PARAMETER_SERVER and self.ps_servers < 1:
+            raise ConfigError("cluster.ps_servers must be >= 1 for parameter_server")
 
     @staticmethod
     def nvswitch(workers: int, busbw_gbps: float = 725.0, latency_ns: int = 10_000) -> "ClusterSpec":
@@ -82,6 +90,8 @@ class SyncRequest:
 
 def comm_time_allreduce(size_bytes: int, cluster: ClusterSpec) -> int:
     """Ring all-reduce duration, integer ns with ceiling rounding; 0 at W=1 (comm.py:87-99)."""
+    if cluster.architecture is not Architecture.RING_ALLREDUCE:
+        raise ConfigError("comm_time_allreduce requires architecture=ring_allreduce")
     if size_bytes < 0:
         raise ValueError("size_bytes must be >= 0")
     w = cluster.workers
@@ -92,13 +102,30 @@ def comm_time_allreduce(size_bytes: int, cluster: ClusterSpec) -> int:
     return 2 * (w - 1) * cluster.latency_per_message + (num + den - 1) // den
 
 
+def comm_time_ps(size_bytes: int, cluster: ClusterSpec) -> int:
+    """Parameter-server push + pull through the worker NIC, integer ns, ceiling (comm.py:102-110)."""
+    if cluster.architecture is not Architecture.PARAMETER_SERVER:
+        raise ConfigError("comm_time_ps requires architecture=parameter_server")
+    if size_bytes < 0:
+        raise ValueError("size_bytes must be >= 0")
+    den = cluster.bandwidth_bytes_per_sec
+    return 2 * cluster.latency_per_message + (2 * size_bytes * NS_PER_S + den - 1) // den
+
+
+def _priced(size_bytes: int, cluster: ClusterSpec) -> int:
+    if cluster.architecture is Architecture.PARAMETER_SERVER:
+        return comm_time_ps(size_bytes, cluster)
+    return comm_time_allreduce(size_bytes, cluster)
+
+
 def comm_time(request: SyncRequest, cluster: ClusterSpec) -> int:
-    return comm_time_allreduce(request.payload.size_bytes, cluster)
+    """One sync under the cluster's architecture (comm.py:119-121)."""
+    return _priced(request.payload.size_bytes, cluster)
 
 
 def comm_time_unfused(messages: Iterable[FusedGradient], cluster: ClusterSpec) -> int:
     """Per-tensor messages each pay the latency term (comm.py:124-126)."""
-    return sum(comm_time_allreduce(m.size_bytes, cluster) for m in messages)
+    return sum(_priced(m.size_bytes, cluster) for m in messages)
 
 
 def comm_comp_ratio(job: JobProfile, cluster: ClusterSpec) -> Fraction:

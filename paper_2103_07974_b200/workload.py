@@ -27,6 +27,8 @@ __all__ = [
     "BucketLayout",
     "tensor_specs_from_module",
     "profile_from_module",
+    "fixture_names",
+    "fixture_profile",
 ]
 
 FP32_BYTES = 4
@@ -180,3 +182,58 @@ def profile_from_module(module, job_id: str, forward_time: int, backward_time: i
 
 def total_bytes(specs: Iterable[TensorSpec]) -> int:
     return sum(s.size_bytes for s in specs)
+
+
+# Bundled calibration profiles (colosim/data/profiles.json, read by workload.py:118-142): the
+# reference pins order-of-magnitude P100 step times at batch 32 and the models' fp32 parameter
+# tensors.  The times are restated here; the tensor tables are taken from the torchvision model
+# itself (built on the meta device, no allocation) -- tests/test_scenario.py checks both against
+# the reference's fixture, tensor by tensor.
+_FIXTURE_TIMES = {"resnet50": (75_000_000, 155_000_000, 100),
+                  "vgg16": (190_000_000, 390_000_000, 100)}
+
+
+def fixture_names() -> list[str]:
+    return sorted(_FIXTURE_TIMES)
+
+
+def fixture_profile(name: str, job_id: str | None = None,
+                    iterations: int | None = None) -> JobProfile:
+    """The reference's named profile (workload.py:128-142) as a JobProfile."""
+    if name not in _FIXTURE_TIMES:
+        raise KeyError(f"unknown fixture profile {name!r}; available: {fixture_names()}")
+    import torch
+    import torchvision
+
+    with torch.device("meta"):
+        module = getattr(torchvision.models, name)()
+    specs = tensor_specs_from_module(module)
+    if name == "vgg16":
+        specs = _vgg_layer_names(module, specs)
+    fwd, bwd, iters = _FIXTURE_TIMES[name]
+    return JobProfile(job_id if job_id is not None else name, fwd, bwd, specs,
+                      iterations if iterations is not None else iters)
+
+
+def _vgg_layer_names(module, specs: tuple[TensorSpec, ...]) -> tuple[TensorSpec, ...]:
+    """torchvision's ``features.<i>`` / ``classifier.<i>`` -> the paper's convB_L / fcK names
+    (the fixture's naming); block B advances at each max-pool."""
+    import torch
+
+    rename, block, layer = {}, 1, 0
+    for i, m in enumerate(module.features):
+        if isinstance(m, torch.nn.MaxPool2d):
+            block, layer = block + 1, 0
+        elif isinstance(m, torch.nn.Conv2d):
+            layer += 1
+            rename[f"features.{i}"] = f"conv{block}_{layer}"
+    fc = 0
+    for i, m in enumerate(module.classifier):
+        if isinstance(m, torch.nn.Linear):
+            fc += 1
+            rename[f"classifier.{i}"] = f"fc{fc}"
+    out = []
+    for t in specs:
+        prefix, _, leaf = t.name.rpartition(".")
+        out.append(TensorSpec(f"{rename.get(prefix, prefix)}.{leaf}", t.size_bytes))
+    return tuple(out)

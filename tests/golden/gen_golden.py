@@ -10,6 +10,9 @@ Outputs (committed, small):
   equivalence.npz    reference fp64 trajectories of run_crossover / run_isolated for a
                      grid of (jobs, workers, loss, T) plus one perturbed run
   fixtures.json      reference fixture bucket inventories (resnet50, vgg16 sizes)
+  scenarios.json     the reference's scenario files (pkg/scenarios/*.json) with the reference
+                     parser's result and simulated makespan for each, plus ~30 malformed
+                     documents with the reference parser's exact error message
 
 The GPU box has no /root/reference: tests there read only these files.
 """
@@ -103,7 +106,127 @@ def main() -> None:
                           "sizes": [t.size_bytes for t in prof.tensors],
                           "names": [t.name for t in prof.tensors]}
     (OUT / "fixtures.json").write_text(json.dumps(fixtures, separators=(",", ":")) + "\n")
+    scenario_golden()
     print("wrote", sorted(p.name for p in OUT.iterdir()))
+
+
+def scenario_golden() -> None:
+    import copy
+    import math
+
+    from colosim.comm import SyncRequest, comm_time
+    from colosim.errors import ConfigError
+    from colosim.scenario import parse_scenario
+    from colosim.workload import fuse_gradients
+    from colosim.scheduler import simulate
+
+    def parsed(sc):
+        c = sc.cluster
+        return {"name": sc.name, "policy": sc.policy.value, "override": sc.iterations_override,
+                "cluster": [c.workers, c.gpus_per_worker, c.bandwidth_bytes_per_sec,
+                            c.latency_per_message, c.architecture.value, c.ps_servers],
+                "jobs": [[j.job_id, j.forward_time, j.backward_time, j.iterations,
+                          [[t.name, t.size_bytes] for t in j.tensors]] for j in sc.jobs],
+                "comm_ns": [comm_time(SyncRequest(j.job_id, 1, fuse_gradients(j, 1)), c)
+                            for j in sc.jobs]}
+
+    files = {}
+    for f in sorted((REF.parent / "scenarios").glob("*.json")):
+        doc = json.loads(f.read_text())
+        sc = parse_scenario(doc, origin=f.name)
+        out = parsed(sc)
+        for iters in (None, 3):
+            plan = sc.plan(iters)
+            tr = simulate(plan)
+            out[f"makespan_iters_{iters}"] = tr.makespan
+            out[f"spans_iters_{iters}"] = len(tr.spans)
+        files[f.name] = {"doc": doc, "parsed": out}
+
+    base = files["speedup_band.json"]["doc"]
+    ps = files["vgg16_2jobs_10g.json"]["doc"]
+
+    def mut(fn, src=None):
+        d = copy.deepcopy(base if src is None else src)
+        fn(d)
+        return d
+
+    def setk(path, value):
+        def f(d):
+            o = d
+            for k in path[:-1]:
+                o = o[k]
+            o[path[-1]] = value
+        return f
+
+    def delk(path):
+        def f(d):
+            o = d
+            for k in path[:-1]:
+                o = o[k]
+            del o[path[-1]]
+        return f
+
+    bad = [
+        ("top_level_array", [1, 2]),
+        ("missing_name", mut(delk(["name"]))),
+        ("empty_name", mut(setk(["name"], ""))),
+        ("unknown_policy", mut(setk(["policy"], "fifo"))),
+        ("missing_policy", mut(delk(["policy"]))),
+        ("jobs_not_list", mut(setk(["jobs"], {}))),
+        ("empty_jobs", mut(setk(["jobs"], []))),
+        ("job_not_object", mut(setk(["jobs", 0], 7))),
+        ("job_missing_id", mut(delk(["jobs", 0, "job_id"]))),
+        ("job_empty_id", mut(setk(["jobs", 0, "job_id"], ""))),
+        ("duplicate_ids", mut(setk(["jobs", 1, "job_id"], "band-a"))),
+        ("unknown_profile", mut(setk(["jobs", 0], {"job_id": "x", "profile": "alexnet"}))),
+        ("profile_bad_iterations", mut(setk(["jobs", 0], {"job_id": "x", "profile": "vgg16", "iterations": 0}))),
+        ("inline_missing_iterations", mut(delk(["jobs", 0, "iterations"]))),
+        ("inline_bool_iterations", mut(setk(["jobs", 0, "iterations"], True))),
+        ("inline_float_iterations", mut(setk(["jobs", 0, "iterations"], 2.0))),
+        ("missing_forward", mut(delk(["jobs", 0, "forward_ms"]))),
+        ("missing_grad", mut(delk(["jobs", 1, "grad_mb"]))),
+        ("tensor_count_zero", mut(setk(["jobs", 0, "tensor_count"], 0))),
+        ("tensor_count_huge", mut(setk(["jobs", 0, "tensor_count"], 10001))),
+        ("negative_grad", mut(setk(["jobs", 0, "grad_mb"], -1))),
+        ("sub_unit_forward", mut(setk(["jobs", 0, "forward_ms"], 1e-7))),
+        ("sub_unit_grad", mut(setk(["jobs", 0, "grad_mb"], 0.0000005))),
+        ("negative_backward", mut(setk(["jobs", 0, "backward_ms"], -1))),
+        ("zero_compute", mut(lambda d: d["jobs"][0].update(forward_ms=0, backward_ms=0))),
+        ("string_number", mut(setk(["jobs", 0, "forward_ms"], "30"))),
+        ("bool_number", mut(setk(["jobs", 0, "backward_ms"], False))),
+        ("overflow", mut(setk(["jobs", 0, "grad_mb"], 1e30))),
+        ("infinite", mut(setk(["jobs", 0, "forward_ms"], math.inf))),
+        ("nan", mut(setk(["jobs", 0, "forward_ms"], math.nan))),
+        ("override_zero", mut(setk(["iterations_override"], 0))),
+        ("missing_cluster", mut(delk(["cluster"]))),
+        ("cluster_not_object", mut(setk(["cluster"], [4]))),
+        ("unknown_architecture", mut(setk(["cluster", "architecture"], "mesh"))),
+        ("missing_architecture", mut(delk(["cluster", "architecture"]))),
+        ("zero_bandwidth", mut(setk(["cluster", "bandwidth_gbps"], 0))),
+        ("sub_unit_bandwidth", mut(setk(["cluster", "bandwidth_gbps"], 1e-10))),
+        ("zero_workers", mut(setk(["cluster", "workers"], 0))),
+        ("missing_workers", mut(delk(["cluster", "workers"]))),
+        ("zero_gpus_per_worker", mut(setk(["cluster", "gpus_per_worker"], 0))),
+        ("negative_latency", mut(setk(["cluster", "latency_us"], -1))),
+        ("sub_unit_latency", mut(setk(["cluster", "latency_us"], 0.0001))),
+        ("zero_ps_servers", mut(setk(["cluster", "ps_servers"], 0), ps)),
+    ]
+    errors = []
+    for name, doc in bad:
+        try:
+            parse_scenario(doc, origin="bad.json")
+            msg = None
+        except ConfigError as exc:
+            msg = str(exc)
+        # json cannot carry inf / nan: keep them as markers the test turns back into floats
+        text = json.dumps(doc).replace("Infinity", '"__inf__"').replace("NaN", '"__nan__"')
+        errors.append({"name": name, "doc": json.loads(text), "error": msg})
+    ok = [{"name": "layered_override", "doc": mut(lambda d: d["jobs"].__setitem__(
+        0, {"job_id": "r", "profile": "resnet50", "iterations": 7}))}]
+    for o in ok:
+        o["parsed"] = parsed(parse_scenario(o["doc"], origin="ok.json"))
+    (OUT / "scenarios.json").write_text(json.dumps({"files": files, "errors": errors, "ok": ok},
+                                                   separators=(",", ":")) + "\n")
 
 
 if __name__ == "__main__":
