@@ -62,9 +62,11 @@ def parse():
     ap.add_argument("--metrics-out", default="", help="colosim.metrics/v1 JSON + CSV of the measured runs")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"],
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
-                         "the fused NVLink P2P kernel; auto = p2p (bucket if peers cannot be mapped)")
+                         "the fused NVLink P2P kernel; ce = copy-engine pulls + shard K2; auto = ce "
+                         "under crossover and p2p for the sequential arm (bucket if peers cannot "
+                         "be mapped)")
     return ap.parse_args()
 
 
@@ -87,8 +89,9 @@ NVLINK_P2P_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
 
 
 def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: str,
-                  isolated: dict | None = None) -> dict:
-    """Roofline of the path's dominant kernel: K2 (HBM) or, in p2p mode, the fused NVLink kernel.
+                  isolated: dict | None = None, sync_seq=None) -> dict:
+    """Roofline of the path's dominant kernel: K2 (HBM), or in p2p mode the fused NVLink kernel,
+    or in ce mode the shard K2 with the copy-engine transport beside it.
 
     Under crossover the P2P kernel is launched on a deliberately small grid (it overlaps the
     other app's compute and only has to finish inside it), so its live fraction is low by
@@ -115,6 +118,25 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
                                  "frac": round(k1["GB/s"] / hbm_peak, 4), "bytes_per_launch": k1["bytes"]}
         return out
     k2 = kernels.get("k2_update", {"GB/s": 0.0})
+    if "c1_ce_reduce_scatter" in kernels:
+        # copy-engine transport: K2 (on the shard, W sources) is the dominant kernel of ours;
+        # the two CE copy phases are reported against the NVLink peer-copy peak beside it
+        t = kernels["c1_ce_reduce_scatter"]["ms"] + kernels["c1_ce_all_gather"]["ms"]
+        ach = sync.c1_bus_bytes() / (t / 1e3) / 1e9
+        out = {"kernel": "k2_update (W-source shard reduce, /W, SGD-momentum) beside copy-engine "
+                         "reduce-scatter / all-gather pulls", "bound": "hbm",
+                "achieved": k2["GB/s"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(k2["GB/s"] / hbm_peak, 4), "traffic": None,
+                "peak_kind": peak_kind, "bytes_per_launch": sync.k2_bytes(),
+                "transport": {"engine": "copy engines (cudaMemcpyAsync peer pulls, no SM)",
+                              "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
+                              "frac": round(ach / NVLINK_P2P_GBS, 4),
+                              "bytes_per_sync": sync.c1_bus_bytes()}}
+        if isolated and sync_seq is not None and sync_seq.mode == "p2p":
+            seq_line = roofline_line(isolated, sync_seq, hbm_peak, peak_kind, model)
+            out["sequential_arm"] = {k: seq_line[k] for k in ("kernel", "bound", "achieved", "peak",
+                                                               "unit", "frac", "grid_cap_ctas")}
+        return out
     return {"kernel": "k2_update (fused 1/W average + SGD-momentum)", "bound": "hbm",
             "achieved": k2["GB/s"], "peak": hbm_peak, "unit": "GB/s",
             "frac": round(k2["GB/s"] / hbm_peak, 4),
@@ -365,7 +387,7 @@ def kernel_summary(kern: dict, sync) -> dict:
         t = statistics.mean(kern["k1_pack"])
         out["k1_pack"] = {"ms": round(t, 4), "bytes": sync.k1_bytes(),
                           "GB/s": round(sync.k1_bytes() / (t / 1e3) / 1e9, 1)}
-    for name in ("c1_reduce_scatter", "c1_all_gather"):
+    for name in ("c1_reduce_scatter", "c1_all_gather", "c1_ce_reduce_scatter", "c1_ce_all_gather"):
         if name in kern:
             t = statistics.mean(kern[name])
             out[name] = {"ms": round(t, 4), "bus_bytes": sync.c1_bus_bytes() / 2,
@@ -403,9 +425,10 @@ def run_ours(args):
         _lib.tune("sync_ctas", args.sync_ctas)
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
-    if args.sync_mode == "auto":
-        args.sync_mode = "p2p" if world > 1 else "auto"
-    flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if world > 1 else False
+    # auto at W > 1: IPC flat parameters, and the scheduler picks the transport per policy
+    # (copy engines under crossover, the fused P2P kernel for the sequential baseline)
+    flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc"}.get(args.sync_mode, False)
+            if world > 1 else False)
     if args.scenario:
         # a reference scenario file (colosim JSON) as device apps: profile jobs -> the model,
         # inline jobs -> exact tensor split + calibrated GEMM compute (paper_2103_07974_b200.scenario)
@@ -440,15 +463,15 @@ def run_ours(args):
 
     sm = args.sync_mode
     prio = -1 if args.comm_priority == "high" else 0
-    if sm == "p2p":
+    if world > 1 and sm in ("p2p", "ce", "auto"):
         # probe once (collective): if any rank cannot map its peers, everyone falls back to bucket
         from paper_2103_07974_b200.errors import ConfigError
         try:
-            probe = timed_run(h, base, Policy.CROSSOVER, 0, 1, sync_mode="p2p", comm_priority=prio)
+            probe = timed_run(h, base, Policy.CROSSOVER, 0, 1, sync_mode=sm, comm_priority=prio)
             del probe
         except ConfigError as exc:
             if rank == 0:
-                print(f"p2p sync unavailable ({exc}); using the bucket all-reduce", file=sys.stderr)
+                print(f"{sm} sync unavailable ({exc}); using the bucket all-reduce", file=sys.stderr)
             sm = args.sync_mode = "bucket"
     cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio)
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio)
@@ -477,7 +500,8 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
     sync0 = cross["sched"].states[0].sync
     kernels = kernel_summary(cross["kernels"], sync0)
-    kernels_isolated = kernel_summary(seq["kernels"], sync0)
+    sync_seq = seq["sched"].states[0].sync
+    kernels_isolated = kernel_summary(seq["kernels"], sync_seq)
 
     out = None
     if rank == 0:
@@ -509,7 +533,8 @@ def run_ours(args):
                                    + ("" if args.aten_bn else ", NHWC BN(+ReLU/+residual) and max-pool kernels"),
                        "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
-                       "sync_mode": sync0.mode},
+                       "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
+                                     {"crossover": sync0.mode, "sequential": sync_seq.mode})},
             "speedup_vs_sequential": round(rot_seq / rot_cross, 4),
             "sequential": {"value": round(seq_value, 2), "ms_per_step": round(rot_seq, 3)},
             "rho": round(sum(comm_t) / sum(comp), 5) if sum(comp) else None,
@@ -520,7 +545,7 @@ def run_ours(args):
                                  "comp_ms": [round(c, 4) for c in comp],
                                  "comm_ms": [round(c, 4) for c in comm_t]},
             "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind, args.model,
-                                      kernels_isolated),
+                                      kernels_isolated, sync_seq),
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
             "gpu_launches": cross["launches"] + bn_launches * K,

@@ -176,6 +176,10 @@ CS_API int cs_device_free(void* ptr);
 CS_API int cs_ipc_get_handle(void* ptr, uint8_t* out /* CS_IPC_HANDLE_BYTES */);
 CS_API int cs_ipc_open_handle(const uint8_t* handle, void** ptr);
 CS_API int cs_ipc_close_handle(void* ptr);
+/* Stream-ordered copy by the copy engines (cudaMemcpyAsync, cudaMemcpyDefault): src / dst may be
+ * local or peer-mapped (IPC) device memory, so a pull from a peer crosses NVLink without
+ * occupying any SM -- the transport of the "ce" sync mode. */
+CS_API int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
 /* channels_last BatchNorm2d (training) for the apps' compute: x / y / dy / dx / residual are
  * bf16 [M, C] row-major (M = N*H*W, C % 8 == 0, C <= 256 or C % 256 == 0), weight / bias /

@@ -235,6 +235,13 @@ int cs_ipc_open_handle(const uint8_t* handle, void** ptr) {
   return cuda_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
 }
 
+int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return 0;
+  if (dst == nullptr || src == nullptr) return set_error(CS_ERR_ARG, "cs_copy_async: NULL pointer");
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream),
+                     "cs_copy_async");
+}
+
 int cs_ipc_close_handle(void* ptr) {
   if (ptr == nullptr) return 0;
   return cuda_status(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");

@@ -129,18 +129,18 @@ class FusedGradientSync:
                 mode = "direct"
             else:
                 mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
-        if mode not in ("bucket", "direct", "sharded", "p2p", "unfused"):
+        if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "unfused"):
             raise ConfigError(f"unknown sync mode {mode!r}")
         if mode == "direct" and self.workers != 1:
             raise ConfigError("direct mode has no bucket and needs exactly one worker")
         if mode == "unfused" and self.local_workers != 1:
             raise ConfigError("unfused mode all-reduces each gradient tensor in place: one worker per rank")
-        if mode in ("sharded", "p2p") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
+        if mode in ("sharded", "p2p", "ce") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
             raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
                               "and one worker per rank")
         self.mode = mode
         self.flat = flat_params
-        sharded = mode in ("sharded", "p2p")
+        sharded = mode in ("sharded", "p2p", "ce")
         multiple = align * self.ranks if sharded else None
         self.layout = BucketLayout.build([p.numel() for p in self.params], align, multiple=multiple)
         if sharded:
@@ -156,13 +156,13 @@ class FusedGradientSync:
 
         self.bucket = None
         self._peer_maps = []
-        if mode == "p2p":
+        if mode in ("p2p", "ce"):
             from .p2p import DeviceBuffer, buffer_of
 
             if self.ranks > _lib.CS_MAX_SOURCES:
-                raise ConfigError(f"p2p sync supports up to {_lib.CS_MAX_SOURCES} ranks")
+                raise ConfigError(f"{mode} sync supports up to {_lib.CS_MAX_SOURCES} ranks")
             if buffer_of(flat_params) is None:
-                raise ConfigError("p2p sync needs IPC-capable flat parameters (flatten_parameters(ipc=True))")
+                raise ConfigError(f"{mode} sync needs IPC-capable flat parameters (flatten_parameters(ipc=True))")
             self._bucket_buf = DeviceBuffer(lay.total, dev)
             self.bucket = self._bucket_buf.tensor
         elif mode in ("bucket", "sharded"):
@@ -210,6 +210,34 @@ class FusedGradientSync:
             self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
             self._finish_init(settings)
             return
+        if mode == "ce":
+            # copy-engine transport: pull every peer's copy of my bucket shard (reduce-scatter
+            # half), K2 over the W shard copies in rank order, pull every peer's updated
+            # parameter shard (all-gather half).  No SM moves a byte across NVLink.
+            from .p2p import buffer_of, exchange_peer_addresses
+
+            off = self.rank * self.shard * 4
+            bmap = exchange_peer_addresses(self._bucket_buf, self.rank, self.ranks)
+            fmap = exchange_peer_addresses(buffer_of(flat_params), self.rank, self.ranks)
+            self._peer_maps = [bmap, fmap]
+            self._recv = torch.empty(lay.total, dtype=torch.float32, device=dev)
+            sb = self.shard * 4
+            self._ce_rs = [(self._recv.data_ptr() + s * sb, bmap.addresses[s] + off)
+                           for s in range(self.ranks) if s != self.rank]
+            f = flat_params.data_ptr()
+            self._ce_ag = [(f + s * sb, fmap.addresses[s] + s * sb)
+                           for s in range(self.ranks) if s != self.rank]
+            self._upd = np.zeros(1, dtype=_lib.UPDATE_DESC)
+            self._upd["param"] = f + off
+            if self.momentum_bufs is not None:
+                self._upd["momentum_buf"] = self.momentum_bufs[0].data_ptr()
+            self._upd["numel"] = self.shard
+            self._sources = np.asarray([self.bucket.data_ptr() + off if s == self.rank
+                                        else self._recv.data_ptr() + s * sb
+                                        for s in range(self.ranks)], dtype=np.uint64)
+            self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
+            self._finish_init(settings)
+            return
         if mode == "sharded":
             # one flat range: this rank's shard of the parameters, bucket and momentum
             off = self.rank * self.shard * 4
@@ -251,7 +279,7 @@ class FusedGradientSync:
     # -- per-iteration pieces (all asynchronous on `stream`) -----------------
     def pack(self, grads_per_worker: Sequence[Sequence[torch.Tensor]], stream: int) -> None:
         """K1: gather each worker's gradients into its bucket row."""
-        if self.mode not in ("bucket", "sharded", "p2p"):
+        if self.mode not in ("bucket", "sharded", "p2p", "ce"):
             raise ConfigError("pack() needs bucket mode")
         n = len(self.params)
         if len(grads_per_worker) != self.local_workers:
@@ -274,7 +302,7 @@ class FusedGradientSync:
                 raise ValueError("direct mode needs the gradient tensors")
             self._upd["grad_offset"] = _grad_ptrs(grads, self.params)
         snap = 0
-        if snapshot_row is not None and self.mode != "sharded":
+        if snapshot_row is not None and self.mode not in ("sharded", "ce"):
             if self.snapshot is None:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
             snap = self.snapshot[snapshot_row].data_ptr()
@@ -321,6 +349,9 @@ class FusedGradientSync:
             return
         if self.mode == "p2p":
             self._p2p_tail(stream, snapshot_row, timer)
+            return
+        if self.mode == "ce":
+            self._ce_tail(stream, snapshot_row, timer)
             return
         if self.comm is not None and self.comm.active:
             if timer is not None:
@@ -378,6 +409,42 @@ class FusedGradientSync:
             with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
                 self.snapshot[snapshot_row].copy_(self.flat)
 
+    def _ce_copies(self, pairs, stream: int) -> None:
+        nbytes = self.shard * 4
+        for dst, src in pairs:
+            _lib.check("cs_copy_async", _lib.lib.cs_copy_async(dst, src, nbytes, stream))
+
+    def _ce_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
+        """barrier -> CE pulls of my shard from every peer -> K2 (rank-order sum, /W, SGD) on the
+        shard -> barrier -> CE pulls of every peer's updated shard into the flat parameters.
+
+        The second barrier orders three things: every rank's shard is updated before anyone
+        pulls it, every peer has finished reading my bucket before my next K1 rewrites it, and
+        (by stream order on each peer) a peer's all-gather pulls of iteration t complete before
+        it enters iteration t+1's first barrier, so my K2 at t+1 never races them."""
+        bar = self._barrier.data_ptr()
+        self.comm.all_reduce_(bar, 1, stream)          # every rank's K1 has landed
+        if timer is not None:
+            timer.begin("c1_ce_reduce_scatter")
+        self._ce_copies(self._ce_rs, stream)
+        if timer is not None:
+            timer.end("c1_ce_reduce_scatter")
+            timer.begin("k2_update")
+        self.update(stream, None, None)
+        if timer is not None:
+            timer.end("k2_update")
+        self.comm.all_reduce_(bar, 1, stream)          # every shard updated, every bucket read
+        if timer is not None:
+            timer.begin("c1_ce_all_gather")
+        self._ce_copies(self._ce_ag, stream)
+        if timer is not None:
+            timer.end("c1_ce_all_gather")
+        if snapshot_row is not None:
+            if self.snapshot is None:
+                raise ConfigError("no snapshot buffer (snapshot_rows=0)")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.snapshot[snapshot_row].copy_(self.flat)
+
     def close(self) -> None:
         for m in self._peer_maps:
             m.close()
@@ -393,6 +460,9 @@ class FusedGradientSync:
             return (2 * self.ranks + 1 + (2 if self.settings.momentum else 0)) * self.shard * 4
         if self.mode == "sharded":
             return (5 if self.settings.momentum else 3) * self.shard * 4
+        if self.mode == "ce":
+            # W source shards + p read/write (+ momentum read/write)
+            return (self.ranks + 2 + (2 if self.settings.momentum else 0)) * self.shard * 4
         s = self.layout.payload_bytes
         streams = self.local_workers if self.mode == "bucket" else 1
         per = (streams + 2) * s            # read sources + read p + write p

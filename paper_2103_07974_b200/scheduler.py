@@ -252,11 +252,27 @@ class CrossoverScheduler:
         p2p_ctas = self.p2p_ctas if self.p2p_ctas is not None else (
             32 if self.policy is Policy.CROSSOVER else 0)
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
-                                 self.sync_mode, app.iterations if self.record_weights else 0,
+                                 self._mode_for(app), app.iterations if self.record_weights else 0,
                                  flat_params=app.flat_params, p2p_ctas=p2p_ctas)
         st = JobRuntimeState(app.job_id, app=app, sync=sync)
         self.states.append(st)
         return st
+
+    def _mode_for(self, app: App) -> str:
+        """Transport per policy when the caller left it to us.
+
+        With peer-mappable flat parameters at W > 1: under crossover the sync overlaps another
+        app's compute, so it goes through the copy engines ("ce": NVLink pulls that hold no SM,
+        ~1-6 % GEMM slowdown vs 15-100 % for SM-driven collectives, tools/cebench.py); the
+        sequential baseline has the GPU to itself and takes the fastest isolated path, the fused
+        P2P kernel on the full grid.  Both sum in rank order, so weights are bitwise identical."""
+        if self.sync_mode != "auto" or self.comm is None or self.comm.world < 2:
+            return self.sync_mode
+        from .p2p import buffer_of
+
+        if app.flat_params is None or buffer_of(app.flat_params) is None or app.local_workers != 1:
+            return self.sync_mode
+        return "ce" if self.policy is Policy.CROSSOVER else "p2p"
 
     @property
     def job_order(self) -> list[str]:

@@ -98,7 +98,8 @@ def main():
     # (3b) momentum on the reference's linear problems, every sync mode vs the fp64 oracle
     Tl = 20
     lin_m = {}
-    for mode, flat in (("bucket", False), ("sharded", True), ("p2p", "ipc"), ("unfused", False)):
+    for mode, flat in (("bucket", False), ("sharded", True), ("p2p", "ipc"), ("ce", "ipc"),
+                       ("unfused", False)):
         s7 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode=mode)
         for k, c in enumerate(lcfg):
             s7.register(linear_app(c, f"lm{k}", 40 + k, Tl, dev, local_workers=1, momentum=0.9, flat=flat))
@@ -119,6 +120,19 @@ def main():
     if world == 2:
         same = all(torch.equal(mom_w["bucket"][k], p2p_w[k][:, :n]) for k in range(2))
         res["checks"].append({"name": "p2p_bitwise_eq_allreduce_w2", "ok": bool(same)})
+
+    # (4b) copy-engine sync: CE pulls + K2 over the W shard copies in rank order -- the same
+    #      arithmetic as the P2P kernel, so bitwise equal to it at any W
+    s8 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode="ce")
+    for k, (ds, rs) in enumerate(specs):
+        s8.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T,
+                            dev, local_workers=1, worker_count=world, flat="ipc"))
+    s8.run()
+    ce_w = [s8.weights(f"m{k}").cpu() for k in range(2)]
+    s8.close()
+    res["checks"].append({"name": "ce_mode_used", "ok": all(st.sync.mode == "ce" for st in s8.states)})
+    res["checks"].append({"name": f"ce_bitwise_eq_p2p_w{world}",
+                          "ok": all(torch.equal(ce_w[k], p2p_w[k]) for k in range(2))})
 
     # every rank must hold identical weights after every iteration
     for k in range(2):

@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--gemm-reps", type=int, default=3)
     ap.add_argument("--out", default="")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "unfused"])
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"])
     ap.add_argument("--p2p-ctas", type=int, default=0)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
     args = ap.parse_args()
@@ -37,7 +37,7 @@ def main():
         bench.P2P_CTAS = args.p2p_ctas
     rows = []
     for mb in [int(x) for x in args.sizes_mb.split(",")]:
-        flat = {"sharded": True, "p2p": "ipc"}.get(args.sync_mode, False) if h.world > 1 else False
+        flat = {"sharded": True, "p2p": "ipc", "ce": "ipc"}.get(args.sync_mode, False) if h.world > 1 else False
         base = [synthetic_app(f"syn{j}", mb * 2**20, 1, h.dev, gemm_reps=args.gemm_reps, seed=j,
                               flat=flat) for j in range(2)]
         cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=args.sync_mode)
