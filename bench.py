@@ -364,6 +364,33 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     return out
 
 
+def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
+    """Peer-mapping probe and (sync_mode auto, W > 1) transport calibration before any timed run.
+
+    Collective: if any rank cannot map its peers, every rank falls back to the bucket all-reduce.
+    In auto mode the probe is an untimed adaptive crossover run (like cudnn.benchmark) whose
+    tuner measures the copy-engine and the P2P-kernel transports (scheduler._TransportTuner);
+    the timed crossover arm then runs the chosen one and the sequential arm the full-grid P2P
+    kernel.  Returns (crossover mode, sequential mode, tuner summary or None)."""
+    from paper_2103_07974_b200.errors import ConfigError
+    from paper_2103_07974_b200.scheduler import Policy, _TransportTuner
+
+    if h.world < 2 or sm not in ("p2p", "ce", "auto"):
+        return sm, sm, None
+    try:
+        n_cal = _TransportTuner.MIN_BUDGET if sm == "auto" else 1
+        probe = timed_run(h, base, Policy.CROSSOVER, 0, n_cal, sync_mode=sm, comm_priority=prio,
+                          time_kernels=False)
+        tuner = probe["sched"].tuner
+        if sm == "auto" and tuner is not None and tuner.active:
+            return tuner.choice, "p2p", tuner.summary()
+        return sm, sm, None
+    except ConfigError as exc:
+        if h.rank == 0:
+            print(f"{sm} sync unavailable ({exc}); using the bucket all-reduce", file=sys.stderr)
+        return "bucket", "bucket", None
+
+
 def phase_medians(spans, order):
     """Per-job median compute (fwd + bwd) and sync durations in ms."""
     from paper_2103_07974_b200.engine import Phase
@@ -463,18 +490,10 @@ def run_ours(args):
 
     sm = args.sync_mode
     prio = -1 if args.comm_priority == "high" else 0
-    if world > 1 and sm in ("p2p", "ce", "auto"):
-        # probe once (collective): if any rank cannot map its peers, everyone falls back to bucket
-        from paper_2103_07974_b200.errors import ConfigError
-        try:
-            probe = timed_run(h, base, Policy.CROSSOVER, 0, 1, sync_mode=sm, comm_priority=prio)
-            del probe
-        except ConfigError as exc:
-            if rank == 0:
-                print(f"{sm} sync unavailable ({exc}); using the bucket all-reduce", file=sys.stderr)
-            sm = args.sync_mode = "bucket"
+    sm, sm_seq, tuner = calibrate_transport(h, base, sm, prio)
+    args.sync_mode = sm
     cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio)
-    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio)
+    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq, comm_priority=prio)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
                                              time_kernels=False, sync_mode=sm, comm_priority=prio)
 
@@ -535,6 +554,7 @@ def run_ours(args):
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
                                      {"crossover": sync0.mode, "sequential": sync_seq.mode})},
+            "transport_tuner": tuner,
             "speedup_vs_sequential": round(rot_seq / rot_cross, 4),
             "sequential": {"value": round(seq_value, 2), "ms_per_step": round(rot_seq, 3)},
             "rho": round(sum(comm_t) / sum(comp), 5) if sum(comp) else None,

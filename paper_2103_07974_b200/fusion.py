@@ -129,18 +129,18 @@ class FusedGradientSync:
                 mode = "direct"
             else:
                 mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
-        if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "unfused"):
+        if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "adaptive", "unfused"):
             raise ConfigError(f"unknown sync mode {mode!r}")
         if mode == "direct" and self.workers != 1:
             raise ConfigError("direct mode has no bucket and needs exactly one worker")
         if mode == "unfused" and self.local_workers != 1:
             raise ConfigError("unfused mode all-reduces each gradient tensor in place: one worker per rank")
-        if mode in ("sharded", "p2p", "ce") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
+        if mode in ("sharded", "p2p", "ce", "adaptive") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
             raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
                               "and one worker per rank")
         self.mode = mode
         self.flat = flat_params
-        sharded = mode in ("sharded", "p2p", "ce")
+        sharded = mode in ("sharded", "p2p", "ce", "adaptive")
         multiple = align * self.ranks if sharded else None
         self.layout = BucketLayout.build([p.numel() for p in self.params], align, multiple=multiple)
         if sharded:
@@ -156,7 +156,8 @@ class FusedGradientSync:
 
         self.bucket = None
         self._peer_maps = []
-        if mode in ("p2p", "ce"):
+        self.transport = None
+        if mode in ("p2p", "ce", "adaptive"):
             from .p2p import DeviceBuffer, buffer_of
 
             if self.ranks > _lib.CS_MAX_SOURCES:
@@ -191,51 +192,21 @@ class FusedGradientSync:
                 sl["dst"] = base + w * row_bytes + offs_bytes
                 sl["numel"] = numels
         # K2 descriptors: fixed except grad_offset in direct mode
-        if mode == "p2p":
+        if mode in ("p2p", "ce", "adaptive"):
             from .p2p import buffer_of, exchange_peer_addresses
 
             off = self.rank * self.shard * 4
             bmap = exchange_peer_addresses(self._bucket_buf, self.rank, self.ranks)
             fmap = exchange_peer_addresses(buffer_of(flat_params), self.rank, self.ranks)
             self._peer_maps = [bmap, fmap]
-            self._p2p = _lib.P2PDesc()
-            for r in range(self.ranks):
-                self._p2p.src[r] = bmap.addresses[r] + off
-                self._p2p.dst[r] = fmap.addresses[r] + off
-            self._p2p.param = flat_params.data_ptr() + off
-            self._p2p.momentum_buf = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else None
-            self._p2p.numel = self.shard
-            self._p2p.nranks = self.ranks
-            self._p2p.max_ctas = int(p2p_ctas)
             self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
-            self._finish_init(settings)
-            return
-        if mode == "ce":
-            # copy-engine transport: pull every peer's copy of my bucket shard (reduce-scatter
-            # half), K2 over the W shard copies in rank order, pull every peer's updated
-            # parameter shard (all-gather half).  No SM moves a byte across NVLink.
-            from .p2p import buffer_of, exchange_peer_addresses
-
-            off = self.rank * self.shard * 4
-            bmap = exchange_peer_addresses(self._bucket_buf, self.rank, self.ranks)
-            fmap = exchange_peer_addresses(buffer_of(flat_params), self.rank, self.ranks)
-            self._peer_maps = [bmap, fmap]
-            self._recv = torch.empty(lay.total, dtype=torch.float32, device=dev)
-            sb = self.shard * 4
-            self._ce_rs = [(self._recv.data_ptr() + s * sb, bmap.addresses[s] + off)
-                           for s in range(self.ranks) if s != self.rank]
-            f = flat_params.data_ptr()
-            self._ce_ag = [(f + s * sb, fmap.addresses[s] + s * sb)
-                           for s in range(self.ranks) if s != self.rank]
-            self._upd = np.zeros(1, dtype=_lib.UPDATE_DESC)
-            self._upd["param"] = f + off
-            if self.momentum_bufs is not None:
-                self._upd["momentum_buf"] = self.momentum_bufs[0].data_ptr()
-            self._upd["numel"] = self.shard
-            self._sources = np.asarray([self.bucket.data_ptr() + off if s == self.rank
-                                        else self._recv.data_ptr() + s * sb
-                                        for s in range(self.ranks)], dtype=np.uint64)
-            self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
+            if mode in ("p2p", "adaptive"):
+                self._init_p2p(bmap, fmap, off, p2p_ctas)
+            if mode in ("ce", "adaptive"):
+                self._init_ce(bmap, fmap, off)
+            # adaptive: both transports are built over the same bucket, flat parameters and
+            # momentum shard (bitwise-identical arithmetic); the scheduler picks one per sync
+            self.transport = "p2p" if mode == "p2p" else "ce"
             self._finish_init(settings)
             return
         if mode == "sharded":
@@ -267,6 +238,45 @@ class FusedGradientSync:
             self._sources = np.zeros(1, dtype=np.uint64)
         self._finish_init(settings)
 
+    def set_transport(self, transport: str) -> None:
+        """Pick the NVLink transport of the next syncs (adaptive mode switches freely: both
+        transports sum the W shards in rank order with the same update rule)."""
+        allowed = {"p2p": ("p2p",), "ce": ("ce",), "adaptive": ("p2p", "ce")}.get(self.mode, ())
+        if transport not in allowed:
+            raise ConfigError(f"transport {transport!r} is not available in {self.mode!r} mode")
+        self.transport = transport
+
+    def _init_p2p(self, bmap, fmap, off: int, p2p_ctas: int) -> None:
+        self._p2p = _lib.P2PDesc()
+        for r in range(self.ranks):
+            self._p2p.src[r] = bmap.addresses[r] + off
+            self._p2p.dst[r] = fmap.addresses[r] + off
+        self._p2p.param = self.flat.data_ptr() + off
+        self._p2p.momentum_buf = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else None
+        self._p2p.numel = self.shard
+        self._p2p.nranks = self.ranks
+        self._p2p.max_ctas = int(p2p_ctas)
+
+    def _init_ce(self, bmap, fmap, off: int) -> None:
+        """Copy-engine transport: pull every peer's copy of my bucket shard (reduce-scatter half),
+        K2 over the W shard copies in rank order, pull every peer's updated parameter shard
+        (all-gather half).  No SM moves a byte across NVLink."""
+        sb = self.shard * 4
+        self._recv = torch.empty(self.layout.total, dtype=torch.float32, device=self.flat.device)
+        self._ce_rs = [(self._recv.data_ptr() + s * sb, bmap.addresses[s] + off)
+                       for s in range(self.ranks) if s != self.rank]
+        f = self.flat.data_ptr()
+        self._ce_ag = [(f + s * sb, fmap.addresses[s] + s * sb)
+                       for s in range(self.ranks) if s != self.rank]
+        self._upd = np.zeros(1, dtype=_lib.UPDATE_DESC)
+        self._upd["param"] = f + off
+        if self.momentum_bufs is not None:
+            self._upd["momentum_buf"] = self.momentum_bufs[0].data_ptr()
+        self._upd["numel"] = self.shard
+        self._sources = np.asarray([self.bucket.data_ptr() + off if s == self.rank
+                                    else self._recv.data_ptr() + s * sb
+                                    for s in range(self.ranks)], dtype=np.uint64)
+
     def _finish_init(self, settings: SgdSettings) -> None:
         self._hyper = _lib.SgdHyper(
             lr=settings.lr, momentum=settings.momentum,
@@ -279,7 +289,7 @@ class FusedGradientSync:
     # -- per-iteration pieces (all asynchronous on `stream`) -----------------
     def pack(self, grads_per_worker: Sequence[Sequence[torch.Tensor]], stream: int) -> None:
         """K1: gather each worker's gradients into its bucket row."""
-        if self.mode not in ("bucket", "sharded", "p2p", "ce"):
+        if self.mode not in ("bucket", "sharded", "p2p", "ce", "adaptive"):
             raise ConfigError("pack() needs bucket mode")
         n = len(self.params)
         if len(grads_per_worker) != self.local_workers:
@@ -302,7 +312,7 @@ class FusedGradientSync:
                 raise ValueError("direct mode needs the gradient tensors")
             self._upd["grad_offset"] = _grad_ptrs(grads, self.params)
         snap = 0
-        if snapshot_row is not None and self.mode not in ("sharded", "ce"):
+        if snapshot_row is not None and self.mode not in ("sharded", "ce", "adaptive"):
             if self.snapshot is None:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
             snap = self.snapshot[snapshot_row].data_ptr()
@@ -347,10 +357,10 @@ class FusedGradientSync:
         if self.mode == "sharded":
             self._sharded_tail(stream, snapshot_row, timer)
             return
-        if self.mode == "p2p":
+        if self.transport == "p2p":
             self._p2p_tail(stream, snapshot_row, timer)
             return
-        if self.mode == "ce":
+        if self.transport == "ce":
             self._ce_tail(stream, snapshot_row, timer)
             return
         if self.comm is not None and self.comm.active:
@@ -454,13 +464,14 @@ class FusedGradientSync:
     def k1_bytes(self) -> int:
         return 2 * self.local_workers * self.layout.payload_bytes
 
-    def k2_bytes(self) -> int:
-        if self.mode == "p2p":
+    def k2_bytes(self, transport: str | None = None) -> int:
+        transport = transport or self.transport
+        if transport == "p2p":
             # W source shards + p read + W destination shards (+ momentum read/write)
             return (2 * self.ranks + 1 + (2 if self.settings.momentum else 0)) * self.shard * 4
         if self.mode == "sharded":
             return (5 if self.settings.momentum else 3) * self.shard * 4
-        if self.mode == "ce":
+        if transport == "ce":
             # W source shards + p read/write (+ momentum read/write)
             return (self.ranks + 2 + (2 if self.settings.momentum else 0)) * self.shard * 4
         s = self.layout.payload_bytes

@@ -236,6 +236,8 @@ class CrossoverScheduler:
         self.cursor = 0
         self._last_update = None
         self._started = False
+        self._slot = 0
+        self.tuner: _TransportTuner | None = None
 
     # -- registration (≙ building a SchedulePlan of JobProfiles) -------------
     def register(self, app: App) -> JobRuntimeState:
@@ -263,16 +265,19 @@ class CrossoverScheduler:
 
         With peer-mappable flat parameters at W > 1: under crossover the sync overlaps another
         app's compute, so it goes through the copy engines ("ce": NVLink pulls that hold no SM,
-        ~1-6 % GEMM slowdown vs 15-100 % for SM-driven collectives, tools/cebench.py); the
-        sequential baseline has the GPU to itself and takes the fastest isolated path, the fused
-        P2P kernel on the full grid.  Both sum in rank order, so weights are bitwise identical."""
+        ~1-6 % GEMM slowdown vs 15-100 % for SM-driven collectives, tools/cebench.py) unless it
+        no longer fits under the other apps' compute -- the copy engines move fewer bytes per
+        second than the P2P kernel -- so the crossover run is "adaptive" (:class:`_TransportTuner`
+        measures both and keeps the faster); the sequential baseline has the GPU to itself and
+        takes the fastest isolated path, the fused P2P kernel on the full grid.  Every transport
+        sums in rank order, so the weights are bitwise identical whichever runs."""
         if self.sync_mode != "auto" or self.comm is None or self.comm.world < 2:
             return self.sync_mode
         from .p2p import buffer_of
 
         if app.flat_params is None or buffer_of(app.flat_params) is None or app.local_workers != 1:
             return self.sync_mode
-        return "ce" if self.policy is Policy.CROSSOVER else "p2p"
+        return "adaptive" if self.policy is Policy.CROSSOVER else "p2p"
 
     @property
     def job_order(self) -> list[str]:
@@ -317,12 +322,23 @@ class CrossoverScheduler:
         if not self._started:
             self._started = True
             self.recorder.start(self.compute_stream)
+            adaptive = [s.sync.mode == "adaptive" for s in self.states]
+            if all(adaptive):
+                self.tuner = _TransportTuner([s.app.iterations for s in self.states], self.comm,
+                                             self.device)
+            elif any(adaptive):
+                raise ConfigError("adaptive transport must be used by every app or none")
         st = self._next_with_work()
         if st is None:
             return False
         app, t = st.app, st.next_iteration
         cs, ms = self.compute_stream, self.comm_stream
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        slot = self._slot
+        self._slot += 1
+        if self.tuner is not None:
+            self.tuner.before_slot(slot, ms)
+            st.sync.set_transport(self.tuner.transport_for(slot))
 
         with torch.cuda.stream(cs):
             # Alg. 1 readiness (scheduler.py:158): compute (j, t) after sync (j, t-1).
@@ -339,6 +355,8 @@ class CrossoverScheduler:
             batches = [self._to_device(app.data(t, w)) for w in workers]
             e_f0 = ev()
             e_f0.record(cs)
+            if self.tuner is not None:
+                self.tuner.mark(slot, e_f0)
             amp = (torch.autocast("cuda", dtype=app.autocast_dtype, cache_enabled=app.autocast_cache)
                    if app.autocast_dtype else contextlib.nullcontext())
             losses = []
@@ -445,6 +463,73 @@ class CrossoverScheduler:
     @property
     def kernel_launches(self) -> int:
         return sum(s.sync.kernel_launches for s in self.states)
+
+
+class _TransportTuner:
+    """Measured choice between the copy-engine and the fused-P2P-kernel transport (adaptive).
+
+    With n apps, slots [0, 3n) sync over the copy engines and slots [3n, 6n) with the P2P kernel
+    (32 CTAs).  Each transport's rotation period is measured on the device over its last two
+    rotations (compute starts of slots n -> 3n and 4n -> 6n), so every measured compute waits on
+    syncs of its own transport.  At slot 7n every rank sums its two periods over the ranks (NCCL
+    all-reduce on the comm stream, at the same position of the collective sequence on every rank)
+    and at slot 8n every rank reads the sums and keeps the faster transport for the rest of the
+    run -- the same decision everywhere, without a host barrier.  Plans too short to afford the
+    calibration (any budget < 10) stay on the copy engines.
+    """
+
+    MIN_BUDGET = 10
+
+    def __init__(self, budgets: list[int], comm, device):
+        self.n = len(budgets)
+        self.active = min(budgets) >= self.MIN_BUDGET and comm is not None and comm.world > 1
+        self.comm = comm
+        self.device = device
+        self.choice = "ce"
+        self.marks: dict[int, torch.cuda.Event] = {}
+        self.periods_ms: dict[str, float] | None = None
+        self._host = torch.zeros(2, dtype=torch.float32).pin_memory() if self.active else None
+        self._dev = torch.zeros(32, dtype=torch.float32, device=device) if self.active else None
+        self._done: torch.cuda.Event | None = None
+
+    def transport_for(self, slot: int) -> str:
+        if not self.active:
+            return "ce"
+        n = self.n
+        if slot < 3 * n:
+            return "ce"
+        if slot < 6 * n:
+            return "p2p"
+        return self.choice
+
+    def mark(self, slot: int, event) -> None:
+        if self.active and slot in (self.n, 3 * self.n, 4 * self.n, 6 * self.n):
+            self.marks[slot] = event
+
+    def before_slot(self, slot: int, comm_stream) -> None:
+        if not self.active:
+            return
+        n = self.n
+        if slot == 7 * n:
+            self.marks[6 * n].synchronize()          # one rotation old: already reached
+            ce = self.marks[n].elapsed_time(self.marks[3 * n]) / 2
+            p2p = self.marks[4 * n].elapsed_time(self.marks[6 * n]) / 2
+            self._host.copy_(torch.tensor([ce, p2p]))
+            with torch.cuda.stream(comm_stream):
+                self._dev[:2].copy_(self._host, non_blocking=True)
+                self.comm.all_reduce_(self._dev.data_ptr(), 2, comm_stream.cuda_stream)
+                self._host.copy_(self._dev[:2], non_blocking=True)
+            self._done = torch.cuda.Event()
+            self._done.record(comm_stream)
+        elif slot == 8 * n:
+            self._done.synchronize()
+            ce, p2p = (float(x) / self.comm.world for x in self._host)
+            self.periods_ms = {"ce": ce, "p2p": p2p}
+            self.choice = "ce" if ce <= p2p else "p2p"
+
+    def summary(self) -> dict:
+        return {"active": self.active, "choice": self.choice,
+                "calibration_period_ms": self.periods_ms}
 
 
 def _nudge_first_coordinate(param: torch.Tensor, sync: FusedGradientSync, row: int | None) -> None:

@@ -134,6 +134,26 @@ def main():
     res["checks"].append({"name": f"ce_bitwise_eq_p2p_w{world}",
                           "ok": all(torch.equal(ce_w[k], p2p_w[k]) for k in range(2))})
 
+    # (4c) auto under crossover with IPC flat parameters = adaptive transport: copy engines for
+    #      two rotations, the P2P kernel for two, then the measured faster one; the choice is the
+    #      same on every rank and the weights stay bitwise equal to either transport
+    s9 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True)
+    for k, (ds, rs) in enumerate(specs):
+        s9.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs,
+                            max(T, 12), dev, local_workers=1, worker_count=world, flat="ipc"))
+    s9.run()
+    ad_w = [s9.weights(f"m{k}").cpu() for k in range(2)]
+    summ = s9.tuner.summary() if s9.tuner is not None else None
+    s9.close()
+    choices = [None] * world
+    dist.all_gather_object(choices, summ["choice"] if summ else None)
+    res["checks"].append({"name": "adaptive_tuner_decided", "ok": bool(summ and summ["active"]
+                          and summ["calibration_period_ms"] is not None), "summary": summ})
+    res["checks"].append({"name": "adaptive_choice_same_on_every_rank",
+                          "ok": len(set(choices)) == 1 and choices[0] in ("ce", "p2p")})
+    res["checks"].append({"name": f"adaptive_bitwise_eq_p2p_w{world}",
+                          "ok": all(torch.equal(ad_w[k][:T], p2p_w[k]) for k in range(2))})
+
     # every rank must hold identical weights after every iteration
     for k in range(2):
         gathered = [torch.empty_like(w_ranks[k]) for _ in range(world)] if rank == 0 else None

@@ -14,7 +14,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-from bench import Harness, kernel_summary, phase_medians, timed_run  # noqa: E402
+from bench import Harness, calibrate_transport, kernel_summary, phase_medians, timed_run  # noqa: E402
 
 
 def main():
@@ -37,16 +37,20 @@ def main():
         bench.P2P_CTAS = args.p2p_ctas
     rows = []
     for mb in [int(x) for x in args.sizes_mb.split(",")]:
-        flat = {"sharded": True, "p2p": "ipc", "ce": "ipc"}.get(args.sync_mode, False) if h.world > 1 else False
+        flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc"}.get(args.sync_mode, False)
+                if h.world > 1 else False)
         base = [synthetic_app(f"syn{j}", mb * 2**20, 1, h.dev, gemm_reps=args.gemm_reps, seed=j,
                               flat=flat) for j in range(2)]
-        cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=args.sync_mode)
-        seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=args.sync_mode)
+        sm, sm_seq, tuner = calibrate_transport(h, base, args.sync_mode)
+        cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=sm)
+        seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=sm_seq)
         comp, comm = phase_medians(seq["timed_spans"], [a.job_id for a in base])
         rho = sum(comm) / sum(comp)
         roof = overlap_roofline(comp, comm)
         rot_x, rot_s = cross["ms"] / args.steps, seq["ms"] / args.steps
         row = {"bucket_MB": mb, "world": h.world, "sync_mode": cross["sched"].states[0].sync.mode,
+               "sync_mode_sequential": seq["sched"].states[0].sync.mode,
+               "transport_tuner": tuner,
                "p2p_ctas": args.p2p_ctas, "nccl_max_ctas": args.nccl_max_ctas,
                "rho": round(rho, 4),
                "speedup": round(rot_s / rot_x, 4),
