@@ -468,17 +468,19 @@ class CrossoverScheduler:
 class _TransportTuner:
     """Measured choice between the copy-engine and the fused-P2P-kernel transport (adaptive).
 
-    With n apps, slots [0, 3n) sync over the copy engines and slots [3n, 6n) with the P2P kernel
-    (32 CTAs).  Each transport's rotation period is measured on the device over its last two
-    rotations (compute starts of slots n -> 3n and 4n -> 6n), so every measured compute waits on
-    syncs of its own transport.  At slot 7n every rank sums its two periods over the ranks (NCCL
-    all-reduce on the comm stream, at the same position of the collective sequence on every rank)
-    and at slot 8n every rank reads the sums and keeps the faster transport for the rest of the
-    run -- the same decision everywhere, without a host barrier.  Plans too short to afford the
-    calibration (any budget < 10) stay on the copy engines.
+    With n apps, slots [0, 4n) sync over the copy engines and slots [4n, 8n) with the P2P kernel
+    (32 CTAs).  Each transport's rotation period is the median of its last three rotations,
+    measured on the device between compute starts (slots n, 2n, 3n, 4n and 5n, 6n, 7n, 8n), so
+    every measured compute waits on syncs of its own transport and a one-off spike (first launch,
+    allocator growth) does not decide.  At slot 9n every rank sums its two medians over the ranks
+    (NCCL all-reduce on the comm stream, at the same position of the collective sequence on every
+    rank) and at slot 10n every rank reads the sums and keeps the faster transport for the rest of
+    the run -- the same decision everywhere, without a host barrier.  Plans too short to afford
+    the calibration (any budget < 12) stay on the copy engines.  The windows must not contain a
+    host-side drain (bench.py calibrates in a separate untimed run for that reason).
     """
 
-    MIN_BUDGET = 10
+    MIN_BUDGET = 12
 
     def __init__(self, budgets: list[int], comm, device):
         self.n = len(budgets)
@@ -495,25 +497,29 @@ class _TransportTuner:
     def transport_for(self, slot: int) -> str:
         if not self.active:
             return "ce"
-        n = self.n
-        if slot < 3 * n:
+        if slot < 4 * self.n:
             return "ce"
-        if slot < 6 * n:
+        if slot < 8 * self.n:
             return "p2p"
         return self.choice
 
     def mark(self, slot: int, event) -> None:
-        if self.active and slot in (self.n, 3 * self.n, 4 * self.n, 6 * self.n):
+        if self.active and slot % self.n == 0 and 1 <= slot // self.n <= 8:
             self.marks[slot] = event
+
+    def _median_period(self, first: int) -> float:
+        n = self.n
+        p = sorted(self.marks[k * n].elapsed_time(self.marks[(k + 1) * n])
+                   for k in range(first, first + 3))
+        return p[1]
 
     def before_slot(self, slot: int, comm_stream) -> None:
         if not self.active:
             return
         n = self.n
-        if slot == 7 * n:
-            self.marks[6 * n].synchronize()          # one rotation old: already reached
-            ce = self.marks[n].elapsed_time(self.marks[3 * n]) / 2
-            p2p = self.marks[4 * n].elapsed_time(self.marks[6 * n]) / 2
+        if slot == 9 * n:
+            self.marks[8 * n].synchronize()          # one rotation old: already reached
+            ce, p2p = self._median_period(1), self._median_period(5)
             self._host.copy_(torch.tensor([ce, p2p]))
             with torch.cuda.stream(comm_stream):
                 self._dev[:2].copy_(self._host, non_blocking=True)
@@ -521,7 +527,7 @@ class _TransportTuner:
                 self._host.copy_(self._dev[:2], non_blocking=True)
             self._done = torch.cuda.Event()
             self._done.record(comm_stream)
-        elif slot == 8 * n:
+        elif slot == 10 * n:
             self._done.synchronize()
             ce, p2p = (float(x) / self.comm.world for x in self._host)
             self.periods_ms = {"ce": ce, "p2p": p2p}

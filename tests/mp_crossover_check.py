@@ -140,7 +140,7 @@ def main():
     s9 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True)
     for k, (ds, rs) in enumerate(specs):
         s9.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs,
-                            max(T, 12), dev, local_workers=1, worker_count=world, flat="ipc"))
+                            max(T, 14), dev, local_workers=1, worker_count=world, flat="ipc"))
     s9.run()
     ad_w = [s9.weights(f"m{k}").cpu() for k in range(2)]
     summ = s9.tuner.summary() if s9.tuner is not None else None
