@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--metrics-out", default="", help="colosim.metrics/v1 JSON + CSV of the measured runs")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
+    ap.add_argument("--bn-no-pdl", action="store_true",
+                    help="launch the BN finalize / apply kernels without programmatic dependent launch")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
                          "the fused NVLink P2P kernel; ce = copy-engine pulls + shard K2; auto = ce "
@@ -450,6 +452,8 @@ def run_ours(args):
         P2P_CTAS = args.p2p_ctas
     if args.sync_ctas:
         _lib.tune("sync_ctas", args.sync_ctas)
+    if args.bn_no_pdl:
+        _lib.tune("bn_no_pdl", 1)
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
     # auto at W > 1: IPC flat parameters, and the scheduler picks the transport per policy

@@ -103,7 +103,8 @@ CS_API int cs_get_kernel_variant(void);
  * "ctas_per_sm"; of the register variant: "reg_shape" (0..4: unroll x CTAs/SM); of the
  * fused P2P kernel: "p2p_ctas" (persistent grid cap, 0 = default 2 CTAs per SM); of
  * the register K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
- * sync that overlaps another app's compute with slack can trade speed for fewer SMs.
+ * sync that overlaps another app's compute with slack can trade speed for fewer SMs; of the BN
+ * kernels: "bn_no_pdl" (1 = launch finalize / apply without programmatic dependent launch).
  * Results never depend on them. */
 CS_API int cs_tune(const char* key, int value);
 

@@ -118,6 +118,7 @@ int cs_tune(const char* key, int value) {
   else if (k == "reg_shape" && value <= 4) g_tune_reg_shape = value;
   else if (k == "p2p_ctas" && value <= 65536) g_tune_p2p_ctas = value;
   else if (k == "sync_ctas" && value <= 65536) g_tune_sync_ctas = value;
+  else if (k == "bn_no_pdl" && value <= 1) g_tune_bn_no_pdl = value;
   else return set_error(CS_ERR_ARG, "cs_tune: unknown key or bad value (%s=%d)", key, value);
   return 0;
 }

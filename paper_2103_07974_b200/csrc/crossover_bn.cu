@@ -27,9 +27,18 @@
 
 namespace cs {
 
+int g_tune_bn_no_pdl = 0;   // 0: finalize / apply use programmatic dependent launch
+
 namespace {
 
 constexpr int kBnThreads = 256;
+
+// Programmatic dependent launch (PDL) inside a BN op: finalize and apply are launched with
+// programmatic stream serialization, so their CTAs are scheduled while the previous kernel of
+// the chain drains; griddepcontrol.wait then blocks until that kernel has completed and its
+// writes are visible (the ordering is unchanged, only the launch latency is hidden).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 constexpr int kBnMaxTile = 256;   // channels per CTA tile in the partial kernels
 constexpr int kRowUnroll = 4;     // rows in flight per thread
 
@@ -129,6 +138,7 @@ bn_fwd_partial_kernel(const __nv_bfloat16* __restrict__ x, int64_t M, int C,
     for (int u = 0; u < U; ++u) shifted8(raw[u], k, s1, s2);
   }
   for (; r < r1; r += s.ty) shifted8(ld_nc16(x + r * C + c0), k, s1, s2);
+  pdl_trigger();
   const int64_t my_rows = r1 > r0 + ty ? (r1 - (r0 + ty) + s.ty - 1) / s.ty : 0;
   float n = (float)my_rows;
 #pragma unroll
@@ -179,6 +189,8 @@ bn_fwd_finalize_kernel(const float* __restrict__ partial, int blocks, int C,
                        float momentum, float eps, float* __restrict__ save_mean,
                        float* __restrict__ save_invstd, float* __restrict__ scale,
                        float* __restrict__ shift) {
+  pdl_trigger();
+  pdl_wait();
   const int ch = blockIdx.x * (kBnThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (ch >= C) return;
@@ -239,6 +251,7 @@ bn_fwd_apply_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
   const int64_t stride = (int64_t)gridDim.x * kBnThreads;   // multiple of cv (host guarantees)
   const int64_t v0 = (int64_t)blockIdx.x * kBnThreads + threadIdx.x;
   const int c = (int)(v0 % cv) * 8;
+  pdl_wait();
   float sc[8], sh[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) { sc[i] = scale[c + i]; sh[i] = shift[c + i]; }
@@ -292,6 +305,7 @@ bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* _
   const int64_t stride = (int64_t)gridDim.x * kBnThreads;
   const int64_t v0 = (int64_t)blockIdx.x * kBnThreads + threadIdx.x;
   const int c = (int)(v0 % cv) * 8;
+  pdl_wait();
   float q1[8], q2[8], q3[8], sc[8], sh[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -369,6 +383,7 @@ bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16*
   for (; r < r1; r += s.ty)
     bwd_acc8<kRelu, kRes>(ld_nc16(dy + r * C + c0), ld_nc16(x + r * C + c0),
                           kLoadRes ? ld_nc16(res + r * C + c0) : zero, mu, sc, sh, sdy, sdx);
+  pdl_trigger();
 
   __shared__ float s_dy[kBnThreads * 8], s_dx[kBnThreads * 8];
 #pragma unroll
@@ -398,6 +413,8 @@ bn_bwd_finalize_kernel(const float* __restrict__ partial, int blocks, int64_t M,
                        const float* __restrict__ weight, float* __restrict__ grad_weight,
                        float* __restrict__ grad_bias, float* __restrict__ k1,
                        float* __restrict__ k2, float* __restrict__ k3) {
+  pdl_trigger();
+  pdl_wait();
   const int ch = blockIdx.x * (kBnThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (ch >= C) return;
@@ -456,6 +473,23 @@ size_t bn_workspace_bytes(int64_t M, int C) {
   return 256 + (size_t)bn_row_blocks(M, C) * (size_t)C * 3 * sizeof(float);
 }
 
+// launch with programmatic stream serialization (cs_tune("bn_no_pdl", 1) turns it off)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_dependent(void (*kernel)(KArgs...), dim3 grid, cudaStream_t s,
+                                    Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kBnThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_tune_bn_no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 static unsigned apply_grid(int64_t M, int C) {
   const int64_t vecs = M * (C / 8);
   const int cv = C / 8;
@@ -473,8 +507,9 @@ static unsigned apply_grid(int64_t M, int C) {
 template <bool kRelu, bool kRes>
 static void fwd_apply(const void* x, const void* res, int64_t M, int C, const float* scale,
                       const float* shift, void* y, cudaStream_t s) {
-  bn_fwd_apply_kernel<kRelu, kRes><<<apply_grid(M, C), kBnThreads, 0, s>>>(
-      (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C, scale, shift, (__nv_bfloat16*)y);
+  launch_dependent(bn_fwd_apply_kernel<kRelu, kRes>, dim3(apply_grid(M, C)), s,
+                   (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C, scale, shift,
+                   (__nv_bfloat16*)y);
 }
 
 cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, const float* w,
@@ -490,10 +525,8 @@ cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, cons
   if (e != cudaSuccess) return e;
   float* scale = scale_shift;
   float* shift = scale_shift + C;
-  bn_fwd_finalize_kernel<<<(C + 7) / 8, kBnThreads, 0, s>>>(partial, blocks, C, w, b, rm, rv,
-                                                             momentum, eps, save_mean, save_invstd,
-                                                             scale, shift);
-  e = cudaGetLastError();
+  e = launch_dependent(bn_fwd_finalize_kernel, dim3((C + 7) / 8), s, (const float*)partial, blocks,
+                       C, w, b, rm, rv, momentum, eps, save_mean, save_invstd, scale, shift);
   if (e != cudaSuccess) return e;
   const bool relu = flags & CS_BN_RELU, resid = flags & CS_BN_RESIDUAL;
   if (relu && resid) fwd_apply<true, true>(x, res, M, C, scale, shift, y, s);
@@ -518,15 +551,13 @@ static cudaError_t bwd_impl(const void* dy, const void* x, const void* res, int6
       save_mean, scale, shift, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  bn_bwd_finalize_kernel<<<(C + 7) / 8, kBnThreads, 0, s>>>(partial, blocks, M, C, save_mean,
-                                                             save_invstd, w, gw, gb, coef,
-                                                             coef + C, coef + 2 * C);
-  e = cudaGetLastError();
+  e = launch_dependent(bn_bwd_finalize_kernel, dim3((C + 7) / 8), s, (const float*)partial, blocks,
+                       M, C, save_mean, save_invstd, w, gw, gb, coef, coef + C, coef + 2 * C);
   if (e != cudaSuccess) return e;
-  bn_bwd_apply_kernel<kRelu, kRes><<<apply_grid(M, C), kBnThreads, 0, s>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C, coef,
-      scale, shift, (__nv_bfloat16*)dx, (__nv_bfloat16*)dres);
-  return cudaGetLastError();
+  return launch_dependent(bn_bwd_apply_kernel<kRelu, kRes>, dim3(apply_grid(M, C)), s,
+                          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                          (const __nv_bfloat16*)res, M, C, (const float*)coef, scale, shift,
+                          (__nv_bfloat16*)dx, (__nv_bfloat16*)dres);
 }
 
 cudaError_t launch_bn_bwd(const void* dy, const void* x, const void* res, int64_t M, int C,

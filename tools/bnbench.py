@@ -26,7 +26,11 @@ def timeit(fn, iters=10):
 
 
 def main():
+    from paper_2103_07974_b200 import _lib
     from paper_2103_07974_b200.bn import CrossoverBatchNorm2d
+
+    if "--no-pdl" in sys.argv:
+        _lib.tune("bn_no_pdl", 1)
 
     dev = torch.device("cuda", 0)
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
@@ -60,8 +64,9 @@ def main():
         out["speedup"] = round(out["aten_ms"] / out["ours_ms"], 2)
         rows.append(out)
         print(json.dumps(out), flush=True)
-    if len(sys.argv) > 1:
-        Path(sys.argv[1]).write_text(json.dumps(rows, indent=1))
+    outs = [a for a in sys.argv[1:] if not a.startswith("--")]
+    if outs:
+        Path(outs[0]).write_text(json.dumps(rows, indent=1))
 
 
 if __name__ == "__main__":
