@@ -105,7 +105,10 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
         out = {"kernel": "k2_p2p_fused (NVLink reads of every rank's bucket shard, rank-order sum, "
                          "/W, SGD-momentum, NVLink writes of the new shard to every rank)",
                "bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
-               "frac": round(ach / NVLINK_P2P_GBS, 4), "traffic": None,
+               "frac": round(ach / NVLINK_P2P_GBS, 4),
+               "traffic": ncu_traffic(f"k2_p2p_fused/{model}/emulated_w{sync.ranks}/momentum"),
+               "traffic_note": "DRAM bytes of the same kernel with the W ranks' buffers local "
+                               "(ncu cannot replay a multi-rank run)",
                "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                "bytes_per_launch": per_dir,
                "grid_cap_ctas": int(sync._p2p.max_ctas) or "2 per SM"}
@@ -128,8 +131,9 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
         out = {"kernel": "k2_update (W-source shard reduce, /W, SGD-momentum) beside copy-engine "
                          "reduce-scatter / all-gather pulls", "bound": "hbm",
                 "achieved": k2["GB/s"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(k2["GB/s"] / hbm_peak, 4), "traffic": None,
-                "peak_kind": peak_kind, "bytes_per_launch": sync.k2_bytes(),
+                "frac": round(k2["GB/s"] / hbm_peak, 4),
+                "traffic": ncu_traffic(f"k2_update/{model}/ce_w{sync.ranks}/momentum"),
+                "peak_kind": peak_kind, "bytes_per_launch": sync.k2_bytes("ce"),
                 "transport": {"engine": "copy engines (cudaMemcpyAsync peer pulls, no SM)",
                               "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
                               "frac": round(ach / NVLINK_P2P_GBS, 4),
@@ -410,8 +414,8 @@ def kernel_summary(kern: dict, sync) -> dict:
     out = {}
     if "k2_update" in kern:
         t = statistics.mean(kern["k2_update"])
-        out["k2_update"] = {"ms": round(t, 4), "bytes": sync.k2_bytes(),
-                            "GB/s": round(sync.k2_bytes() / (t / 1e3) / 1e9, 1)}
+        kb = sync.k2_bytes("ce" if sync.mode in ("ce", "adaptive") else None)
+        out["k2_update"] = {"ms": round(t, 4), "bytes": kb, "GB/s": round(kb / (t / 1e3) / 1e9, 1)}
     if "k1_pack" in kern:
         t = statistics.mean(kern["k1_pack"])
         out["k1_pack"] = {"ms": round(t, 4), "bytes": sync.k1_bytes(),
@@ -428,8 +432,8 @@ def kernel_summary(kern: dict, sync) -> dict:
     if "k2_p2p_fused" in kern:
         t = statistics.mean(kern["k2_p2p_fused"])
         nv = sync.c1_bus_bytes()
-        out["k2_p2p_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes(),
-                               "GB/s": round(sync.k2_bytes() / (t / 1e3) / 1e9, 1),
+        out["k2_p2p_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes("p2p"),
+                               "GB/s": round(sync.k2_bytes("p2p") / (t / 1e3) / 1e9, 1),
                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
     if "c1_allreduce" in kern:
         t = statistics.mean(kern["c1_allreduce"])
