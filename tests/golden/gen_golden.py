@@ -10,6 +10,8 @@ Outputs (committed, small):
   equivalence.npz    reference fp64 trajectories of run_crossover / run_isolated for a
                      grid of (jobs, workers, loss, T) plus one perturbed run
   fixtures.json      reference fixture bucket inventories (resnet50, vgg16 sizes)
+  metrics.json       the reference's metrics reports (json / csv / table, both policies + the
+                     crossover-vs-sequential comparison) for the first 60 schedule cases
   scenarios.json     the reference's scenario files (pkg/scenarios/*.json) with the reference
                      parser's result and simulated makespan for each, plus ~30 malformed
                      documents with the reference parser's exact error message
@@ -68,6 +70,19 @@ def main() -> None:
         c["sequential"] = {"spans": spans(seq), "makespan": seq.makespan}
     (OUT / "schedule.json").write_text(json.dumps({"generator": "colosim (reference) 0.1.0",
                                                    "cases": cases}, separators=(",", ":")) + "\n")
+
+    from colosim.metrics import compare, measure, report
+    mcases = []
+    for c in cases[:60]:
+        px, ps = plan(Policy.CROSSOVER, c["jobs"]), plan(Policy.SEQUENTIAL, c["jobs"])
+        mx = measure(schedule_crossover(px), px, scenario=c["name"])
+        ms = measure(schedule_sequential(ps), ps, scenario=c["name"])
+        cmp = compare(mx, ms)
+        mcases.append({"name": c["name"],
+                       "crossover": {f: report(mx, f) for f in ("json", "csv", "table")},
+                       "sequential": {f: report(ms, f) for f in ("json", "csv", "table")},
+                       "compare": {f: report(cmp, f) for f in ("json", "csv", "table")}})
+    (OUT / "metrics.json").write_text(json.dumps(mcases, separators=(",", ":")) + "\n")
 
     losses = (LossKind.LEAST_SQUARES, LossKind.LOGISTIC)
     arrays = {}
