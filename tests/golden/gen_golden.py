@@ -71,6 +71,7 @@ def main() -> None:
     (OUT / "schedule.json").write_text(json.dumps({"generator": "colosim (reference) 0.1.0",
                                                    "cases": cases}, separators=(",", ":")) + "\n")
 
+    from colosim.engine import trace_to_chrome_json, trace_to_json
     from colosim.metrics import compare, measure, report
     mcases = []
     for c in cases[:60]:
@@ -81,7 +82,9 @@ def main() -> None:
         mcases.append({"name": c["name"],
                        "crossover": {f: report(mx, f) for f in ("json", "csv", "table")},
                        "sequential": {f: report(ms, f) for f in ("json", "csv", "table")},
-                       "compare": {f: report(cmp, f) for f in ("json", "csv", "table")}})
+                       "compare": {f: report(cmp, f) for f in ("json", "csv", "table")},
+                       "trace_json": trace_to_json(schedule_crossover(px)),
+                       "trace_chrome": trace_to_chrome_json(schedule_crossover(px))})
     (OUT / "metrics.json").write_text(json.dumps(mcases, separators=(",", ":")) + "\n")
 
     losses = (LossKind.LEAST_SQUARES, LossKind.LOGISTIC)

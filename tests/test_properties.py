@@ -17,7 +17,8 @@ from conftest import GOLDEN
 from oracle import schedule as osched
 from paper_2103_07974_b200.comm import (Architecture, ClusterSpec, SyncRequest, comm_time,
                                         comm_time_unfused)
-from paper_2103_07974_b200.engine import Phase, Span, Trace, validate_trace
+from paper_2103_07974_b200.engine import (Phase, Span, Trace, trace_to_chrome_json, trace_to_json,
+                                          validate_trace)
 from paper_2103_07974_b200.metrics import compare, measure, report
 from paper_2103_07974_b200.scenario import scaled_int
 from paper_2103_07974_b200.scheduler import (Policy, SchedulePlan, rotation_schedule,
@@ -50,6 +51,9 @@ def test_metrics_reports_match_reference_byte_for_byte():
             assert report(mx, fmt) == g["crossover"][fmt], (g["name"], fmt)
             assert report(ms, fmt) == g["sequential"][fmt], (g["name"], fmt)
             assert report(compare(mx, ms), fmt) == g["compare"][fmt], (g["name"], fmt)
+        # span exports (engine.py:245-289): JSON and Chrome trace-event documents
+        assert trace_to_json(_trace(c["crossover"]["spans"])) == g["trace_json"], g["name"]
+        assert trace_to_chrome_json(_trace(c["crossover"]["spans"])) == g["trace_chrome"], g["name"]
 
 
 plans = st.lists(st.tuples(st.integers(0, 12), st.integers(1, 12), st.integers(0, 15),
