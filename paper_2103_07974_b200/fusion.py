@@ -100,7 +100,17 @@ class SgdSettings:
 
 
 class FusedGradientSync:
-    """Owns one app's bucket, momentum buffers and K1/K2 descriptor tables."""
+    """Owns one app's bucket, momentum buffers and K1/K2 descriptor tables.
+
+    Sync modes (one per app):
+      direct    W = 1: K2 reads the gradient tensors in place (no bucket)
+      bucket    K1 -> NCCL all-reduce of the bucket -> K2 (also W simulated workers on one GPU)
+      sharded   K1 -> reduce-scatter -> K2 on this rank's shard -> all-gather into flat params
+      p2p       K1 -> barrier -> one NVLink kernel (rank-order reduce, /W, SGD, broadcast writes)
+      ce        K1 -> barrier -> copy-engine pulls -> shard K2 -> barrier -> copy-engine pulls
+      adaptive  p2p and ce over the same buffers; the scheduler picks one per sync
+      unfused   one all-reduce per gradient tensor (the per-message counterfactual), then K2
+    """
 
     def __init__(self, params: Sequence[torch.Tensor], settings: SgdSettings,
                  comm: NcclCommunicator | None = None, local_workers: int = 1,
