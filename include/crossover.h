@@ -104,8 +104,10 @@ CS_API int cs_get_kernel_variant(void);
  * fused P2P kernel: "p2p_ctas" (persistent grid cap, 0 = default 2 CTAs per SM); of
  * the register K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
  * sync that overlaps another app's compute with slack can trade speed for fewer SMs; of the BN
- * kernels: "bn_no_pdl" (1 = launch finalize / apply without programmatic dependent launch).
- * Results never depend on them. */
+ * kernels: "bn_no_pdl" (1 = launch finalize / apply without programmatic dependent launch),
+ * "bn_ctas_per_sm" (row-block CTAs per SM of the partial kernels, 0 = 3; changes the partial
+ * merge tree, so results are deterministic per setting but not bitwise across settings).
+ * Results never depend on them (except bn_ctas_per_sm, see above). */
 CS_API int cs_tune(const char* key, int value);
 
 /* Streams and events -- the crossover pipeline's primitives for hosts without torch
