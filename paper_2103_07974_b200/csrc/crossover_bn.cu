@@ -28,6 +28,7 @@
 namespace cs {
 
 int g_tune_bn_no_pdl = 0;   // 0: finalize / apply use programmatic dependent launch
+int g_tune_bn_ctas_per_sm = 0;   // partial kernels: row-block CTAs per SM (0 = 3, the measured best)
 int g_tune_bn_ctas_per_sm = 0;
 int g_tune_bn_pipe = 0;          // 1: double-buffered row batches in bn_fwd_partial   // partial kernels: row blocks x tiles per SM (0 = 3)
 

@@ -34,6 +34,9 @@ def main():
     for a in sys.argv[1:]:
         if a.startswith("--ctas-per-sm="):
             _lib.tune("bn_ctas_per_sm", int(a.split("=")[1]))
+    for a in sys.argv[1:]:
+        if a.startswith("--ctas-per-sm="):
+            _lib.tune("bn_ctas_per_sm", int(a.split("=")[1]))
         if a == "--pipe":
             _lib.tune("bn_pipe", 1)
 
