@@ -120,8 +120,6 @@ int cs_tune(const char* key, int value) {
   else if (k == "sync_ctas" && value <= 65536) g_tune_sync_ctas = value;
   else if (k == "bn_no_pdl" && value <= 1) g_tune_bn_no_pdl = value;
   else if (k == "bn_ctas_per_sm" && value <= 8) g_tune_bn_ctas_per_sm = value;
-  else if (k == "bn_ctas_per_sm" && value <= 8) g_tune_bn_ctas_per_sm = value;
-  else if (k == "bn_pipe" && value <= 1) g_tune_bn_pipe = value;
   else return set_error(CS_ERR_ARG, "cs_tune: unknown key or bad value (%s=%d)", key, value);
   return 0;
 }

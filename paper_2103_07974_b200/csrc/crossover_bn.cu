@@ -29,8 +29,6 @@ namespace cs {
 
 int g_tune_bn_no_pdl = 0;   // 0: finalize / apply use programmatic dependent launch
 int g_tune_bn_ctas_per_sm = 0;   // partial kernels: row-block CTAs per SM (0 = 3, the measured best)
-int g_tune_bn_ctas_per_sm = 0;
-int g_tune_bn_pipe = 0;          // 1: double-buffered row batches in bn_fwd_partial   // partial kernels: row blocks x tiles per SM (0 = 3)
 
 namespace {
 
@@ -117,7 +115,6 @@ __device__ __forceinline__ void shifted8(const uint4& raw, const float* k, float
 // ---------------------------------------------------------------------------
 // forward statistics
 // ---------------------------------------------------------------------------
-template <bool kPipe>
 __global__ void __launch_bounds__(kBnThreads)
 bn_fwd_partial_kernel(const __nv_bfloat16* __restrict__ x, int64_t M, int C,
                       float* __restrict__ partial) {
@@ -134,38 +131,12 @@ bn_fwd_partial_kernel(const __nv_bfloat16* __restrict__ x, int64_t M, int C,
   for (int i = 0; i < 8; ++i) { k[i] = 0.f; s1[i] = 0.f; s2[i] = 0.f; }
   int64_t r = r0 + ty;
   if (r < r1) unpack8(ld_nc16(x + r * C + c0), k);   // the shift
-  if (kPipe) {
-    // double-buffered batches of B rows: batch i+1's loads are in flight while batch i is
-    // accumulated (same row order per thread as the plain loop -> bitwise-identical sums)
-    constexpr int B = kRowUnroll;
-    uint4 cur[B], nxt[B];
-    bool have = r + (B - 1) * s.ty < r1;
-    if (have) {
+  for (; r + (U - 1) * s.ty < r1; r += U * s.ty) {
+    uint4 raw[U];
 #pragma unroll
-      for (int u = 0; u < B; ++u) cur[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
-    }
-    while (have) {
-      const int64_t rn = r + B * s.ty;
-      const bool have_n = rn + (B - 1) * s.ty < r1;
-      if (have_n) {
+    for (int u = 0; u < U; ++u) raw[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
 #pragma unroll
-        for (int u = 0; u < B; ++u) nxt[u] = ld_nc16(x + (rn + u * s.ty) * C + c0);
-      }
-#pragma unroll
-      for (int u = 0; u < B; ++u) shifted8(cur[u], k, s1, s2);
-      r = rn;
-      have = have_n;
-#pragma unroll
-      for (int u = 0; u < B; ++u) cur[u] = nxt[u];
-    }
-  } else {
-    for (; r + (U - 1) * s.ty < r1; r += U * s.ty) {
-      uint4 raw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) raw[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
-#pragma unroll
-      for (int u = 0; u < U; ++u) shifted8(raw[u], k, s1, s2);
-    }
+    for (int u = 0; u < U; ++u) shifted8(raw[u], k, s1, s2);
   }
   for (; r < r1; r += s.ty) shifted8(ld_nc16(x + r * C + c0), k, s1, s2);
   pdl_trigger();
@@ -550,12 +521,8 @@ cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, cons
   const TileShape sh = tile_shape(C);
   const int blocks = bn_row_blocks(M, C);
   float* partial = (float*)((char*)ws + 256);
-  if (g_tune_bn_pipe)
-    bn_fwd_partial_kernel<true><<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
-        (const __nv_bfloat16*)x, M, C, partial);
-  else
-    bn_fwd_partial_kernel<false><<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
-        (const __nv_bfloat16*)x, M, C, partial);
+  bn_fwd_partial_kernel<<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
+      (const __nv_bfloat16*)x, M, C, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   float* scale = scale_shift;

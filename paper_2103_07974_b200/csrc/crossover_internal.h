@@ -70,8 +70,6 @@ extern int g_tune_sync_ctas;
 extern int g_tune_p2p_ctas;
 extern int g_tune_bn_no_pdl;
 extern int g_tune_bn_ctas_per_sm;
-extern int g_tune_bn_ctas_per_sm;
-extern int g_tune_bn_pipe;
 extern int g_tune_k1_chunk, g_tune_k2_chunk, g_tune_k2_stages, g_tune_ctas_per_sm, g_tune_k2_debug;
 int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s);

@@ -34,11 +34,6 @@ def main():
     for a in sys.argv[1:]:
         if a.startswith("--ctas-per-sm="):
             _lib.tune("bn_ctas_per_sm", int(a.split("=")[1]))
-    for a in sys.argv[1:]:
-        if a.startswith("--ctas-per-sm="):
-            _lib.tune("bn_ctas_per_sm", int(a.split("=")[1]))
-        if a == "--pipe":
-            _lib.tune("bn_pipe", 1)
 
     dev = torch.device("cuda", 0)
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
