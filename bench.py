@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--scenario", default="", help="run a reference scenario JSON file's jobs")
     ap.add_argument("--scenario-time-scale", type=float, default=0.02,
                     help="multiplier on inline scenario jobs' forward/backward ms")
+    ap.add_argument("--barrier", default="auto", choices=["auto", "flags", "nccl"],
+                    help="cross-rank barrier of the p2p / ce transports: SM-free stream-memory-op "
+                         "flags (auto when supported) or a 1-element NCCL all-reduce")
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
     ap.add_argument("--sync-ctas", type=int, default=0, help="persistent grid cap of K1/K2")
     ap.add_argument("--comm-priority", default="high", choices=["high", "low"],
@@ -312,6 +315,7 @@ class Harness:
 
 
 P2P_CTAS: int | None = None   # --p2p-ctas; None = the scheduler's per-policy default
+BARRIER = "auto"              # --barrier: cross-rank barrier of the p2p / ce transports
 
 
 def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
@@ -327,7 +331,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
 
     mode = sync_mode if h.world > 1 else "auto"
     sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
-                               comm_priority=comm_priority, p2p_ctas=P2P_CTAS)
+                               comm_priority=comm_priority, p2p_ctas=P2P_CTAS, barrier=BARRIER)
     for j, a in enumerate(base):
         sched.register(dataclasses.replace(a, iterations=W + K,
                                            data=host_data[j] if host_data else a.data))
@@ -451,9 +455,10 @@ def run_ours(args):
     h = Harness(args.nccl_max_ctas)
     rank, world, dev = h.rank, h.world, h.dev
     from paper_2103_07974_b200 import _lib
+    global P2P_CTAS, BARRIER
     if args.p2p_ctas:   # override the scheduler's policy-dependent cap, both arms
-        global P2P_CTAS
         P2P_CTAS = args.p2p_ctas
+    BARRIER = args.barrier
     if args.sync_ctas:
         _lib.tune("sync_ctas", args.sync_ctas)
     if args.bn_no_pdl:
@@ -561,7 +566,8 @@ def run_ours(args):
                        "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
-                                     {"crossover": sync0.mode, "sequential": sync_seq.mode})},
+                                     {"crossover": sync0.mode, "sequential": sync_seq.mode}),
+                       "rank_barrier": sync0.barrier_kind},
             "transport_tuner": tuner,
             "speedup_vs_sequential": round(rot_seq / rot_cross, 4),
             "sequential": {"value": round(seq_value, 2), "ms_per_step": round(rot_seq, 3)},

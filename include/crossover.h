@@ -183,6 +183,16 @@ CS_API int cs_ipc_close_handle(void* ptr);
  * local or peer-mapped (IPC) device memory, so a pull from a peer crosses NVLink without
  * occupying any SM -- the transport of the "ce" sync mode. */
 CS_API int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+/* Cross-rank barrier without SMs: stream memory operations on IPC-mapped uint32 flag arrays.
+ * Rank r writes `epoch` into slot r of every peer's array (peer_flags[p] = rank p's array as
+ * mapped here; a system-scope fence orders all earlier work of the stream before each write),
+ * then the stream waits until every peer's slot in its own array (local_flags) is >= epoch
+ * (cyclic compare).  Every rank must call it with the same epoch sequence.  Replaces the
+ * 1-element NCCL all-reduce barriers of the p2p / ce transports, whose kernels need a free SM
+ * while the other app's GEMMs occupy them. */
+CS_API int cs_stream_memops_supported(void);
+CS_API int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, int nranks,
+                           uint32_t epoch, void* stream);
 
 /* channels_last BatchNorm2d (training) for the apps' compute: x / y / dy / dx / residual are
  * bf16 [M, C] row-major (M = N*H*W, C % 8 == 0, C <= 256 or C % 256 == 0), weight / bias /

@@ -3,6 +3,7 @@
 // Host-side work per call is O(n_tensors): validate, build the chunk prefix,
 // copy descriptors into a by-value kernel-parameter block, launch.  No device
 // allocation, no synchronisation, no host<->device copies.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -11,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "crossover.h"
@@ -242,6 +244,71 @@ int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   if (dst == nullptr || src == nullptr) return set_error(CS_ERR_ARG, "cs_copy_async: NULL pointer");
   return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream),
                      "cs_copy_async");
+}
+
+// ---------------------------------------------------------------------------
+// SM-free cross-rank barrier: stream memory operations (executed by the GPU front end, no
+// kernel).  The driver entry points come from cudaGetDriverEntryPointByVersion, so the library
+// does not link libcuda and still loads on a host without a driver.
+// ---------------------------------------------------------------------------
+namespace {
+typedef CUresult (*PFN_memop32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_attr)(int*, CUdevice_attribute, CUdevice);
+PFN_memop32 g_wait32 = nullptr, g_write32 = nullptr;
+PFN_attr g_attr = nullptr;
+std::once_flag g_memops_once;
+int g_memops_status = (int)cudaErrorNotSupported;
+
+void load_memops() {
+  cudaDriverEntryPointQueryResult q1, q2, q3;
+  cudaError_t e1 = cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", (void**)&g_wait32, 12000,
+                                                    cudaEnableDefault, &q1);
+  cudaError_t e2 = cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", (void**)&g_write32, 12000,
+                                                    cudaEnableDefault, &q2);
+  cudaError_t e3 = cudaGetDriverEntryPointByVersion("cuDeviceGetAttribute", (void**)&g_attr, 12000,
+                                                    cudaEnableDefault, &q3);
+  if (e1 == cudaSuccess && e2 == cudaSuccess && e3 == cudaSuccess && q1 == cudaDriverEntryPointSuccess &&
+      q2 == cudaDriverEntryPointSuccess && q3 == cudaDriverEntryPointSuccess && g_wait32 && g_write32)
+    g_memops_status = 0;
+  else
+    g_memops_status = (int)cudaErrorNotSupported;
+  cudaGetLastError();
+}
+}  // namespace
+
+int cs_stream_memops_supported(void) {
+  std::call_once(g_memops_once, load_memops);
+  if (g_memops_status) return 0;
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if (g_attr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_STREAM_MEM_OPS_V1, (CUdevice)dev) != CUDA_SUCCESS) return 0;
+  return v ? 1 : 0;
+}
+
+int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, int nranks,
+                    uint32_t epoch, void* stream) {
+  if (peer_flags == nullptr || local_flags == 0 || nranks < 1 || nranks > CS_MAX_SOURCES ||
+      rank < 0 || rank >= nranks)
+    return set_error(CS_ERR_ARG, "cs_flag_barrier: invalid arguments");
+  std::call_once(g_memops_once, load_memops);
+  if (g_memops_status)
+    return set_error(g_memops_status, "cs_flag_barrier: stream memory operations unavailable");
+  CUstream s = (CUstream)stream;
+  // announce: my slot in every peer's flag array (a system-scope fence precedes each write, so
+  // everything this stream did before is visible to the peer that observes the flag)
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    if (peer_flags[p] == 0) return set_error(CS_ERR_ARG, "cs_flag_barrier: NULL flag array of rank %d", p);
+    CUresult r = g_write32(s, (CUdeviceptr)(peer_flags[p] + 4u * (uint64_t)rank), epoch, 0);
+    if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: write to rank %d failed (%d)", p, (int)r);
+  }
+  // wait: every peer's slot in my array has reached this epoch (cyclic >=)
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    CUresult r = g_wait32(s, (CUdeviceptr)(local_flags + 4u * (uint64_t)p), epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: wait on rank %d failed (%d)", p, (int)r);
+  }
+  return 0;
 }
 
 int cs_ipc_close_handle(void* ptr) {

@@ -115,7 +115,8 @@ class FusedGradientSync:
     def __init__(self, params: Sequence[torch.Tensor], settings: SgdSettings,
                  comm: NcclCommunicator | None = None, local_workers: int = 1,
                  align: int = 32, mode: str = "auto", snapshot_rows: int = 0,
-                 flat_params: torch.Tensor | None = None, p2p_ctas: int = 0):
+                 flat_params: torch.Tensor | None = None, p2p_ctas: int = 0,
+                 barrier: str = "auto"):
         if not params:
             raise ConfigError("an app needs at least one trainable parameter")
         dev = params[0].device
@@ -210,6 +211,7 @@ class FusedGradientSync:
             fmap = exchange_peer_addresses(buffer_of(flat_params), self.rank, self.ranks)
             self._peer_maps = [bmap, fmap]
             self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
+            self._init_barrier(barrier)
             if mode in ("p2p", "adaptive"):
                 self._init_p2p(bmap, fmap, off, p2p_ctas)
             if mode in ("ce", "adaptive"):
@@ -247,6 +249,45 @@ class FusedGradientSync:
         elif mode == "direct":
             self._sources = np.zeros(1, dtype=np.uint64)
         self._finish_init(settings)
+
+    def _init_barrier(self, barrier: str) -> None:
+        """Cross-rank barriers of the p2p / ce transports: SM-free stream-memory-op flags
+        (cs_flag_barrier) when every rank supports them ("auto" / "flags"), else a 1-element
+        NCCL all-reduce ("nccl").  The NCCL barrier's kernel needs a free SM, which it may wait
+        for while the other app's GEMMs hold every SM; the flag barrier runs in the GPU front end."""
+        from .p2p import DeviceBuffer, all_ranks_agree, exchange_peer_addresses
+
+        if barrier not in ("auto", "flags", "nccl"):
+            raise ConfigError(f"unknown barrier {barrier!r}")
+        self._flag_peers = None
+        self._epoch = 0
+        if barrier == "nccl":
+            return
+        supported = bool(_lib.lib.cs_stream_memops_supported())
+        if not all_ranks_agree(supported):
+            if barrier == "flags":
+                raise ConfigError("stream memory operations are not supported on every rank")
+            return
+        self._flags_buf = DeviceBuffer(32, self.bucket.device)     # uint32 slots, zeroed
+        fm = exchange_peer_addresses(self._flags_buf, self.rank, self.ranks)
+        self._peer_maps.append(fm)
+        self._flag_peers = np.asarray(fm.addresses, dtype=np.uint64)
+        self._flag_local = self._flags_buf.ptr
+
+    def _rank_barrier(self, stream: int) -> None:
+        if self._flag_peers is None:
+            self.comm.all_reduce_(self._barrier.data_ptr(), 1, stream)
+            return
+        self._epoch = (self._epoch + 1) & 0xFFFFFFFF
+        _lib.check("cs_flag_barrier", _lib.lib.cs_flag_barrier(
+            self._flag_peers.ctypes.data, self._flag_local, self.rank, self.ranks, self._epoch,
+            stream))
+
+    @property
+    def barrier_kind(self) -> str | None:
+        if self.mode not in ("p2p", "ce", "adaptive"):
+            return None
+        return "flags" if self._flag_peers is not None else "nccl"
 
     def set_transport(self, transport: str) -> None:
         """Pick the NVLink transport of the next syncs (adaptive mode switches freely: both
@@ -411,8 +452,7 @@ class FusedGradientSync:
 
     def _p2p_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
         """barrier -> fused reduce + update + all-gather over NVLink -> barrier."""
-        bar = self._barrier.data_ptr()
-        self.comm.all_reduce_(bar, 1, stream)          # every rank's K1 has landed
+        self._rank_barrier(stream)                     # every rank's K1 has landed
         if timer is not None:
             timer.begin("k2_p2p_fused")
         self._hyper.first_step = int(self.first_step)
@@ -422,7 +462,7 @@ class FusedGradientSync:
         self.kernel_launches += 1
         if timer is not None:
             timer.end("k2_p2p_fused")
-        self.comm.all_reduce_(bar, 1, stream)          # every rank's parameter writes landed
+        self._rank_barrier(stream)                     # every rank's parameter writes landed
         if snapshot_row is not None:
             if self.snapshot is None:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
@@ -442,8 +482,7 @@ class FusedGradientSync:
         pulls it, every peer has finished reading my bucket before my next K1 rewrites it, and
         (by stream order on each peer) a peer's all-gather pulls of iteration t complete before
         it enters iteration t+1's first barrier, so my K2 at t+1 never races them."""
-        bar = self._barrier.data_ptr()
-        self.comm.all_reduce_(bar, 1, stream)          # every rank's K1 has landed
+        self._rank_barrier(stream)                     # every rank's K1 has landed
         if timer is not None:
             timer.begin("c1_ce_reduce_scatter")
         self._ce_copies(self._ce_rs, stream)
@@ -453,7 +492,7 @@ class FusedGradientSync:
         self.update(stream, None, None)
         if timer is not None:
             timer.end("k2_update")
-        self.comm.all_reduce_(bar, 1, stream)          # every shard updated, every bucket read
+        self._rank_barrier(stream)                     # every shard updated, every bucket read
         if timer is not None:
             timer.begin("c1_ce_all_gather")
         self._ce_copies(self._ce_ag, stream)

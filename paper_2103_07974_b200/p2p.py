@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping"]
+__all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping", "all_ranks_agree"]
 
 _live: dict[int, "DeviceBuffer"] = {}
 
@@ -103,3 +103,12 @@ def exchange_peer_addresses(buf: DeviceBuffer, rank: int, world: int) -> PeerMap
         mapping.close()
         raise ConfigError("p2p peer mapping failed on some rank" + (f" ({error})" if error else ""))
     return mapping
+
+
+def all_ranks_agree(ok: bool) -> bool:
+    """True iff every rank passes True (collective over torch.distributed's CPU group)."""
+    import torch.distributed as dist
+
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(int(t.item()))

@@ -207,7 +207,7 @@ class CrossoverScheduler:
                  record_weights: bool = False, align: int = 32, sync_mode: str = "auto",
                  time_kernels: bool = False, comm_priority: int = -1,
                  perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0,
-                 nvtx: bool = False, p2p_ctas: int | None = None):
+                 nvtx: bool = False, p2p_ctas: int | None = None, barrier: str = "auto"):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -224,6 +224,7 @@ class CrossoverScheduler:
         self.watchdog_s = watchdog_s
         self.nvtx = nvtx
         self.p2p_ctas = p2p_ctas
+        self.barrier = barrier
         with torch.cuda.device(self.device):
             self.compute_stream = torch.cuda.Stream(self.device)
             lo, hi = torch.cuda.Stream.priority_range()
@@ -255,7 +256,8 @@ class CrossoverScheduler:
             32 if self.policy is Policy.CROSSOVER else 0)
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
                                  self._mode_for(app), app.iterations if self.record_weights else 0,
-                                 flat_params=app.flat_params, p2p_ctas=p2p_ctas)
+                                 flat_params=app.flat_params, p2p_ctas=p2p_ctas,
+                                 barrier=self.barrier)
         st = JobRuntimeState(app.job_id, app=app, sync=sync)
         self.states.append(st)
         return st

@@ -131,8 +131,23 @@ def main():
     ce_w = [s8.weights(f"m{k}").cpu() for k in range(2)]
     s8.close()
     res["checks"].append({"name": "ce_mode_used", "ok": all(st.sync.mode == "ce" for st in s8.states)})
+    res["checks"].append({"name": "sm_free_flag_barrier_used",
+                          "ok": all(st.sync.barrier_kind == "flags" for st in s8.states)})
     res["checks"].append({"name": f"ce_bitwise_eq_p2p_w{world}",
                           "ok": all(torch.equal(ce_w[k], p2p_w[k]) for k in range(2))})
+
+    # (4b') the same ce run with the NCCL 1-element all-reduce barriers instead of the flags
+    s10 = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode="ce",
+                             barrier="nccl")
+    for k, (ds, rs) in enumerate(specs):
+        s10.register(mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T,
+                             dev, local_workers=1, worker_count=world, flat="ipc"))
+    s10.run()
+    ce_nccl_w = [s10.weights(f"m{k}").cpu() for k in range(2)]
+    kinds = {st.sync.barrier_kind for st in s10.states}
+    s10.close()
+    res["checks"].append({"name": "ce_nccl_barrier_bitwise_eq_flags",
+                          "ok": kinds == {"nccl"} and all(torch.equal(ce_nccl_w[k], ce_w[k]) for k in range(2))})
 
     # (4c) auto under crossover with IPC flat parameters = adaptive transport: copy engines for
     #      two rotations, the P2P kernel for two, then the measured faster one; the choice is the

@@ -27,11 +27,14 @@ def main():
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"])
     ap.add_argument("--p2p-ctas", type=int, default=0)
     ap.add_argument("--nccl-max-ctas", type=int, default=0)
+    ap.add_argument("--barrier", default="auto", choices=["auto", "flags", "nccl"])
     args = ap.parse_args()
     from paper_2103_07974_b200.apps import synthetic_app
     from paper_2103_07974_b200.scheduler import Policy, overlap_roofline
 
     h = Harness(args.nccl_max_ctas)
+    import bench
+    bench.BARRIER = args.barrier
     if args.p2p_ctas:
         import bench
         bench.P2P_CTAS = args.p2p_ctas
@@ -50,6 +53,7 @@ def main():
         rot_x, rot_s = cross["ms"] / args.steps, seq["ms"] / args.steps
         row = {"bucket_MB": mb, "world": h.world, "sync_mode": cross["sched"].states[0].sync.mode,
                "sync_mode_sequential": seq["sched"].states[0].sync.mode,
+               "rank_barrier": cross["sched"].states[0].sync.barrier_kind,
                "transport_tuner": tuner,
                "p2p_ctas": args.p2p_ctas, "nccl_max_ctas": args.nccl_max_ctas,
                "rho": round(rho, 4),
