@@ -253,22 +253,18 @@ int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
 // ---------------------------------------------------------------------------
 namespace {
 typedef CUresult (*PFN_memop32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*PFN_attr)(int*, CUdevice_attribute, CUdevice);
 PFN_memop32 g_wait32 = nullptr, g_write32 = nullptr;
-PFN_attr g_attr = nullptr;
 std::once_flag g_memops_once;
 int g_memops_status = (int)cudaErrorNotSupported;
 
 void load_memops() {
-  cudaDriverEntryPointQueryResult q1, q2, q3;
+  cudaDriverEntryPointQueryResult q1, q2;
   cudaError_t e1 = cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", (void**)&g_wait32, 12000,
                                                     cudaEnableDefault, &q1);
   cudaError_t e2 = cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", (void**)&g_write32, 12000,
                                                     cudaEnableDefault, &q2);
-  cudaError_t e3 = cudaGetDriverEntryPointByVersion("cuDeviceGetAttribute", (void**)&g_attr, 12000,
-                                                    cudaEnableDefault, &q3);
-  if (e1 == cudaSuccess && e2 == cudaSuccess && e3 == cudaSuccess && q1 == cudaDriverEntryPointSuccess &&
-      q2 == cudaDriverEntryPointSuccess && q3 == cudaDriverEntryPointSuccess && g_wait32 && g_write32)
+  if (e1 == cudaSuccess && e2 == cudaSuccess && q1 == cudaDriverEntryPointSuccess &&
+      q2 == cudaDriverEntryPointSuccess && g_wait32 && g_write32)
     g_memops_status = 0;
   else
     g_memops_status = (int)cudaErrorNotSupported;
@@ -277,12 +273,11 @@ void load_memops() {
 }  // namespace
 
 int cs_stream_memops_supported(void) {
+  // 32-bit wait / write stream memory operations (the v2 API) are part of the CUDA 12 driver on
+  // every supported GPU; the legacy CAN_USE_STREAM_MEM_OPS_V1 attribute describes the v1 API
+  // only, so availability = the entry points resolve.
   std::call_once(g_memops_once, load_memops);
-  if (g_memops_status) return 0;
-  int dev = 0, v = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
-  if (g_attr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_STREAM_MEM_OPS_V1, (CUdevice)dev) != CUDA_SUCCESS) return 0;
-  return v ? 1 : 0;
+  return g_memops_status == 0 ? 1 : 0;
 }
 
 int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, int nranks,
