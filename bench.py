@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import dataclasses
+import gc
 import json
 import os
 import statistics
@@ -353,6 +354,10 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
         sched.timer.clear()
     launches0 = sched.kernel_launches
     n_spans0 = len(sched.recorder._pending)
+    # Python's cyclic GC can pause the host for tens of ms (the previous runs' autograd / span
+    # objects); a paused host lets the GPU queue drain.  Collect now, keep it off while timing.
+    gc.collect()
+    gc.disable()
     clk = Clocks(h.local) if clocks else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(cs)
@@ -363,6 +368,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     cs.wait_event(join)
     end.record(cs)
     end.synchronize()
+    gc.enable()
     clk_info = clk.stop() if clk else None
     ms_total = h.max_over_ranks(start.elapsed_time(end))
     trace = sched.recorder.resolve()
@@ -388,7 +394,7 @@ def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
     if h.world < 2 or sm not in ("p2p", "ce", "auto"):
         return sm, sm, None
     try:
-        n_cal = _TransportTuner.MIN_BUDGET if sm == "auto" else 1
+        n_cal = _TransportTuner.MIN_BUDGET if sm == "auto" else int(os.environ.get("CS_PROBE_ROTATIONS", "1"))
         probe = timed_run(h, base, Policy.CROSSOVER, 0, n_cal, sync_mode=sm, comm_priority=prio,
                           time_kernels=False)
         tuner = probe["sched"].tuner
@@ -510,6 +516,11 @@ def run_ours(args):
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
                                              time_kernels=False, sync_mode=sm, comm_priority=prio)
 
+    # the models must still be numerically healthy: a diverged model (NaN weights) changes the
+    # kernels' speed and invalidates the measurement
+    import torch as _torch
+    weights_finite = all(bool(_torch.isfinite(p).all()) for a in base for p in a.params)
+
     # legality + bit-exact schedule of the measured runs
     order = [a.job_id for a in base]
     for r in (cross, seq):
@@ -569,6 +580,7 @@ def run_ours(args):
                                      {"crossover": sync0.mode, "sequential": sync_seq.mode}),
                        "rank_barrier": sync0.barrier_kind},
             "transport_tuner": tuner,
+            "weights_finite": weights_finite,
             "speedup_vs_sequential": round(rot_seq / rot_cross, 4),
             "sequential": {"value": round(seq_value, 2), "ms_per_step": round(rot_seq, 3)},
             "rho": round(sum(comm_t) / sum(comp), 5) if sum(comp) else None,
@@ -591,6 +603,9 @@ def run_ours(args):
         }
         if args.trace_out:
             Path(args.trace_out).write_text(trace_to_chrome_json(cross["trace"]))
+            Path(args.trace_out).with_suffix(".spans.json").write_text(json.dumps(
+                [[s.lane_id, s.job_id, s.phase.value, s.iteration, s.start, s.end]
+                 for s in cross["trace"].spans]))
         if args.metrics_out:
             # the reference's own measure / compare / report (metrics.py:62-200) on measured traces
             from paper_2103_07974_b200.metrics import compare, measure, report

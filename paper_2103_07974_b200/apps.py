@@ -325,6 +325,10 @@ def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
 
 
 DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
+# VGG-16 has no BatchNorm: the torchvision recipe trains it at lr 0.01 / weight decay 5e-4; at
+# lr 0.1 it diverges within ~13 steps on synthetic data (weights -> NaN), which invalidates any
+# throughput measured afterwards (tools/diag_mix3.py)
+VGG_SGD = SgdSettings(lr=0.01, momentum=0.9, weight_decay=5e-4)
 
 
 def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
@@ -338,7 +342,7 @@ def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device,
 
 
 def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
-                 host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
+                 host_data: bool = False, sgd: SgdSettings = VGG_SGD,
                  graphed: bool = False, flat: bool = False, fast_bn: bool = False) -> App:
     import torchvision
 

@@ -29,6 +29,7 @@ returned as a measured ``Trace``.
 from __future__ import annotations
 
 import contextlib
+import gc
 import time
 from dataclasses import dataclass, field
 from enum import Enum
@@ -441,9 +442,20 @@ class CrossoverScheduler:
         raise DeadlockError(job, it, f"policy={self.policy.value}; {detail}")
 
     def run(self) -> Trace:
-        """Step every app through its budget; returns the measured trace."""
-        while self.step():
-            pass
+        """Step every app through its budget; returns the measured trace.
+
+        Python's cyclic GC is paused while stepping: a collection pauses the host for tens of
+        ms, the GPU queue drains meanwhile, and at W > 1 every rank then waits for the paused
+        one at the next barrier."""
+        was_enabled = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        try:
+            while self.step():
+                pass
+        finally:
+            if was_enabled:
+                gc.enable()
         self.drain()
         stuck = self.pending()
         if stuck:
