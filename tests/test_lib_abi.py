@@ -77,9 +77,19 @@ def test_argument_errors_without_gpu():
     assert _lib.lib.cs_bn_forward(16, None, 100, 7, None, None, None, None, 0.1, 1e-5, 16, 16, 16, 16,
                                   16, 0, None) == _lib.CS_ERR_ARG
     assert b"cs_bn_forward" in _lib.lib.cs_last_error()
+    # copy-engine transport and the SM-free flag barrier validate before touching CUDA
+    assert _lib.lib.cs_copy_async(None, None, 0, None) == 0
+    assert _lib.lib.cs_copy_async(None, None, 16, None) == _lib.CS_ERR_ARG
+    assert _lib.lib.cs_flag_barrier(None, 0, 0, 2, 1, None) == _lib.CS_ERR_ARG
+    peers = np.zeros(2, dtype=np.uint64)
+    assert _lib.lib.cs_flag_barrier(peers.ctypes.data, 64, 2, 2, 1, None) == _lib.CS_ERR_ARG   # rank out of range
+    assert _lib.lib.cs_stream_memops_supported() in (0, 1)
     p2p = _lib.P2PDesc()
     p2p.nranks = 9
     assert _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(p2p), ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=9)),
+                                            None) == _lib.CS_ERR_ARG
+    p2p.nranks, p2p.max_ctas = 2, -1
+    assert _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(p2p), ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=2)),
                                             None) == _lib.CS_ERR_ARG
 
 
