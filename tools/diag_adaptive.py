@@ -1,3 +1,7 @@
+"""Per-slot timeline of a 2-app synthetic crossover run (diagnosing transport choices).
+
+    torchrun --nproc-per-node 4 tools/diag_adaptive.py <bucket MB> <sync mode>
+"""
 import sys, json
 sys.path.insert(0, "/root/repo")
 from bench import Harness, timed_run

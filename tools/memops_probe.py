@@ -1,3 +1,10 @@
+"""Single-GPU probe of the stream-memory-op flag barrier (cs_flag_barrier).
+
+    python tools/memops_probe.py
+
+Emulates rank 0 of 2 with both flag arrays local: the "peer" slot is pre-set, so the wait
+returns immediately; prints whether the driver entry points resolved and the barrier's rc.
+"""
 import ctypes, torch, sys
 sys.path.insert(0, "/root/repo")
 from paper_2103_07974_b200 import _lib
