@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--metrics-out", default="", help="colosim.metrics/v1 JSON + CSV of the measured runs")
     ap.add_argument("--no-graphs", action="store_true", help="eager forward/backward (no CUDA graphs)")
     ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
+    ap.add_argument("--cudnn-stem", action="store_true",
+                    help="cuDNN for the RGB stem convolution instead of im2col + tensor-core GEMMs")
     ap.add_argument("--bn-no-pdl", action="store_true",
                     help="launch the BN finalize / apply kernels without programmatic dependent launch")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"],
@@ -496,11 +498,13 @@ def run_ours(args):
             else:
                 fn = apps.resnet50_app if name == "resnet50" else apps.vgg16_app
                 base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j + rank,
-                               graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn))
+                               graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
+                               stem="cudnn" if args.cudnn_stem else "gemm"))
         args.no_e2e, args.no_cpu_baseline = True, True
     else:
         base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
-                      graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn)
+                      graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
+                      stem="cudnn" if args.cudnn_stem else "gemm")
             for j in range(args.jobs)]
     host_data = None if args.no_e2e else [
         apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + j, dev, host_uint8=True))
@@ -539,7 +543,10 @@ def run_ours(args):
     from paper_2103_07974_b200.bn import CrossoverBatchNorm2d, CrossoverMaxPool2d
     n_bn = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverBatchNorm2d)) for a in base)
     n_pool = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverMaxPool2d)) for a in base)
-    bn_launches = 6 * n_bn + 2 * n_pool
+    n_stem = 0 if args.cudnn_stem else sum(
+        sum(1 for m in a.model.modules() if isinstance(m, _torch.nn.Conv2d) and m.in_channels == 3)
+        for a in base)
+    bn_launches = 6 * n_bn + 2 * n_pool + n_stem           # + one im2col per RGB stem
     hbm_peak, peak_kind = peaks()
     sync0 = cross["sched"].states[0].sync
     kernels = kernel_summary(cross["kernels"], sync0)
@@ -573,7 +580,8 @@ def run_ours(args):
                                     f"{args.batch}/GPU")
                                    + ", bf16 autocast, fp32 params/grads, SGD momentum 0.9"
                                    + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs")
-                                   + ("" if args.aten_bn else ", NHWC BN(+ReLU/+residual) and max-pool kernels"),
+                                   + ("" if args.aten_bn else ", NHWC BN(+ReLU/+residual) and max-pool kernels")
+                                   + ("" if args.cudnn_stem else ", RGB stem as im2col + GEMMs"),
                        "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
                        "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
                        "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else

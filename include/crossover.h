@@ -228,6 +228,12 @@ CS_API int cs_maxpool2d_forward(const void* x, void* y, uint8_t* argmax, const i
 CS_API int cs_maxpool2d_backward(const void* dy, const uint8_t* argmax, void* dx,
                                  const int* shape, void* stream);
 
+/* Patch matrix of an NHWC bf16 image batch for a convolution as a GEMM (the models' RGB stem):
+ * shape = {N, H, W, C, OH, OW, kh, kw, sh, sw, ph, pw, KP}; patches: bf16 [N*OH*OW, KP],
+ * row m = output pixel (n, oh, ow), column j < kh*kw*C = x[n, oh*sh-ph+j/(kw*C), ow*sw-pw+(j/C)%kw,
+ * j%C] (0 outside the image), columns >= kh*kw*C zero; KP % 8 == 0, patches 16-byte aligned. */
+CS_API int cs_im2col_nhwc(const void* x, void* patches, const int* shape, void* stream);
+
 /* NCCL communicator over NVLink / NVSwitch (one per process, one per job set).
  * min_ctas / max_ctas <= 0 leave NCCL's defaults. */
 CS_API int cs_nccl_version(void);

@@ -304,13 +304,17 @@ class _GraphedImageModel(torch.nn.Module):
 def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
                device: torch.device, seed: int, host_data: bool, sgd: SgdSettings,
                n_batches: int = 2, graphed: bool = False, flat: bool = False,
-               fast_bn: bool = False) -> App:
+               fast_bn: bool = False, stem: str = "gemm") -> App:
     if fast_bn:   # NHWC BatchNorm kernels of libcrossover.so instead of ATen's (same semantics)
         from .bn import fuse_resnet, swap_batchnorm
 
         swap_batchnorm(model)
         if hasattr(model, "layer1"):
             fuse_resnet(model)      # BN + ReLU (+ residual add) in one pass
+    if stem == "gemm":   # RGB stem as im2col + tensor-core GEMMs instead of cuDNN (stem.py)
+        from .stem import gemm_stem
+
+        gemm_stem(model)
     model = model.to(device).to(memory_format=torch.channels_last)
     data = _CycleData(synthetic_image_batches(batch, n_batches, seed, device, host_uint8=host_data))
     params = [p for p in model.parameters() if p.requires_grad]
@@ -333,22 +337,24 @@ VGG_SGD = SgdSettings(lr=0.01, momentum=0.9, weight_decay=5e-4)
 
 def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
-                 graphed: bool = False, flat: bool = False, fast_bn: bool = False) -> App:
+                 graphed: bool = False, flat: bool = False, fast_bn: bool = False,
+                 stem: str = "gemm") -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn)
+                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn, stem=stem)
 
 
 def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = VGG_SGD,
-                 graphed: bool = False, flat: bool = False, fast_bn: bool = False) -> App:
+                 graphed: bool = False, flat: bool = False, fast_bn: bool = False,
+                 stem: str = "gemm") -> App:
     import torchvision
 
     torch.manual_seed(seed)
     return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn)
+                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn, stem=stem)
 
 
 def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,

@@ -373,6 +373,19 @@ int cs_maxpool2d_forward(const void* x, void* y, uint8_t* argmax, const int* sha
                      "cs_maxpool2d_forward launch");
 }
 
+int cs_im2col_nhwc(const void* x, void* patches, const int* s, void* stream) {
+  bool ok = x != nullptr && patches != nullptr && s != nullptr && !(((uintptr_t)patches) & 15u);
+  if (ok) {
+    for (int i = 0; i < 10; ++i) ok = ok && s[i] > 0;
+    ok = ok && s[10] >= 0 && s[11] >= 0 && s[12] > 0 && s[12] % 8 == 0 && s[12] >= s[3] * s[6] * s[7] &&
+         s[4] == (s[1] + 2 * s[10] - s[6]) / s[8] + 1 && s[5] == (s[2] + 2 * s[11] - s[7]) / s[9] + 1 &&
+         (int64_t)s[0] * s[4] * s[5] * (s[12] / 8) < (int64_t)INT32_MAX &&
+         (int64_t)s[0] * s[1] * s[2] * s[3] < (int64_t)INT32_MAX * 8;
+  }
+  if (!ok) return set_error(CS_ERR_ARG, "cs_im2col_nhwc: invalid arguments");
+  return cuda_status(launch_im2col_nhwc(x, patches, s, (cudaStream_t)stream), "cs_im2col_nhwc launch");
+}
+
 int cs_maxpool2d_backward(const void* dy, const uint8_t* argmax, void* dx, const int* shape,
                           void* stream) {
   if (dy == nullptr || dx == nullptr || argmax == nullptr || !pool_shape_ok(shape) ||

@@ -74,6 +74,7 @@ extern int g_tune_k1_chunk, g_tune_k2_chunk, g_tune_k2_stages, g_tune_ctas_per_s
 int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s);
 int bn_row_blocks(int64_t M, int C);
+cudaError_t launch_im2col_nhwc(const void* x, void* p, const int* shape, cudaStream_t stream);
 size_t bn_workspace_bytes(int64_t M, int C);
 cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, const float* w,
                           const float* b, float* rm, float* rv, float momentum, float eps,

@@ -186,3 +186,36 @@ def test_maxpool_matches_aten_exactly(cuda_device, shape, k, s, p):
     yb.backward(dy)
     torch.testing.assert_close(xa.grad.float(), xb.grad.float(), rtol=1e-2, atol=1e-2)
     assert torch.equal(xa.grad != 0, xb.grad != 0)      # same selected positions
+
+
+@pytest.mark.parametrize("cfg", [dict(k=7, s=2, p=3, bias=False, hw=32),    # ResNet stem
+                                 dict(k=3, s=1, p=1, bias=True, hw=24),     # VGG stem
+                                 dict(k=5, s=3, p=2, bias=True, hw=17)])    # generic shape path
+def test_gemm_stem_matches_conv(cuda_device, cfg):
+    """The RGB stem as im2col + GEMMs (stem.py) vs F.conv2d in fp32: output at bf16 rounding,
+    weight / bias gradients at the tolerance of a bf16 GEMM over N*OH*OW terms."""
+    import torch.nn.functional as F
+
+    from paper_2103_07974_b200.stem import gemm_stem
+
+    torch.manual_seed(0)
+    conv = torch.nn.Conv2d(3, 64, cfg["k"], stride=cfg["s"], padding=cfg["p"], bias=cfg["bias"]).to(cuda_device)
+    ref = torch.nn.Conv2d(3, 64, cfg["k"], stride=cfg["s"], padding=cfg["p"], bias=cfg["bias"]).to(cuda_device)
+    ref.load_state_dict(conv.state_dict())
+    assert gemm_stem(conv) == 1
+    x = torch.randn(4, 3, cfg["hw"], cfg["hw"], device=cuda_device).to(torch.bfloat16).contiguous(
+        memory_format=torch.channels_last)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        y = conv(x)
+    y_ref = F.conv2d(x.float(), ref.weight, ref.bias, stride=cfg["s"], padding=cfg["p"])
+    assert y.shape == y_ref.shape and y.dtype == torch.bfloat16
+    assert y.is_contiguous(memory_format=torch.channels_last)
+    torch.testing.assert_close(y.float(), y_ref, rtol=2e-2, atol=2e-2)
+    dy = torch.randn_like(y_ref).to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    y.backward(dy)
+    y_ref.backward(dy.float())
+    torch.testing.assert_close(conv.weight.grad, ref.weight.grad, rtol=2e-2, atol=0.5)
+    if cfg["bias"]:
+        torch.testing.assert_close(conv.bias.grad, ref.bias.grad, rtol=1e-2, atol=0.1)
+    # the patch matrix itself is exact (a gather): im2col . W^T in fp32 == conv in fp32
+    assert conv.weight.grad.dtype == torch.float32
