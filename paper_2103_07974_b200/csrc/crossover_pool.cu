@@ -41,16 +41,19 @@ struct PoolShape {
   int N, H, W, C, OH, OW, kh, kw, sh, sw, ph, pw;
 };
 
-// 3x3 windows (the ResNet stem): all nine 16-byte loads issued before the first compare
+// 3x3 windows (the ResNet stem): all nine 16-byte loads issued before the first compare.
+// Idx = int when the element count fits (the host picks it): the per-thread index
+// decomposition is then 32-bit division, several times cheaper than 64-bit.
+template <typename Idx>
 __global__ void __launch_bounds__(kPoolThreads)
 maxpool3_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                     uint8_t* __restrict__ arg, PoolShape s) {
   const int cv = s.C / 8;
-  const int64_t total = (int64_t)s.N * s.OH * s.OW * cv;
-  for (int64_t i = (int64_t)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * kPoolThreads) {
+  const Idx total = (Idx)s.N * s.OH * s.OW * cv;
+  for (Idx i = (Idx)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
+       i += (Idx)gridDim.x * kPoolThreads) {
     const int c8 = (int)(i % cv);
-    int64_t t = i / cv;
+    Idx t = i / cv;
     const int ow = (int)(t % s.OW);
     t /= s.OW;
     const int oh = (int)(t % s.OH);
@@ -132,15 +135,16 @@ maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   }
 }
 
+template <typename Idx>
 __global__ void __launch_bounds__(kPoolThreads)
 maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
                    __nv_bfloat16* __restrict__ dx, PoolShape s) {
   const int cv = s.C / 8;
-  const int64_t total = (int64_t)s.N * s.H * s.W * cv;
-  for (int64_t i = (int64_t)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * kPoolThreads) {
+  const Idx total = (Idx)s.N * s.H * s.W * cv;
+  for (Idx i = (Idx)blockIdx.x * kPoolThreads + threadIdx.x; i < total;
+       i += (Idx)gridDim.x * kPoolThreads) {
     const int c8 = (int)(i % cv);
-    int64_t t = i / cv;
+    Idx t = i / cv;
     const int iw = (int)(t % s.W);
     t /= s.W;
     const int ih = (int)(t % s.H);
@@ -204,6 +208,102 @@ maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restri
   }
 }
 
+// The ResNet stem's pool (3x3, stride 2, padding 1, C = 8 * kCV): one CTA per row and the
+// channel-vector count a compile-time constant, so the per-thread index arithmetic is shifts and
+// masks (the generic kernels spend most of their time in runtime integer division).
+template <int kCV>
+__global__ void __launch_bounds__(128)
+maxpool_k3s2_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                        uint8_t* __restrict__ arg, PoolShape s) {
+  const int row = blockIdx.x;                 // n * OH + oh
+  const int n = row / s.OH, oh = row - n * s.OH;
+  const int h0 = 2 * oh - 1;
+  const __nv_bfloat16* img = x + (int64_t)n * s.H * s.W * (kCV * 8);
+  for (int v = threadIdx.x; v < s.OW * kCV; v += blockDim.x) {
+    const int ow = v / kCV, c8 = v % kCV;
+    const int w0 = 2 * ow - 1;
+    uint4 raw[9];
+    bool ok[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int ih = h0 + a, iw = w0 + b;
+        ok[a * 3 + b] = (unsigned)ih < (unsigned)s.H && (unsigned)iw < (unsigned)s.W;
+        raw[a * 3 + b] = ok[a * 3 + b]
+            ? __ldg(reinterpret_cast<const uint4*>(img + ((int64_t)ih * s.W + iw) * (kCV * 8) + c8 * 8))
+            : make_uint4(0, 0, 0, 0);
+      }
+    float best[8];
+    uint8_t idx[8];
+    const uint8_t first = (uint8_t)(max(0, -h0) * 3 + max(0, -w0));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { best[k] = -INFINITY; idx[k] = first; }
+#pragma unroll
+    for (int o = 0; o < 9; ++o) {
+      if (!ok[o]) continue;
+      float f[8];
+      unpack8p(raw[o], f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (f[k] > best[k] || isnan(f[k])) { best[k] = f[k]; idx[k] = (uint8_t)o; }   // ATen's rule
+    }
+    const int64_t out = ((int64_t)row * s.OW + ow) * kCV + c8;
+    *reinterpret_cast<uint4*>(y + out * 8) = pack8p(best);
+    uint2 packed;
+    packed.x = idx[0] | (idx[1] << 8) | (idx[2] << 16) | ((uint32_t)idx[3] << 24);
+    packed.y = idx[4] | (idx[5] << 8) | (idx[6] << 16) | ((uint32_t)idx[7] << 24);
+    *reinterpret_cast<uint2*>(arg + out * 8) = packed;
+  }
+}
+
+template <int kCV>
+__global__ void __launch_bounds__(128)
+maxpool_k3s2_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
+                        __nv_bfloat16* __restrict__ dx, PoolShape s) {
+  const int row = blockIdx.x;                 // n * H + ih
+  const int n = row / s.H, ih = row - n * s.H;
+  // windows oh with 2*oh - 1 <= ih <= 2*oh + 1
+  const int oh_lo = ih >> 1, oh_hi = min(s.OH - 1, (ih + 1) >> 1);
+  for (int v = threadIdx.x; v < s.W * kCV; v += blockDim.x) {
+    const int iw = v / kCV, c8 = v % kCV;
+    const int ow_lo = iw >> 1, ow_hi = min(s.OW - 1, (iw + 1) >> 1);
+    uint4 rg[4];
+    uint2 ra[4];
+    uint8_t me[4];
+    bool use[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int oh = oh_lo + (q >> 1), ow = ow_lo + (q & 1);
+      use[q] = oh <= oh_hi && ow <= ow_hi;
+      me[q] = (uint8_t)((ih - (2 * oh - 1)) * 3 + (iw - (2 * ow - 1)));
+      const int64_t o = (((int64_t)n * s.OH + oh) * s.OW + ow) * kCV + c8;
+      rg[q] = use[q] ? __ldg(reinterpret_cast<const uint4*>(dy + o * 8)) : make_uint4(0, 0, 0, 0);
+      ra[q] = use[q] ? __ldg(reinterpret_cast<const uint2*>(arg + o * 8)) : make_uint2(0, 0);
+    }
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!use[q]) continue;
+      float g[8];
+      unpack8p(rg[q], g);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t word = k < 4 ? ra[q].x : ra[q].y;
+        if (((word >> (8 * (k & 3))) & 0xffu) == me[q]) acc[k] += g[k];
+      }
+    }
+    const int64_t out = ((int64_t)row * s.W + iw) * kCV + c8;
+    *reinterpret_cast<uint4*>(dx + out * 8) = pack8p(acc);
+  }
+}
+
+static bool stem_pool(const PoolShape& s) {
+  return s.kh == 3 && s.kw == 3 && s.sh == 2 && s.sw == 2 && s.ph == 1 && s.pw == 1 && s.C == 64;
+}
+
 static unsigned pool_grid(int64_t total) {
   int64_t g = (total + kPoolThreads - 1) / kPoolThreads;
   if (g > 148 * 16) g = 148 * 16;
@@ -214,8 +314,15 @@ cudaError_t launch_maxpool_fwd(const void* x, void* y, void* arg, const int* sha
   PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5],
               shape[6], shape[7], shape[8], shape[9], shape[10], shape[11]};
   const int64_t total = (int64_t)s.N * s.OH * s.OW * (s.C / 8);
-  if (s.kh == 3 && s.kw == 3)
-    maxpool3_fwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
+  const bool narrow = (int64_t)s.N * s.H * s.W * s.C < INT32_MAX;   // every flat index fits int
+  if (stem_pool(s))
+    maxpool_k3s2_fwd_kernel<8><<<(unsigned)(s.N * s.OH), 128, 0, st>>>(
+        (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
+  else if (s.kh == 3 && s.kw == 3 && narrow)
+    maxpool3_fwd_kernel<int><<<pool_grid(total), kPoolThreads, 0, st>>>(
+        (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
+  else if (s.kh == 3 && s.kw == 3)
+    maxpool3_fwd_kernel<int64_t><<<pool_grid(total), kPoolThreads, 0, st>>>(
         (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)arg, s);
   else
     maxpool_fwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
@@ -228,8 +335,15 @@ cudaError_t launch_maxpool_bwd(const void* dy, const void* arg, void* dx, const 
   PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5],
               shape[6], shape[7], shape[8], shape[9], shape[10], shape[11]};
   const int64_t total = (int64_t)s.N * s.H * s.W * (s.C / 8);
-  maxpool_bwd_kernel<<<pool_grid(total), kPoolThreads, 0, st>>>(
-      (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
+  if (stem_pool(s))
+    maxpool_k3s2_bwd_kernel<8><<<(unsigned)(s.N * s.H), 128, 0, st>>>(
+        (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
+  else if ((int64_t)s.N * s.H * s.W * s.C < INT32_MAX)
+    maxpool_bwd_kernel<int><<<pool_grid(total), kPoolThreads, 0, st>>>(
+        (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
+  else
+    maxpool_bwd_kernel<int64_t><<<pool_grid(total), kPoolThreads, 0, st>>>(
+        (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
   return cudaGetLastError();
 }
 
