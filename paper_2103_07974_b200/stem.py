@@ -46,16 +46,22 @@ class _StemGemm(torch.autograd.Function):
         shape = (ctypes.c_int * 13)(n, h, w, c, oh, ow, kh, kw, sh, sw, ph, pw, kp)
         stream = torch.cuda.current_stream(x.device).cuda_stream
         _lib.check("cs_im2col_nhwc", _lib.lib.cs_im2col_nhwc(x.data_ptr(), p.data_ptr(), shape, stream))
+        # the output is allocated channels_last and the GEMM writes its NHWC storage through a
+        # 2-D view, so the Function returns a base tensor (consumers such as VGG's in-place
+        # ReLU may modify it) without a layout copy
+        y = torch.empty((n, o, oh, ow), dtype=torch.bfloat16, device=x.device,
+                        memory_format=torch.channels_last)
+        y2d = y.permute(0, 2, 3, 1).view(n * oh * ow, o)
         with torch.autocast("cuda", enabled=False):
             wm = torch.zeros((o, kp), dtype=torch.bfloat16, device=x.device)
             wm[:, :k] = weight.detach().permute(0, 2, 3, 1).reshape(o, k)
             if bias is not None:
-                y = torch.addmm(bias.detach().to(torch.bfloat16), p, wm.t())
+                torch.addmm(bias.detach().to(torch.bfloat16), p, wm.t(), out=y2d)
             else:
-                y = p @ wm.t()
+                torch.mm(p, wm.t(), out=y2d)
         ctx.save_for_backward(p)
         ctx.meta = (o, c, kh, kw, k, weight.dtype, bias is not None)
-        return y.view(n, oh, ow, o).permute(0, 3, 1, 2)
+        return y
 
     @staticmethod
     def backward(ctx, dy):
