@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--aten-bn", action="store_true", help="ATen BatchNorm instead of the NHWC BN kernels")
     ap.add_argument("--cudnn-stem", action="store_true",
                     help="cuDNN for the RGB stem convolution instead of im2col + tensor-core GEMMs")
+    ap.add_argument("--side-grads", action="store_true",
+                    help="hand each bottleneck's identity gradient to the producing BN's backward "
+                         "(cs_bn_backward2) instead of an autograd add kernel")
     ap.add_argument("--bn-no-pdl", action="store_true",
                     help="launch the BN finalize / apply kernels without programmatic dependent launch")
     ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"],
@@ -474,6 +477,9 @@ def run_ours(args):
         _lib.tune("sync_ctas", args.sync_ctas)
     if args.bn_no_pdl:
         _lib.tune("bn_no_pdl", 1)
+    if args.side_grads:
+        from paper_2103_07974_b200 import bn as _bn
+        _bn._SIDE_GRADS = True
     K, W = args.steps, args.warmup
     build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
     # auto at W > 1: IPC flat parameters, and the scheduler picks the transport per policy

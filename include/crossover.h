@@ -219,6 +219,15 @@ CS_API int cs_bn_backward(const void* dy, const void* x, const void* residual, i
                           const float* scale_shift, const float* weight, float* grad_weight,
                           float* grad_bias, float* coef, void* dx, void* dresidual,
                           void* workspace, int flags, void* stream);
+/* cs_bn_backward with a second incoming gradient of the same output (dy2, bf16 [M, C], may be
+ * NULL): g = (dy + dy2) is formed in fp32 inside the kernels, before the activation mask.  The
+ * ResNet bottleneck delivers the identity-path gradient of a block's input this way instead of
+ * materialising the autograd sum (one elementwise add kernel per block). */
+CS_API int cs_bn_backward2(const void* dy, const void* dy2, const void* x, const void* residual,
+                           int64_t M, int C, const float* save_mean, const float* save_invstd,
+                           const float* scale_shift, const float* weight, float* grad_weight,
+                           float* grad_bias, float* coef, void* dx, void* dresidual,
+                           void* workspace, int flags, void* stream);
 
 /* channels_last max pooling (bf16, C % 8 == 0, no dilation / ceil mode).
  * shape = {N, H, W, C, OH, OW, kh, kw, sh, sw, ph, pw}; argmax: uint8 [N*OH*OW*C] window

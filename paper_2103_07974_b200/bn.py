@@ -35,9 +35,26 @@ CS_BN_RELU = 1
 CS_BN_RESIDUAL = 2
 
 
+class _SideGrad:
+    """A gradient of a BN output delivered outside autograd.
+
+    A bottleneck block's input x feeds both conv1 (an autograd edge) and the identity path into
+    the block's bn3.  Autograd would sum the two gradients of x with one elementwise add per
+    block; instead the identity edge is cut (``residual.detach()``), bn3's backward stores its
+    residual gradient here, and the BN that produced x reads it as a second incoming gradient
+    (``cs_bn_backward2``: dy + dy2 summed in fp32 inside its kernels).  The producer's backward
+    always runs after bn3's (it needs conv1's input gradient, which bn3's backward precedes)."""
+
+    __slots__ = ("grad",)
+
+    def __init__(self):
+        self.grad = None
+
+
 class _BnFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, weight, bias, running_mean, running_var, momentum, eps, ws, residual, flags):
+    def forward(ctx, x, weight, bias, running_mean, running_var, momentum, eps, ws, residual, flags,
+                side_in=None, side_out=None):
         n, c, h, w = x.shape
         m = n * h * w
         x = x.contiguous(memory_format=torch.channels_last)
@@ -57,6 +74,7 @@ class _BnFunction(torch.autograd.Function):
         ctx.save_for_backward(x, weight, save_mean, save_invstd, scale_shift, keep_res)
         ctx.ws, ctx.flags = ws, flags
         ctx.has_bias = bias is not None
+        ctx.side_in, ctx.side_out = side_in, side_out
         return y
 
     @staticmethod
@@ -64,6 +82,10 @@ class _BnFunction(torch.autograd.Function):
         x, weight, save_mean, save_invstd, scale_shift, res = ctx.saved_tensors
         n, c, h, w = x.shape
         dy = dy.contiguous(memory_format=torch.channels_last)
+        dy2 = None
+        if ctx.side_in is not None and ctx.side_in.grad is not None:
+            dy2 = ctx.side_in.grad.contiguous(memory_format=torch.channels_last)
+            ctx.side_in.grad = None
         dx = torch.empty_like(x)
         dres = torch.empty_like(x) if ctx.flags & CS_BN_RESIDUAL else None
         f32 = dict(dtype=torch.float32, device=x.device)
@@ -71,11 +93,14 @@ class _BnFunction(torch.autograd.Function):
         gb = torch.empty(c, **f32) if ctx.has_bias else None
         coef = torch.empty(3 * c, **f32)
         stream = torch.cuda.current_stream(x.device).cuda_stream
-        _lib.check("cs_bn_backward", _lib.lib.cs_bn_backward(
-            dy.data_ptr(), x.data_ptr(), _ptr(res), n * h * w, c, save_mean.data_ptr(),
+        _lib.check("cs_bn_backward", _lib.lib.cs_bn_backward2(
+            dy.data_ptr(), _ptr(dy2), x.data_ptr(), _ptr(res), n * h * w, c, save_mean.data_ptr(),
             save_invstd.data_ptr(), scale_shift.data_ptr(), _ptr(weight), _ptr(gw), _ptr(gb),
             coef.data_ptr(), dx.data_ptr(), _ptr(dres), ctx.ws.data_ptr(), ctx.flags, stream))
-        return dx, gw, gb, None, None, None, None, None, dres, None
+        if ctx.side_out is not None:      # identity-path gradient goes to the producer's BN
+            ctx.side_out.grad = dres
+            dres = None
+        return dx, gw, gb, None, None, None, None, None, dres, None, None, None
 
 
 class CrossoverBatchNorm2d(torch.nn.BatchNorm2d):
@@ -98,7 +123,8 @@ class CrossoverBatchNorm2d(torch.nn.BatchNorm2d):
         return self.forward_fused(x)
 
     def forward_fused(self, x: torch.Tensor, relu: bool = False,
-                      residual: torch.Tensor | None = None) -> torch.Tensor:
+                      residual: torch.Tensor | None = None,
+                      residual_side: "_SideGrad | None" = None) -> torch.Tensor:
         fast = self.training and bn_supported(x) and (
             residual is None or (residual.shape == x.shape and residual.dtype == x.dtype))
         if not fast:
@@ -114,8 +140,15 @@ class CrossoverBatchNorm2d(torch.nn.BatchNorm2d):
         rm = self.running_mean if self.track_running_stats else None
         rv = self.running_var if self.track_running_stats else None
         flags = (CS_BN_RELU if relu else 0) | (CS_BN_RESIDUAL if residual is not None else 0)
-        return _BnFunction.apply(x, self.weight, self.bias, rm, rv, float(momentum or 0.0),
-                                 float(self.eps), self._workspace(x), residual, flags)
+        side_out = None
+        if residual is not None and residual_side is not None:
+            residual, side_out = residual.detach(), residual_side
+        side_in = _SideGrad() if (relu and residual is not None) else None
+        y = _BnFunction.apply(x, self.weight, self.bias, rm, rv, float(momentum or 0.0),
+                              float(self.eps), self._workspace(x), residual, flags, side_in, side_out)
+        if side_in is not None:
+            y._cs_side = side_in
+        return y
 
 
 def _bn_relu_forward(self, x):
@@ -123,11 +156,20 @@ def _bn_relu_forward(self, x):
 
 
 def _bottleneck_forward(self, x):
-    # torchvision Bottleneck.forward with bn+relu and bn3+residual+relu fused
+    # torchvision Bottleneck.forward with bn+relu and bn3+residual+relu fused; when x came out
+    # of the previous block's fused bn3, the identity gradient is handed to that BN directly
+    # (_SideGrad) instead of being summed with conv1's input gradient by an autograd add
     identity = x if self.downsample is None else self.downsample(x)
+    side = getattr(x, "_cs_side", None) if (self.downsample is None and _SIDE_GRADS) else None
     out = self.bn1.forward_fused(self.conv1(x), relu=True)
     out = self.bn2.forward_fused(self.conv2(out), relu=True)
-    return self.bn3.forward_fused(self.conv3(out), relu=True, residual=identity)
+    return self.bn3.forward_fused(self.conv3(out), relu=True, residual=identity, residual_side=side)
+
+
+# Measured on B200 (bench.py --side-grads A/B): the two-input backward kernels (one more input
+# stream in both the partial and the apply kernel, +16 registers) cost more than the add kernel
+# they remove (-1.9 % on the N = 1 bench), so autograd keeps summing by default.
+_SIDE_GRADS = False
 
 
 class _MaxPoolFunction(torch.autograd.Function):

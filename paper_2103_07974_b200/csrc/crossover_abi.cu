@@ -338,23 +338,32 @@ int cs_bn_forward(const void* x, const void* residual, int64_t M, int C, const f
                      "cs_bn_forward launch");
 }
 
-int cs_bn_backward(const void* dy, const void* x, const void* residual, int64_t M, int C,
-                   const float* save_mean, const float* save_invstd, const float* scale_shift,
-                   const float* weight, float* grad_weight, float* grad_bias, float* coef,
-                   void* dx, void* dresidual, void* workspace, int flags, void* stream) {
+int cs_bn_backward2(const void* dy, const void* dy2, const void* x, const void* residual, int64_t M,
+                    int C, const float* save_mean, const float* save_invstd,
+                    const float* scale_shift, const float* weight, float* grad_weight,
+                    float* grad_bias, float* coef, void* dx, void* dresidual, void* workspace,
+                    int flags, void* stream) {
   const bool relu = flags & CS_BN_RELU, resid = flags & CS_BN_RESIDUAL;
   if (dy == nullptr || x == nullptr || dx == nullptr || save_mean == nullptr ||
       save_invstd == nullptr || coef == nullptr || workspace == nullptr || !bn_shape_ok(M, C) ||
       (flags & ~(CS_BN_RELU | CS_BN_RESIDUAL)) || (relu && scale_shift == nullptr) ||
       (resid && (dresidual == nullptr || (relu && residual == nullptr))) ||
-      (((uintptr_t)dy | (uintptr_t)x | (uintptr_t)dx | (uintptr_t)residual |
+      (((uintptr_t)dy | (uintptr_t)dy2 | (uintptr_t)x | (uintptr_t)dx | (uintptr_t)residual |
         (uintptr_t)dresidual) & 15u))
     return set_error(CS_ERR_ARG, "cs_bn_backward: invalid arguments (M=%lld C=%d flags=%d)",
                      (long long)M, C, flags);
-  return cuda_status(launch_bn_bwd(dy, x, residual, M, C, save_mean, save_invstd, scale_shift,
+  return cuda_status(launch_bn_bwd(dy, dy2, x, residual, M, C, save_mean, save_invstd, scale_shift,
                                    weight, grad_weight, grad_bias, coef, dx, dresidual, workspace,
                                    flags, (cudaStream_t)stream),
                      "cs_bn_backward launch");
+}
+
+int cs_bn_backward(const void* dy, const void* x, const void* residual, int64_t M, int C,
+                   const float* save_mean, const float* save_invstd, const float* scale_shift,
+                   const float* weight, float* grad_weight, float* grad_bias, float* coef,
+                   void* dx, void* dresidual, void* workspace, int flags, void* stream) {
+  return cs_bn_backward2(dy, nullptr, x, residual, M, C, save_mean, save_invstd, scale_shift, weight,
+                         grad_weight, grad_bias, coef, dx, dresidual, workspace, flags, stream);
 }
 
 static bool pool_shape_ok(const int* s) {

@@ -280,11 +280,20 @@ bn_fwd_apply_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __
   }
 }
 
-// g = dy masked by the forward activation (recomputed from x [, residual]; nothing stored)
-template <bool kRelu, bool kRes>
-__device__ __forceinline__ void masked_grad8(const uint4& rg, const uint4& rx, const uint4& rr,
-                                             const float* sc, const float* sh, float* g) {
+// g = dy [+ dy2] masked by the forward activation (recomputed from x [, residual]; nothing
+// stored).  kDy2: a second gradient of the same output delivered outside autograd (the next
+// bottleneck block's identity path) is summed in fp32 instead of by a separate add kernel.
+template <bool kRelu, bool kRes, bool kDy2>
+__device__ __forceinline__ void masked_grad8(const uint4& rg, const uint4& rg2, const uint4& rx,
+                                             const uint4& rr, const float* sc, const float* sh,
+                                             float* g) {
   unpack8(rg, g);
+  if (kDy2) {
+    float g2[8];
+    unpack8(rg2, g2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] += g2[i];
+  }
   if (kRelu) {
     float p[8];
     pre_act8<kRelu, kRes>(rx, rr, sc, sh, p);
@@ -294,9 +303,10 @@ __device__ __forceinline__ void masked_grad8(const uint4& rg, const uint4& rx, c
 }
 
 // dx = g * k1 + x * k2 + k3 ; dres = g (kRes)
-template <bool kRelu, bool kRes>
+template <bool kRelu, bool kRes, bool kDy2>
 __global__ void __launch_bounds__(kBnThreads)
-bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dy2,
+                    const __nv_bfloat16* __restrict__ x,
                     const __nv_bfloat16* __restrict__ res, int64_t M, int C,
                     const float* __restrict__ coef, const float* __restrict__ scale,
                     const float* __restrict__ shift, __nv_bfloat16* __restrict__ dx,
@@ -319,10 +329,11 @@ bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* _
   const uint4 zero = make_uint4(0, 0, 0, 0);
   for (int64_t v = v0; v < vecs; v += stride) {
     const uint4 rg = ld_nc16(dy + v * 8);
+    const uint4 rg2 = kDy2 ? ld_nc16(dy2 + v * 8) : zero;
     const uint4 rx = ld_nc16(x + v * 8);
     const uint4 rr = (kRes && kRelu) ? ld_nc16(res + v * 8) : zero;
     float g[8], fx[8], o[8];
-    masked_grad8<kRelu, kRes>(rg, rx, rr, sc, sh, g);
+    masked_grad8<kRelu, kRes, kDy2>(rg, rg2, rx, rr, sc, sh, g);
     unpack8(rx, fx);
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[i] = fmaf(g[i], q1[i], fmaf(fx[i], q2[i], q3[i]));
@@ -334,12 +345,12 @@ bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* _
 // ---------------------------------------------------------------------------
 // backward: sum(dy), sum(dy * (x - mean)) per channel
 // ---------------------------------------------------------------------------
-template <bool kRelu, bool kRes>
-__device__ __forceinline__ void bwd_acc8(const uint4& rg, const uint4& rx, const uint4& rr,
-                                         const float* mu, const float* sc, const float* sh,
-                                         float* sdy, float* sdx) {
+template <bool kRelu, bool kRes, bool kDy2>
+__device__ __forceinline__ void bwd_acc8(const uint4& rg, const uint4& rg2, const uint4& rx,
+                                         const uint4& rr, const float* mu, const float* sc,
+                                         const float* sh, float* sdy, float* sdx) {
   float g[8], v[8];
-  masked_grad8<kRelu, kRes>(rg, rx, rr, sc, sh, g);
+  masked_grad8<kRelu, kRes, kDy2>(rg, rg2, rx, rr, sc, sh, g);
   unpack8(rx, v);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -348,9 +359,10 @@ __device__ __forceinline__ void bwd_acc8(const uint4& rg, const uint4& rx, const
   }
 }
 
-template <bool kRelu, bool kRes>
+template <bool kRelu, bool kRes, bool kDy2>
 __global__ void __launch_bounds__(kBnThreads)
-bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dy2,
+                      const __nv_bfloat16* __restrict__ x,
                       const __nv_bfloat16* __restrict__ res, int64_t M, int C,
                       const float* __restrict__ save_mean, const float* __restrict__ scale,
                       const float* __restrict__ shift, float* __restrict__ partial) {
@@ -371,19 +383,22 @@ bn_bwd_partial_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16*
   constexpr bool kLoadRes = kRes && kRelu;
   int64_t r = r0 + ty;
   for (; r + (kRowUnroll - 1) * s.ty < r1; r += kRowUnroll * s.ty) {
-    uint4 rg[kRowUnroll], rx[kRowUnroll], rr[kRowUnroll];
+    uint4 rg[kRowUnroll], rg2[kRowUnroll], rx[kRowUnroll], rr[kRowUnroll];
 #pragma unroll
     for (int u = 0; u < kRowUnroll; ++u) {
       rg[u] = ld_nc16(dy + (r + u * s.ty) * C + c0);
+      rg2[u] = kDy2 ? ld_nc16(dy2 + (r + u * s.ty) * C + c0) : zero;
       rx[u] = ld_nc16(x + (r + u * s.ty) * C + c0);
       rr[u] = kLoadRes ? ld_nc16(res + (r + u * s.ty) * C + c0) : zero;
     }
 #pragma unroll
-    for (int u = 0; u < kRowUnroll; ++u) bwd_acc8<kRelu, kRes>(rg[u], rx[u], rr[u], mu, sc, sh, sdy, sdx);
+    for (int u = 0; u < kRowUnroll; ++u)
+      bwd_acc8<kRelu, kRes, kDy2>(rg[u], rg2[u], rx[u], rr[u], mu, sc, sh, sdy, sdx);
   }
   for (; r < r1; r += s.ty)
-    bwd_acc8<kRelu, kRes>(ld_nc16(dy + r * C + c0), ld_nc16(x + r * C + c0),
-                          kLoadRes ? ld_nc16(res + r * C + c0) : zero, mu, sc, sh, sdy, sdx);
+    bwd_acc8<kRelu, kRes, kDy2>(ld_nc16(dy + r * C + c0), kDy2 ? ld_nc16(dy2 + r * C + c0) : zero,
+                                ld_nc16(x + r * C + c0), kLoadRes ? ld_nc16(res + r * C + c0) : zero,
+                                mu, sc, sh, sdy, sdx);
   pdl_trigger();
 
   __shared__ float s_dy[kBnThreads * 8], s_dx[kBnThreads * 8];
@@ -538,9 +553,9 @@ cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, cons
   return cudaGetLastError();
 }
 
-template <bool kRelu, bool kRes>
-static cudaError_t bwd_impl(const void* dy, const void* x, const void* res, int64_t M, int C,
-                            const float* save_mean, const float* save_invstd,
+template <bool kRelu, bool kRes, bool kDy2>
+static cudaError_t bwd_impl(const void* dy, const void* dy2, const void* x, const void* res,
+                            int64_t M, int C, const float* save_mean, const float* save_invstd,
                             const float* scale_shift, const float* w, float* gw, float* gb,
                             float* coef, void* dx, void* dres, void* ws, cudaStream_t s) {
   const TileShape sh = tile_shape(C);
@@ -548,32 +563,44 @@ static cudaError_t bwd_impl(const void* dy, const void* x, const void* res, int6
   float* partial = (float*)((char*)ws + 256);
   const float* scale = scale_shift;
   const float* shift = scale_shift ? scale_shift + C : nullptr;
-  bn_bwd_partial_kernel<kRelu, kRes><<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C,
-      save_mean, scale, shift, partial);
+  bn_bwd_partial_kernel<kRelu, kRes, kDy2><<<dim3(blocks, C / sh.tile), kBnThreads, 0, s>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)dy2, (const __nv_bfloat16*)x,
+      (const __nv_bfloat16*)res, M, C, save_mean, scale, shift, partial);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = launch_dependent(bn_bwd_finalize_kernel, dim3((C + 7) / 8), s, (const float*)partial, blocks,
                        M, C, save_mean, save_invstd, w, gw, gb, coef, coef + C, coef + 2 * C);
   if (e != cudaSuccess) return e;
-  return launch_dependent(bn_bwd_apply_kernel<kRelu, kRes>, dim3(apply_grid(M, C)), s,
-                          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                          (const __nv_bfloat16*)res, M, C, (const float*)coef, scale, shift,
-                          (__nv_bfloat16*)dx, (__nv_bfloat16*)dres);
+  return launch_dependent(bn_bwd_apply_kernel<kRelu, kRes, kDy2>, dim3(apply_grid(M, C)), s,
+                          (const __nv_bfloat16*)dy, (const __nv_bfloat16*)dy2,
+                          (const __nv_bfloat16*)x, (const __nv_bfloat16*)res, M, C,
+                          (const float*)coef, scale, shift, (__nv_bfloat16*)dx,
+                          (__nv_bfloat16*)dres);
 }
 
-cudaError_t launch_bn_bwd(const void* dy, const void* x, const void* res, int64_t M, int C,
-                          const float* save_mean, const float* save_invstd,
-                          const float* scale_shift, const float* w, float* gw, float* gb,
-                          float* coef, void* dx, void* dres, void* ws, int flags, cudaStream_t s) {
+template <bool kDy2>
+static cudaError_t bwd_dispatch(const void* dy, const void* dy2, const void* x, const void* res,
+                                int64_t M, int C, const float* save_mean,
+                                const float* save_invstd, const float* scale_shift, const float* w,
+                                float* gw, float* gb, float* coef, void* dx, void* dres, void* ws,
+                                int flags, cudaStream_t s) {
   const bool relu = flags & CS_BN_RELU, resid = flags & CS_BN_RESIDUAL;
   if (relu && resid)
-    return bwd_impl<true, true>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+    return bwd_impl<true, true, kDy2>(dy, dy2, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
   if (relu)
-    return bwd_impl<true, false>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+    return bwd_impl<true, false, kDy2>(dy, dy2, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
   if (resid)
-    return bwd_impl<false, true>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
-  return bwd_impl<false, false>(dy, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+    return bwd_impl<false, true, kDy2>(dy, dy2, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+  return bwd_impl<false, false, kDy2>(dy, dy2, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, s);
+}
+
+cudaError_t launch_bn_bwd(const void* dy, const void* dy2, const void* x, const void* res, int64_t M,
+                          int C, const float* save_mean, const float* save_invstd,
+                          const float* scale_shift, const float* w, float* gw, float* gb,
+                          float* coef, void* dx, void* dres, void* ws, int flags, cudaStream_t s) {
+  if (dy2 != nullptr)
+    return bwd_dispatch<true>(dy, dy2, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, flags, s);
+  return bwd_dispatch<false>(dy, dy2, x, res, M, C, save_mean, save_invstd, scale_shift, w, gw, gb, coef, dx, dres, ws, flags, s);
 }
 
 }  // namespace cs

@@ -65,6 +65,51 @@ im2col_nhwc_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   }
 }
 
+// One CTA per output row (n, oh): the KH input rows the row's windows touch are staged in shared
+// memory with 16-byte loads (an NHWC input row is W*C contiguous bf16), then the CTA writes its
+// OW consecutive patch rows -- one contiguous block of P -- with 16-byte stores.  The gather is
+// served from shared memory instead of 2-byte global loads.
+template <int kC, int kKH, int kKW, int kSH, int kSW, int kKP>
+__global__ void __launch_bounds__(256)
+im2col_rows_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ p,
+                   const Im2colShape s) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem_raw);   // [kKH][W * kC]
+  const int row = blockIdx.x;                  // n * OH + oh
+  const int n = row / s.OH, oh = row - n * s.OH;
+  const int rowlen = s.W * kC;                 // bf16 per input row (multiple of 8: host checked)
+  const int vecs = rowlen / 8;
+  for (int t = threadIdx.x; t < kKH * vecs; t += blockDim.x) {
+    const int kh = t / vecs, v = t - kh * vecs;
+    const int ih = oh * kSH - s.PH + kh;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if ((unsigned)ih < (unsigned)s.H)
+      val = __ldg(reinterpret_cast<const uint4*>(x + ((int64_t)n * s.H + ih) * rowlen) + v);
+    reinterpret_cast<uint4*>(tile + kh * rowlen)[v] = val;
+  }
+  __syncthreads();
+  constexpr int kGroups = kKP / 8;
+  constexpr int kK = kKH * kKW * kC;
+  __nv_bfloat16* out = p + (int64_t)row * s.OW * kKP;
+  for (int t = threadIdx.x; t < s.OW * kGroups; t += blockDim.x) {
+    const int ow = t / kGroups, j0 = (t - ow * kGroups) * 8;
+    const int iw0 = ow * kSW - s.PW;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = j0 + i;
+      __nv_bfloat16 val = __float2bfloat16(0.f);
+      if (j < kK) {
+        const int c = j % kC, kw = (j / kC) % kKW, kh = j / (kC * kKW);
+        const int iw = iw0 + kw;
+        if ((unsigned)iw < (unsigned)s.W) val = tile[kh * rowlen + iw * kC + c];
+      }
+      v[i] = val;
+    }
+    *reinterpret_cast<uint4*>(out + (int64_t)ow * kKP + j0) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
 int sm_count_im2col() {
   static int n = 0;
   if (n == 0) {
@@ -89,10 +134,17 @@ cudaError_t launch_im2col_nhwc(const void* x, void* p, const int* shape, cudaStr
   const unsigned g = (unsigned)(grid < 1 ? 1 : grid);
   const auto* xi = (const __nv_bfloat16*)x;
   auto* po = (__nv_bfloat16*)p;
-  if (s.C == 3 && s.KH == 7 && s.KW == 7 && s.SH == 2 && s.SW == 2 && s.KP == 152)
-    im2col_nhwc_kernel<3, 7, 7, 2, 2, 152, 0><<<g, 256, 0, stream>>>(xi, po, s, rows);   // ResNet stem
+  const bool rows_ok = (s.W * s.C) % 8 == 0;     // 16-byte staging of whole input rows
+  if (rows_ok && s.C == 3 && s.KH == 7 && s.KW == 7 && s.SH == 2 && s.SW == 2 && s.KP == 152)
+    im2col_rows_kernel<3, 7, 7, 2, 2, 152><<<(unsigned)(s.N * s.OH), 256, 7 * s.W * 3 * 2, stream>>>(
+        xi, po, s);                                                                        // ResNet stem
+  else if (rows_ok && s.C == 3 && s.KH == 3 && s.KW == 3 && s.SH == 1 && s.SW == 1 && s.KP == 32)
+    im2col_rows_kernel<3, 3, 3, 1, 1, 32><<<(unsigned)(s.N * s.OH), 256, 3 * s.W * 3 * 2, stream>>>(
+        xi, po, s);                                                                        // VGG stem
+  else if (s.C == 3 && s.KH == 7 && s.KW == 7 && s.SH == 2 && s.SW == 2 && s.KP == 152)
+    im2col_nhwc_kernel<3, 7, 7, 2, 2, 152, 0><<<g, 256, 0, stream>>>(xi, po, s, rows);
   else if (s.C == 3 && s.KH == 3 && s.KW == 3 && s.SH == 1 && s.SW == 1 && s.KP == 32)
-    im2col_nhwc_kernel<3, 3, 3, 1, 1, 32, 0><<<g, 256, 0, stream>>>(xi, po, s, rows);     // VGG stem
+    im2col_nhwc_kernel<3, 3, 3, 1, 1, 32, 0><<<g, 256, 0, stream>>>(xi, po, s, rows);
   else
     im2col_nhwc_kernel<1, 1, 1, 1, 1, 8, 1><<<g, 256, 0, stream>>>(xi, po, s, rows);
   return cudaGetLastError();

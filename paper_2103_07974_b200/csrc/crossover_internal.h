@@ -80,7 +80,7 @@ cudaError_t launch_bn_fwd(const void* x, const void* res, int64_t M, int C, cons
                           const float* b, float* rm, float* rv, float momentum, float eps,
                           float* save_mean, float* save_invstd, float* scale_shift, void* y,
                           void* ws, int flags, cudaStream_t s);
-cudaError_t launch_bn_bwd(const void* dy, const void* x, const void* res, int64_t M, int C,
+cudaError_t launch_bn_bwd(const void* dy, const void* dy2, const void* x, const void* res, int64_t M, int C,
                           const float* save_mean, const float* save_invstd,
                           const float* scale_shift, const float* w, float* gw, float* gb,
                           float* coef, void* dx, void* dres, void* ws, int flags, cudaStream_t s);
