@@ -143,8 +143,8 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
                 "frac": round(k2["GB/s"] / hbm_peak, 4),
                 "traffic": ncu_traffic(f"k2_update/{model}/ce_w{sync.ranks}/momentum"),
                 "note": ("live: the shard K2 waits for SM slots held by the other app's "
-                         "convolutions (it is a ~40 us kernel alone, 0.86 of the measured peak "
-                         "at W = 4 in profiles/r01_shard_kernels_ncu.md)"),
+                         "convolutions; alone the same kernel runs at 0.91 (W = 2) / 0.86 (W = 4) "
+                         "of the measured peak (profiles/r01_shard_kernels_ncu.md)"),
                 "peak_kind": peak_kind, "bytes_per_launch": sync.k2_bytes("ce"),
                 "transport": {"engine": "copy engines (cudaMemcpyAsync peer pulls, no SM)",
                               "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
