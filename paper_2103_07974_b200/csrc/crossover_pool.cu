@@ -300,6 +300,59 @@ maxpool_k3s2_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __r
   }
 }
 
+// Backward of the stem pool for even H, W with OH = H/2, OW = W/2: one thread per 2x2 input
+// block (2a..2a+1, 2b..2b+1) x 8 channels.  The block's 4 dx vectors are covered by exactly the
+// windows (a, b), (a, b+1), (a+1, b), (a+1, b+1), so every window's dy / argmax is loaded once
+// instead of ~2.25 times; window offsets of the 4 positions are compile-time constants.
+template <int kCV>
+__global__ void __launch_bounds__(128)
+maxpool_k3s2_bwd_2x2_kernel(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
+                            __nv_bfloat16* __restrict__ dx, PoolShape s) {
+  const int row = blockIdx.x;                 // n * OH + a
+  const int n = row / s.OH, a = row - n * s.OH;
+  for (int v = threadIdx.x; v < s.OW * kCV; v += blockDim.x) {
+    const int b = v / kCV, c8 = v % kCV;
+    uint4 rg[4];
+    uint2 ra[4];
+    bool use[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {               // q = 2 * dh + dw: window (a + dh, b + dw)
+      const int oh = a + (q >> 1), ow = b + (q & 1);
+      use[q] = oh < s.OH && ow < s.OW;
+      const int64_t o = (((int64_t)n * s.OH + oh) * s.OW + ow) * kCV + c8;
+      rg[q] = use[q] ? __ldg(reinterpret_cast<const uint4*>(dy + o * 8)) : make_uint4(0, 0, 0, 0);
+      ra[q] = use[q] ? __ldg(reinterpret_cast<const uint2*>(arg + o * 8)) : make_uint2(0, 0);
+    }
+    float g[4][8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) unpack8p(rg[q], g[q]);
+    // position p = 2 * di + dj (input (2a + di, 2b + dj)); for window q its offset in the 3x3
+    // window is (di - 2*(q>>1) + 1) * 3 + (dj - 2*(q&1) + 1) when inside, else not covered
+#pragma unroll
+    for (int pos = 0; pos < 4; ++pos) {
+      const int di = pos >> 1, dj = pos & 1;
+      float acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = di - 2 * (q >> 1) + 1, c = dj - 2 * (q & 1) + 1;
+        if (r < 0 || r > 2 || c < 0 || c > 2) continue;          // compile-time after unrolling
+        if (!use[q]) continue;
+        const uint32_t me = (uint32_t)(r * 3 + c);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t word = k < 4 ? ra[q].x : ra[q].y;
+          if (((word >> (8 * (k & 3))) & 0xffu) == me) acc[k] += g[q][k];
+        }
+      }
+      const int ih = 2 * a + di, iw = 2 * b + dj;
+      const int64_t out = (((int64_t)n * s.H + ih) * s.W + iw) * kCV + c8;
+      *reinterpret_cast<uint4*>(dx + out * 8) = pack8p(acc);
+    }
+  }
+}
+
 static bool stem_pool(const PoolShape& s) {
   return s.kh == 3 && s.kw == 3 && s.sh == 2 && s.sw == 2 && s.ph == 1 && s.pw == 1 && s.C == 64;
 }
@@ -335,7 +388,10 @@ cudaError_t launch_maxpool_bwd(const void* dy, const void* arg, void* dx, const 
   PoolShape s{shape[0], shape[1], shape[2], shape[3], shape[4], shape[5],
               shape[6], shape[7], shape[8], shape[9], shape[10], shape[11]};
   const int64_t total = (int64_t)s.N * s.H * s.W * (s.C / 8);
-  if (stem_pool(s))
+  if (stem_pool(s) && s.H == 2 * s.OH && s.W == 2 * s.OW)
+    maxpool_k3s2_bwd_2x2_kernel<8><<<(unsigned)(s.N * s.OH), 128, 0, st>>>(
+        (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
+  else if (stem_pool(s))
     maxpool_k3s2_bwd_kernel<8><<<(unsigned)(s.N * s.H), 128, 0, st>>>(
         (const __nv_bfloat16*)dy, (const uint8_t*)arg, (__nv_bfloat16*)dx, s);
   else if ((int64_t)s.N * s.H * s.W * s.C < INT32_MAX)

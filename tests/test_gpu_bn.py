@@ -168,6 +168,7 @@ def test_fused_resnet_no_less_accurate_than_aten(cuda_device):
 
 
 @pytest.mark.parametrize("shape,k,s,p", [((8, 64, 112, 112), 3, 2, 1), ((2, 64, 9, 7), 3, 2, 1),
+                                         ((2, 64, 10, 12), 3, 2, 1),
                                          ((4, 16, 9, 7), 3, 2, 1),
                                          ((2, 8, 10, 10), 2, 2, 0), ((3, 24, 11, 13), 3, 1, 1)])
 def test_maxpool_matches_aten_exactly(cuda_device, shape, k, s, p):
