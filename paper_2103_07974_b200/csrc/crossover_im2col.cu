@@ -90,23 +90,29 @@ im2col_rows_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   __syncthreads();
   constexpr int kGroups = kKP / 8;
   constexpr int kK = kKH * kKW * kC;
+  constexpr int kRowsPerPass = 256 / kGroups;    // blockDim = kGroups * kRowsPerPass (host)
   __nv_bfloat16* out = p + (int64_t)row * s.OW * kKP;
-  for (int t = threadIdx.x; t < s.OW * kGroups; t += blockDim.x) {
-    const int ow = t / kGroups, j0 = (t - ow * kGroups) * 8;
+  // each thread owns one fixed 8-column group of every patch row it writes: the (kh, kw, c)
+  // decomposition of its 8 columns is done once, the row loop is a shared-memory gather
+  const int g = threadIdx.x % kGroups, r0 = threadIdx.x / kGroups;
+  if (r0 >= kRowsPerPass) return;
+  int off[8], kwv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = g * 8 + i;
+    const int c = j % kC, kw = (j / kC) % kKW, kh = j / (kC * kKW);
+    off[i] = j < kK ? kh * rowlen + kw * kC + c : -1;
+    kwv[i] = j < kK ? kw : -1 - s.W;              // never in range for padding columns
+  }
+  for (int ow = r0; ow < s.OW; ow += kRowsPerPass) {
     const int iw0 = ow * kSW - s.PW;
     __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int j = j0 + i;
-      __nv_bfloat16 val = __float2bfloat16(0.f);
-      if (j < kK) {
-        const int c = j % kC, kw = (j / kC) % kKW, kh = j / (kC * kKW);
-        const int iw = iw0 + kw;
-        if ((unsigned)iw < (unsigned)s.W) val = tile[kh * rowlen + iw * kC + c];
-      }
-      v[i] = val;
+      const int iw = iw0 + kwv[i];
+      v[i] = (unsigned)iw < (unsigned)s.W ? tile[off[i] + iw0 * kC] : __float2bfloat16(0.f);
     }
-    *reinterpret_cast<uint4*>(out + (int64_t)ow * kKP + j0) = *reinterpret_cast<const uint4*>(v);
+    *reinterpret_cast<uint4*>(out + (int64_t)ow * kKP + g * 8) = *reinterpret_cast<const uint4*>(v);
   }
 }
 
@@ -136,10 +142,10 @@ cudaError_t launch_im2col_nhwc(const void* x, void* p, const int* shape, cudaStr
   auto* po = (__nv_bfloat16*)p;
   const bool rows_ok = (s.W * s.C) % 8 == 0;     // 16-byte staging of whole input rows
   if (rows_ok && s.C == 3 && s.KH == 7 && s.KW == 7 && s.SH == 2 && s.SW == 2 && s.KP == 152)
-    im2col_rows_kernel<3, 7, 7, 2, 2, 152><<<(unsigned)(s.N * s.OH), 256, 7 * s.W * 3 * 2, stream>>>(
+    im2col_rows_kernel<3, 7, 7, 2, 2, 152><<<(unsigned)(s.N * s.OH), 19 * (256 / 19), 7 * s.W * 3 * 2, stream>>>(
         xi, po, s);                                                                        // ResNet stem
   else if (rows_ok && s.C == 3 && s.KH == 3 && s.KW == 3 && s.SH == 1 && s.SW == 1 && s.KP == 32)
-    im2col_rows_kernel<3, 3, 3, 1, 1, 32><<<(unsigned)(s.N * s.OH), 256, 3 * s.W * 3 * 2, stream>>>(
+    im2col_rows_kernel<3, 3, 3, 1, 1, 32><<<(unsigned)(s.N * s.OH), 4 * (256 / 4), 3 * s.W * 3 * 2, stream>>>(
         xi, po, s);                                                                        // VGG stem
   else if (s.C == 3 && s.KH == 7 && s.KW == 7 && s.SH == 2 && s.SW == 2 && s.KP == 152)
     im2col_nhwc_kernel<3, 7, 7, 2, 2, 152, 0><<<g, 256, 0, stream>>>(xi, po, s, rows);
