@@ -11,7 +11,8 @@ with 3 input channels it pads the input and falls back to sm80-era fprop / wgrad
 
 The input gradient is not formed: the stem's input is the data.  The weight keeps its
 [O, C, KH, KW] fp32 parameter; the GEMMs run in bf16 with fp32 accumulation like autocast's
-convolution, so the result matches `F.conv2d` to bf16 rounding (tests/test_gpu_bn.py).
+convolution (the weight gradient is returned in fp32 straight from the accumulator), so the
+result matches `F.conv2d` to bf16 rounding (tests/test_gpu_bn.py).
 """
 
 from __future__ import annotations
@@ -70,7 +71,8 @@ class _StemGemm(torch.autograd.Function):
         dy = dy.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
         dym = dy.permute(0, 2, 3, 1).reshape(-1, o)
         with torch.autocast("cuda", enabled=False):
-            dwm = dym.t() @ p
+            # fp32 output straight from the bf16 GEMM's fp32 accumulator (no bf16 rounding of dW)
+            dwm = torch.mm(dym.t(), p, out_dtype=torch.float32)
             dw = dwm[:, :k].reshape(o, kh, kw, c).permute(0, 3, 1, 2).to(wdt)
             db = dym.sum(0, dtype=torch.float32).to(wdt) if has_bias else None
         return None, dw, db, None, None

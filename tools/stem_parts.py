@@ -38,10 +38,13 @@ def main():
     t_im = timeit(lambda: _lib.lib.cs_im2col_nhwc(x.data_ptr(), p.data_ptr(), shape, st))
     t_f = timeit(lambda: torch.mm(p, wm.t(), out=y))
     t_w = timeit(lambda: dy.t() @ p)
+    t_w2 = timeit(lambda: p.t() @ dy)
+    t_w3 = timeit(lambda: torch.mm(dy.t(), p, out_dtype=torch.float32) if hasattr(torch.mm, "__call__") else None)
     gb = lambda b, t: b / (t / 1e3) / 1e9  # noqa: E731
     print(f"im2col {t_im:.3f} ms ({gb(p.numel() * 2 + x.numel() * 2, t_im):.0f} GB/s)")
     print(f"fwd GEMM {t_f:.3f} ms ({gb(p.numel() * 2 + y.numel() * 2, t_f):.0f} GB/s)")
     print(f"wgrad GEMM {t_w:.3f} ms ({gb(p.numel() * 2 + dy.numel() * 2, t_w):.0f} GB/s)")
+    print(f"wgrad GEMM as P^T.dy {t_w2:.3f} ms; fp32-out variant {t_w3:.3f} ms")
 
 
 if __name__ == "__main__":
