@@ -397,17 +397,23 @@ def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
     the timed crossover arm then runs the chosen one and the sequential arm the full-grid P2P
     kernel.  Returns (crossover mode, sequential mode, tuner summary or None)."""
     from paper_2103_07974_b200.errors import ConfigError
-    from paper_2103_07974_b200.scheduler import Policy, _TransportTuner
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
 
     if h.world < 2 or sm not in ("p2p", "ce", "auto"):
         return sm, sm, None
     try:
-        n_cal = _TransportTuner.MIN_BUDGET if sm == "auto" else int(os.environ.get("CS_PROBE_ROTATIONS", "1"))
-        probe = timed_run(h, base, Policy.CROSSOVER, 0, n_cal, sync_mode=sm, comm_priority=prio,
-                          time_kernels=False)
-        tuner = probe["sched"].tuner
-        if sm == "auto" and tuner is not None and tuner.active:
-            return tuner.choice, "p2p", tuner.summary()
+        sched = CrossoverScheduler(Policy.CROSSOVER, comm=h.comm, sync_mode=sm, comm_priority=prio,
+                                   p2p_ctas=P2P_CTAS, barrier=BARRIER, record_spans=False)
+        for a in base:
+            sched.register(dataclasses.replace(a, iterations=9))
+        summary = sched.calibrate(4) if sm == "auto" else None
+        while sched.step():
+            pass
+        sched.drain()
+        sched.close()
+        h.barrier()
+        if summary is not None and summary["active"]:
+            return summary["choice"], "p2p", summary
         return sm, sm, None
     except ConfigError as exc:
         if h.rank == 0:

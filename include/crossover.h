@@ -48,7 +48,7 @@ extern "C" {
 #define CS_API
 #endif
 
-#define CS_ABI_VERSION 1
+#define CS_ABI_VERSION 2
 #define CS_ERR_ARG (-1)
 #define CS_ERR_NCCL_BASE 10000
 #define CS_NCCL_UNIQUE_ID_BYTES 128
@@ -90,19 +90,9 @@ typedef struct cs_sgd_hyper {
 CS_API int cs_abi_version(void);
 CS_API const char* cs_last_error(void);
 
-/* Kernel implementation used by cs_pack / cs_unpack_sgd (process-wide).
- * CS_VARIANT_REGISTER (default): one CTA per chunk, 128-bit register loads/stores.
- * CS_VARIANT_TMA: persistent CTAs streaming through a shared-memory stage ring
- * with cp.async.bulk loads (+ bulk stores in K1) and mbarriers.
- * Both produce bit-identical results. */
-enum { CS_VARIANT_TMA = 0, CS_VARIANT_REGISTER = 1 };
-CS_API int cs_set_kernel_variant(int variant);
-CS_API int cs_get_kernel_variant(void);
-/* Launch-shape knobs of the TMA variant (0 restores the built-in heuristic):
- * "k1_chunk", "k2_chunk" (fp32 elements per stream per stage), "k2_stages",
- * "ctas_per_sm"; of the register variant: "reg_shape" (0..4: unroll x CTAs/SM); of the
- * fused P2P kernel: "p2p_ctas" (persistent grid cap, 0 = default 2 CTAs per SM); of
- * the register K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
+/* Launch-shape knobs (0 restores the built-in default): of the register K1/K2 "reg_shape"
+ * (0..4: unroll x CTAs/SM); of the fused P2P kernel: "p2p_ctas" (persistent grid cap, 0 = default
+ * 2 CTAs per SM); of the K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
  * sync that overlaps another app's compute with slack can trade speed for fewer SMs; of the BN
  * kernels: "bn_no_pdl" (1 = launch finalize / apply without programmatic dependent launch),
  * "bn_ctas_per_sm" (row-block CTAs per SM of the partial kernels, 0 = 3; changes the partial
@@ -151,6 +141,12 @@ CS_API size_t cs_gradient_stats_workspace_bytes(int64_t numel);
 CS_API int cs_gradient_stats(const float* data, int64_t numel, double* out,
                       void* workspace, void* stream);
 
+/* A compute phase of known device duration: one thread on one SM spins on %globaltimer for `ns`
+ * nanoseconds (no memory traffic).  The fixed compute kernel of the comm/comp sweep and of the
+ * timing-level schedule tests (reference: JobProfile.forward_time / backward_time as durations,
+ * workload.py:43-56).  At most 60 s. */
+CS_API int cs_spin_ns(uint64_t ns, void* stream);
+
 /* Collective-fused update over NVLink peer memory (replaces reduce-scatter + K2 +
  * all-gather).  For this rank's shard of an app's flat parameters:
  *   acc = 0 + src[0][k] + ... + src[W-1][k]   (rank order == equivalence.py:156-159)
@@ -183,7 +179,8 @@ CS_API int cs_ipc_close_handle(void* ptr);
  * local or peer-mapped (IPC) device memory, so a pull from a peer crosses NVLink without
  * occupying any SM -- the transport of the "ce" sync mode. */
 CS_API int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream);
-/* Cross-rank barrier without SMs: stream memory operations on IPC-mapped uint32 flag arrays.
+/* Cross-rank barrier without SMs: stream memory operations on uint32 flag arrays (device memory
+ * mapped over IPC, or host shared memory registered with cs_host_register).
  * Rank r writes `epoch` into slot r of every peer's array (peer_flags[p] = rank p's array as
  * mapped here; a system-scope fence orders all earlier work of the stream before each write),
  * then the stream waits until every peer's slot in its own array (local_flags) is >= epoch
@@ -191,6 +188,12 @@ CS_API int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream)
  * 1-element NCCL all-reduce barriers of the p2p / ce transports, whose kernels need a free SM
  * while the other app's GEMMs occupy them. */
 CS_API int cs_stream_memops_supported(void);
+/* Page-locked, device-mapped host memory for the flag arrays (cudaHostRegister, mapped +
+ * portable).  The p2p / ce transports keep their barrier flags in one host shared-memory segment
+ * mapped by every rank of the node, so a host can release every rank's pending waits on failure
+ * (write a final epoch into the segment) without issuing any GPU work. */
+CS_API int cs_host_register(void* ptr, size_t bytes, void** dev_ptr);
+CS_API int cs_host_unregister(void* ptr);
 CS_API int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, int nranks,
                            uint32_t epoch, void* stream);
 

@@ -21,8 +21,6 @@ CS_NCCL_UNIQUE_ID_BYTES = 128
 CS_MAX_SOURCES = 8
 CS_ROUND_REFERENCE = 0
 CS_ROUND_TORCH = 1
-CS_VARIANT_TMA = 0
-CS_VARIANT_REGISTER = 1
 
 # numpy mirrors of the C descriptor structs (layouts asserted below)
 PACK_DESC = np.dtype([("src", "<u8"), ("dst", "<u8"), ("numel", "<i8")])
@@ -58,8 +56,6 @@ class CrossoverLibError(RuntimeError):
 EXPORTS = {
     "cs_abi_version": ([], ctypes.c_int),
     "cs_last_error": ([], ctypes.c_char_p),
-    "cs_set_kernel_variant": ([ctypes.c_int], ctypes.c_int),
-    "cs_get_kernel_variant": ([], ctypes.c_int),
     "cs_tune": ([ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
     "cs_stream_create": ([ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "cs_stream_destroy": ([ctypes.c_void_p], ctypes.c_int),
@@ -73,6 +69,7 @@ EXPORTS = {
     "cs_pack": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "cs_unpack_sgd": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                        ctypes.c_void_p, ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),
+    "cs_spin_ns": ([ctypes.c_uint64, ctypes.c_void_p], ctypes.c_int),
     "cs_gradient_stats_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "cs_gradient_stats": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p], ctypes.c_int),
@@ -85,6 +82,8 @@ EXPORTS = {
     "cs_ipc_close_handle": ([ctypes.c_void_p], ctypes.c_int),
     "cs_copy_async": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p], ctypes.c_int),
     "cs_stream_memops_supported": ([], ctypes.c_int),
+    "cs_host_register": ([ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cs_host_unregister": ([ctypes.c_void_p], ctypes.c_int),
     "cs_flag_barrier": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
                          ctypes.c_void_p], ctypes.c_int),
     "cs_bn_workspace_bytes": ([ctypes.c_int64, ctypes.c_int], ctypes.c_size_t),
@@ -135,7 +134,7 @@ def _load() -> ctypes.CDLL:
 
 
 lib = _load()
-assert lib.cs_abi_version() == 1, "libcrossover.so ABI version mismatch"
+assert lib.cs_abi_version() == 2, "libcrossover.so ABI version mismatch"
 
 
 def check(fn: str, rc: int) -> None:
@@ -168,15 +167,11 @@ def gradient_stats(data: int, numel: int, out: int, workspace: int, stream: int)
     check("cs_gradient_stats", lib.cs_gradient_stats(data, numel, out, workspace, stream))
 
 
-def set_kernel_variant(variant: int) -> None:
-    """Select the K1/K2 implementation (CS_VARIANT_TMA or CS_VARIANT_REGISTER)."""
-    check("cs_set_kernel_variant", lib.cs_set_kernel_variant(variant))
-
-
-def kernel_variant() -> int:
-    return int(lib.cs_get_kernel_variant())
-
-
 def tune(key: str, value: int) -> None:
-    """Launch-shape knob of the TMA kernels (see include/crossover.h cs_tune)."""
+    """Launch-shape knob (see include/crossover.h cs_tune)."""
     check("cs_tune", lib.cs_tune(key.encode(), value))
+
+
+def spin_ns(ns: int, stream: int) -> None:
+    """Enqueue a compute phase of `ns` nanoseconds of device time (cs_spin_ns)."""
+    check("cs_spin_ns", lib.cs_spin_ns(int(ns), stream))

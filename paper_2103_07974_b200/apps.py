@@ -61,6 +61,7 @@ __all__ = [
     "bert_app",
     "synthetic_image_batches",
     "synthetic_app",
+    "fixed_time_app",
 ]
 
 
@@ -431,3 +432,61 @@ def synthetic_app(job_id: str, bucket_bytes: int, iterations: int, device: torch
     flat_params = _flatten(list(model.weights), flat)
     return App(job_id, model, loss_fn, lambda t, w: (), sgd, iterations, samples_per_batch=1,
                flat_params=flat_params)
+
+
+# ---------------------------------------------------------------------------
+# apps of known compute duration (timing-level schedule tests, comm/comp sweeps)
+# ---------------------------------------------------------------------------
+class _FixedTimePhase(torch.autograd.Function):
+    """Forward and backward that each take a fixed device time (cs_spin_ns) and hand back a
+    preallocated gradient: the app's compute is exactly `forward_ns + backward_ns` of device time
+    on one SM, with no memory traffic, so measured schedules can be compared with the reference's
+    recurrences in its own units (JobProfile.forward_time / backward_time, workload.py:43-56)."""
+
+    @staticmethod
+    def forward(ctx, weight, forward_ns, backward_ns, grad):
+        from . import _lib
+
+        _lib.spin_ns(forward_ns, torch.cuda.current_stream(weight.device).cuda_stream)
+        ctx.backward_ns, ctx.grad = backward_ns, grad
+        return weight.new_zeros(())
+
+    @staticmethod
+    def backward(ctx, _dloss):
+        from . import _lib
+
+        _lib.spin_ns(ctx.backward_ns, torch.cuda.current_stream(ctx.grad.device).cuda_stream)
+        return ctx.grad, None, None, None
+
+
+class _FixedTimeModel(torch.nn.Module):
+    def __init__(self, numel: int, device, seed: int):
+        super().__init__()
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        base = min(numel, 1 << 20)
+        reps = (numel + base - 1) // base
+
+        def tile(scale):   # small seeded block on the host, tiled on the device
+            return (torch.randn(base, generator=g) * scale).to(device).repeat(reps)[:numel].clone()
+
+        self.weight = torch.nn.Parameter(tile(0.01))
+        self.grad = tile(1e-3)      # the gradient K2 consumes every iteration (fixed address)
+
+
+def fixed_time_app(job_id: str, forward_ns: int, backward_ns: int, bucket_bytes: int, iterations: int,
+                   device: torch.device, seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-3, momentum=0.9),
+                   flat=False, samples_per_batch: int = 1) -> App:
+    """An app whose forward / backward take `forward_ns` / `backward_ns` of device time and whose
+    fused gradient is `bucket_bytes` of fp32 (one tensor).  The sync is the real one (K1 / NVLink
+    transport / K2 over the bucket), so its duration is dialed by the bucket size the way
+    cli._payload_for_ratio (cli.py:79-98) dials the payload against a fixed compute time."""
+    numel = max(1, int(bucket_bytes) // 4)
+    model = _FixedTimeModel(numel, device, seed)
+    flat_params = _flatten([model.weight], flat)
+    fwd, bwd = int(forward_ns), int(backward_ns)
+
+    def loss_fn(m, batch):
+        return _FixedTimePhase.apply(m.weight, fwd, bwd, m.grad)
+
+    return App(job_id, model, loss_fn, lambda t, w: (), sgd, iterations,
+               params=[model.weight], samples_per_batch=samples_per_batch, flat_params=flat_params)

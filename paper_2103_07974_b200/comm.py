@@ -33,6 +33,7 @@ __all__ = [
     "comm_comp_ratio",
     "allreduce_bus_bytes",
     "NcclCommunicator",
+    "PeerGroup",
     "NVLINK5_GBPS",
 ]
 
@@ -171,6 +172,8 @@ class NcclCommunicator:
         _lib.check("cs_nccl_init", _lib.lib.cs_nccl_init(
             ctypes.byref(self.handle), world, rank, uid, min_ctas, max_ctas))
 
+    has_collectives = True
+
     @property
     def active(self) -> bool:
         return self.world > 1
@@ -204,3 +207,47 @@ class NcclCommunicator:
         if self.world > 1 and self.handle:
             self._lib.check("cs_nccl_destroy", self._lib.lib.cs_nccl_destroy(self.handle))
             self.handle = ctypes.c_void_p(None)
+
+
+class PeerGroup:
+    """The ranks of the peer-memory transports without an NCCL communicator.
+
+    The ``p2p`` and ``ce`` syncs move every byte themselves (NVLink loads / stores or copy-engine
+    pulls from IPC-mapped peer buffers) and order the ranks with SM-free flag barriers, so they need
+    only the process group's rank and size -- torch.distributed (any backend) for the one-off
+    exchange of IPC handles.  This is also what lets W ranks share ONE GPU (NCCL refuses two ranks
+    on a device): CUDA IPC and stream memory operations work between processes on the same device,
+    which is how the W > 1 data plane is parity-tested on a single B200.
+    """
+
+    has_collectives = False
+
+    def __init__(self, rank: int, world: int):
+        if world < 1 or not 0 <= rank < world:
+            raise ConfigError(f"invalid rank {rank} of world {world}")
+        if world > 1:
+            import torch.distributed as dist
+
+            if not dist.is_initialized():
+                raise ConfigError("world > 1 needs torch.distributed initialised for the handle exchange")
+        self.rank = rank
+        self.world = world
+        self.handle = None
+
+    @property
+    def active(self) -> bool:
+        return False      # no collectives: the bucket all-reduce path is unavailable
+
+    def _no_collectives(self, *_args) -> None:
+        raise ConfigError("this sync mode needs an NCCL communicator (PeerGroup serves p2p / ce only)")
+
+    all_reduce_ = reduce_scatter = all_gather = _no_collectives
+
+    def check_async_error(self) -> None:
+        pass
+
+    def abort(self) -> None:
+        pass
+
+    def close(self) -> None:
+        pass

@@ -36,16 +36,13 @@ int cuda_status(cudaError_t e, const char* where) {
   return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
 }
 
-static int g_variant = CS_VARIANT_REGISTER;
-
 static int64_t chunks_of(int64_t numel, int chunk) { return (numel + chunk - 1) / chunk; }
 
 template <int CAP>
 static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
   static thread_local PackArgs<CAP> a;  // ~28 KB for the large capacity: keep off the stack
   a.n = n;
-  const bool tma = g_variant == CS_VARIANT_TMA;
-  const int chunk = tma ? tma_pack_chunk() : reg_pack_chunk();
+  const int chunk = reg_pack_chunk();
   int64_t c = 0;
   for (int i = 0; i < n; ++i) {
     a.chunk_begin[i] = (int)c;
@@ -57,7 +54,7 @@ static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
   a.chunk_begin[n] = (int)c;
   if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_pack: %lld chunks exceed grid limit", (long long)c);
   a.total_chunks = (int)c;
-  return cuda_status(tma ? launch_pack_tma<CAP>(a, s) : launch_pack<CAP>(a, s), "cs_pack launch");
+  return cuda_status(launch_pack<CAP>(a, s), "cs_pack launch");
 }
 
 template <int CAP>
@@ -71,8 +68,7 @@ static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources,
   for (int k = 0; k < CS_MAX_SOURCES; ++k) a.base[k] = k < nsrc ? sources[k] : 0;
   a.h = *h;
   const bool mom = h->momentum != 0.0f;
-  const bool tma = g_variant == CS_VARIANT_TMA;
-  const int chunk = tma ? tma_update_chunk(nsrc, mom) : reg_update_chunk();
+  const int chunk = reg_update_chunk();
   int64_t c = 0;
   for (int i = 0; i < n; ++i) {
     a.chunk_begin[i] = (int)c;
@@ -86,8 +82,7 @@ static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources,
   a.chunk_begin[n] = (int)c;
   if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_unpack_sgd: %lld chunks exceed grid limit", (long long)c);
   a.total_chunks = (int)c;
-  return cuda_status(tma ? launch_unpack_sgd_tma<CAP>(a, mom, s) : launch_unpack_sgd<CAP>(a, mom, s),
-                     "cs_unpack_sgd launch");
+  return cuda_status(launch_unpack_sgd<CAP>(a, mom, s), "cs_unpack_sgd launch");
 }
 
 }  // namespace cs
@@ -100,24 +95,10 @@ int cs_abi_version(void) { return CS_ABI_VERSION; }
 
 const char* cs_last_error(void) { return g_last_error.c_str(); }
 
-int cs_set_kernel_variant(int variant) {
-  if (variant != CS_VARIANT_TMA && variant != CS_VARIANT_REGISTER)
-    return set_error(CS_ERR_ARG, "cs_set_kernel_variant: unknown variant %d", variant);
-  g_variant = variant;
-  return 0;
-}
-
-int cs_get_kernel_variant(void) { return g_variant; }
-
 int cs_tune(const char* key, int value) {
   if (key == nullptr || value < 0) return set_error(CS_ERR_ARG, "cs_tune: invalid arguments");
   const std::string k(key);
-  if (k == "k1_chunk" && (value == 0 || (value % 1024 == 0 && value <= 16384))) g_tune_k1_chunk = value;
-  else if (k == "k2_chunk" && (value == 0 || (value % 256 == 0 && value <= 8192))) g_tune_k2_chunk = value;
-  else if (k == "k2_stages" && value <= kTmaMaxStages) g_tune_k2_stages = value;
-  else if (k == "ctas_per_sm" && value <= 4) g_tune_ctas_per_sm = value;
-  else if (k == "k2_debug" && value <= 2) g_tune_k2_debug = value;  // ablation only: wrong results
-  else if (k == "reg_shape" && value <= 4) g_tune_reg_shape = value;
+  if (k == "reg_shape" && value <= 4) g_tune_reg_shape = value;
   else if (k == "p2p_ctas" && value <= 65536) g_tune_p2p_ctas = value;
   else if (k == "sync_ctas" && value <= 65536) g_tune_sync_ctas = value;
   else if (k == "bn_no_pdl" && value <= 1) g_tune_bn_no_pdl = value;
@@ -289,6 +270,24 @@ int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, 
   if (g_memops_status)
     return set_error(g_memops_status, "cs_flag_barrier: stream memory operations unavailable");
   CUstream s = (CUstream)stream;
+  // When the device can flush remote writes, each wait also makes every write that reached this
+  // GPU before the flag (a peer's NVLink stores into my parameters) visible to the work queued
+  // behind it.  Without the attribute the ordering comes from the writer: its flag write is
+  // preceded by a system-scope fence, so its earlier peer stores land first.
+  static int flush_cache[64] = {0};   // per device: 0 unknown, 1 no, 2 yes
+  int dev = 0, can_flush = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+    if (flush_cache[dev] == 0) {
+      int v = 0;
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) != cudaSuccess) {
+        cudaGetLastError();
+        v = 0;
+      }
+      flush_cache[dev] = v ? 2 : 1;
+    }
+    can_flush = flush_cache[dev] == 2;
+  }
+  const unsigned int wait_flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
   // announce: my slot in every peer's flag array (a system-scope fence precedes each write, so
   // everything this stream did before is visible to the peer that observes the flag)
   for (int p = 0; p < nranks; ++p) {
@@ -300,10 +299,26 @@ int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, 
   // wait: every peer's slot in my array has reached this epoch (cyclic >=)
   for (int p = 0; p < nranks; ++p) {
     if (p == rank) continue;
-    CUresult r = g_wait32(s, (CUdeviceptr)(local_flags + 4u * (uint64_t)p), epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    CUresult r = g_wait32(s, (CUdeviceptr)(local_flags + 4u * (uint64_t)p), epoch, wait_flags);
     if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: wait on rank %d failed (%d)", p, (int)r);
   }
   return 0;
+}
+
+int cs_host_register(void* ptr, size_t bytes, void** dev_ptr) {
+  if (ptr == nullptr || bytes == 0 || dev_ptr == nullptr)
+    return set_error(CS_ERR_ARG, "cs_host_register: invalid arguments");
+  int rc = cuda_status(cudaHostRegister(ptr, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable),
+                       "cudaHostRegister");
+  if (rc) return rc;
+  rc = cuda_status(cudaHostGetDevicePointer(dev_ptr, ptr, 0), "cudaHostGetDevicePointer");
+  if (rc) cudaHostUnregister(ptr);
+  return rc;
+}
+
+int cs_host_unregister(void* ptr) {
+  if (ptr == nullptr) return 0;
+  return cuda_status(cudaHostUnregister(ptr), "cudaHostUnregister");
 }
 
 int cs_ipc_close_handle(void* ptr) {
@@ -467,6 +482,11 @@ int cs_event_elapsed_ns(void* start, void* end, int64_t* ns) {
   if (rc) return rc;
   *ns = (int64_t)llround((double)ms * 1e6);
   return 0;
+}
+
+int cs_spin_ns(uint64_t ns, void* stream) {
+  if (ns > 60ull * 1000000000ull) return set_error(CS_ERR_ARG, "cs_spin_ns: more than 60 s");
+  return cuda_status(launch_spin_ns(ns, (cudaStream_t)stream), "cs_spin_ns launch");
 }
 
 size_t cs_gradient_stats_workspace_bytes(int64_t numel) {

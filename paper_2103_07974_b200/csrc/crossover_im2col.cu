@@ -140,7 +140,8 @@ cudaError_t launch_im2col_nhwc(const void* x, void* p, const int* shape, cudaStr
   const unsigned g = (unsigned)(grid < 1 ? 1 : grid);
   const auto* xi = (const __nv_bfloat16*)x;
   auto* po = (__nv_bfloat16*)p;
-  const bool rows_ok = (s.W * s.C) % 8 == 0;     // 16-byte staging of whole input rows
+  // 16-byte staging of whole input rows: row length and base address must be 16-byte multiples
+  const bool rows_ok = (s.W * s.C) % 8 == 0 && ((uintptr_t)xi & 15u) == 0;
   if (rows_ok && s.C == 3 && s.KH == 7 && s.KW == 7 && s.SH == 2 && s.SW == 2 && s.KP == 152)
     im2col_rows_kernel<3, 7, 7, 2, 2, 152><<<(unsigned)(s.N * s.OH), 19 * (256 / 19), 7 * s.W * 3 * 2, stream>>>(
         xi, po, s);                                                                        // ResNet stem

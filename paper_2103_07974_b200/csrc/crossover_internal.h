@@ -10,15 +10,6 @@ namespace cs {
 constexpr int kThreads = 256;                      // 8 warps per CTA
 constexpr int kStatsMaxGrid = 148 * 8;             // fixed -> deterministic partial order
 
-// TMA (cp.async.bulk) variants: one persistent CTA per SM, stage ring in shared memory
-constexpr int kTmaBarrierBytes = 256;              // mbarriers in front of the stage ring
-constexpr int kTmaWsThreads = 32 + 256;            // producer warp + 8 consumer warps
-constexpr int kTmaSmemBudget = 200 * 1024;         // dynamic shared memory per CTA
-constexpr int kTmaMaxStages = 8;
-constexpr int kTmaMinStages = 6;
-constexpr int kTmaPackChunk = 8192;                // fp32 per stage for K1 (32 KB)
-constexpr int kTmaMaxChunk = 2048;                 // fp32 per stream per stage for K2
-
 // descriptor capacities per launch (kernel parameters are <= 32 KB on sm_70+)
 constexpr int kCapSmall = 16;
 constexpr int kCapMid = 128;
@@ -58,11 +49,6 @@ template <int CAP>
 cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s);
 template <int CAP>
 cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
-template <int CAP>
-cudaError_t launch_pack_tma(const PackArgs<CAP>& a, cudaStream_t s);
-template <int CAP>
-cudaError_t launch_unpack_sgd_tma(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
-int tma_pack_chunk();
 int reg_pack_chunk();
 int reg_update_chunk();
 extern int g_tune_reg_shape;
@@ -70,8 +56,6 @@ extern int g_tune_sync_ctas;
 extern int g_tune_p2p_ctas;
 extern int g_tune_bn_no_pdl;
 extern int g_tune_bn_ctas_per_sm;
-extern int g_tune_k1_chunk, g_tune_k2_chunk, g_tune_k2_stages, g_tune_ctas_per_sm, g_tune_k2_debug;
-int tma_update_chunk(int nsrc, bool mom);
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s);
 int bn_row_blocks(int64_t M, int C);
 cudaError_t launch_im2col_nhwc(const void* x, void* p, const int* shape, cudaStream_t stream);
@@ -90,6 +74,7 @@ cudaError_t launch_maxpool_bwd(const void* dy, const void* arg, void* dx, const 
 cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws,
                          cudaStream_t s);
 int stats_grid(int64_t numel);
+cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t s);
 
 // thread-local error reporting shared by every translation unit of the library
 int set_error(int code, const char* fmt, ...);

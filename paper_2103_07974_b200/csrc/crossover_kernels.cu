@@ -318,6 +318,22 @@ cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// fixed-duration compute stand-in: one thread spins on the global nanosecond timer
+// ---------------------------------------------------------------------------
+__global__ void spin_ns_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t s) {
+  spin_ns_kernel<<<1, 1, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
 int stats_grid(int64_t numel) {
   int64_t per_cta = (int64_t)kThreads * 4 * 8;
   int64_t g = (numel + per_cta - 1) / per_cta;

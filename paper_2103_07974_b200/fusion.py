@@ -138,6 +138,8 @@ class FusedGradientSync:
         if mode == "auto":
             if self.workers == 1:
                 mode = "direct"
+            elif not getattr(comm, "has_collectives", True):
+                mode = "ce"
             else:
                 mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
         if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "adaptive", "unfused"):
@@ -149,6 +151,9 @@ class FusedGradientSync:
         if mode in ("sharded", "p2p", "ce", "adaptive") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
             raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
                               "and one worker per rank")
+        if (self.ranks > 1 and mode in ("bucket", "sharded", "unfused")
+                and not getattr(comm, "has_collectives", True)):
+            raise ConfigError(f"{mode} sync needs an NCCL communicator at world > 1")
         self.mode = mode
         self.flat = flat_params
         sharded = mode in ("sharded", "p2p", "ce", "adaptive")
@@ -167,6 +172,8 @@ class FusedGradientSync:
 
         self.bucket = None
         self._peer_maps = []
+        self._flags = None
+        self.failed = False
         self.transport = None
         if mode in ("p2p", "ce", "adaptive"):
             from .p2p import DeviceBuffer, buffer_of
@@ -255,24 +262,26 @@ class FusedGradientSync:
         (cs_flag_barrier) when every rank supports them ("auto" / "flags"), else a 1-element
         NCCL all-reduce ("nccl").  The NCCL barrier's kernel needs a free SM, which it may wait
         for while the other app's GEMMs hold every SM; the flag barrier runs in the GPU front end."""
-        from .p2p import DeviceBuffer, all_ranks_agree, exchange_peer_addresses
+        from .p2p import FlagArray, all_ranks_agree
 
         if barrier not in ("auto", "flags", "nccl"):
             raise ConfigError(f"unknown barrier {barrier!r}")
         self._flag_peers = None
+        self._flags = None
         self._epoch = 0
+        nccl = getattr(self.comm, "has_collectives", True)
         if barrier == "nccl":
+            if not nccl:
+                raise ConfigError("the NCCL barrier needs an NcclCommunicator")
             return
         supported = bool(_lib.lib.cs_stream_memops_supported())
         if not all_ranks_agree(supported):
-            if barrier == "flags":
+            if barrier == "flags" or not nccl:
                 raise ConfigError("stream memory operations are not supported on every rank")
             return
-        self._flags_buf = DeviceBuffer(32, self.bucket.device)     # uint32 slots, zeroed
-        fm = exchange_peer_addresses(self._flags_buf, self.rank, self.ranks)
-        self._peer_maps.append(fm)
-        self._flag_peers = np.asarray(fm.addresses, dtype=np.uint64)
-        self._flag_local = self._flags_buf.ptr
+        self._flags = FlagArray(self.rank, self.ranks)      # host shared memory, zeroed
+        self._flag_peers = self._flags.peer_rows
+        self._flag_local = self._flags.local_row
 
     def _rank_barrier(self, stream: int) -> None:
         if self._flag_peers is None:
@@ -504,10 +513,36 @@ class FusedGradientSync:
             with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
                 self.snapshot[snapshot_row].copy_(self.flat)
 
+    def release_waits(self) -> None:
+        """Failure path: satisfy every pending flag-barrier wait of every rank (host writes into
+        the shared flag segment, no GPU work), so no comm stream stays blocked behind a peer that
+        stopped.  The transport is unusable afterwards."""
+        if self._flags is not None:
+            self._flags.release(self._epoch)
+            self.failed = True
+
     def close(self) -> None:
+        """Unmap the peers' buffers, then free this app's IPC bucket and flag segment.  At W > 1
+        this is collective (every rank unmaps before any rank frees) unless the sync failed."""
         for m in self._peer_maps:
             m.close()
         self._peer_maps = []
+        bucket = getattr(self, "_bucket_buf", None)
+        if bucket is None and self._flags is None:
+            return
+        if self.ranks > 1 and not self.failed:
+            import torch.distributed as dist
+
+            if dist.is_initialized():
+                dist.barrier()
+        if bucket is not None:
+            self.bucket = None
+            bucket.close()
+            self._bucket_buf = None
+        if self._flags is not None:
+            self._flags.close()
+            self._flags = None
+            self._flag_peers = None
 
     # -- algorithmic bytes per launch (SURVEY §8d) ---------------------------
     def k1_bytes(self) -> int:
@@ -571,6 +606,10 @@ def _grad_ptrs(grads: Sequence[torch.Tensor | None], params: Sequence[torch.Tens
             if g.dtype != torch.float32:
                 raise ConfigError("gradients must be fp32 (parameters are fp32 masters)")
             if g.stride() != p.stride() or not _dense(g):
+                # the copy runs on the current (comm) stream while `g` was allocated on the
+                # compute stream: record the use, or the caching allocator could hand g's
+                # memory to the next app's forward before the queued copy has read it
+                g.record_stream(torch.cuda.current_stream(g.device))
                 fixed = torch.empty_like(p)
                 fixed.copy_(g)
                 g = fixed

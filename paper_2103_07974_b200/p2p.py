@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 
-__all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping", "all_ranks_agree"]
+__all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping", "all_ranks_agree", "FlagArray"]
 
 _live: dict[int, "DeviceBuffer"] = {}
 
@@ -112,3 +112,88 @@ def all_ranks_agree(ok: bool) -> bool:
     t = torch.tensor([1 if ok else 0], dtype=torch.int32)
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     return bool(int(t.item()))
+
+
+class FlagArray:
+    """The barrier flags of one app's p2p / ce transport, shared by every rank of the node.
+
+    A W x W uint32 matrix in one POSIX shared-memory segment (rank 0 creates it, the others attach
+    by name, every rank page-locks and device-maps it with cs_host_register).  Row r holds the flags
+    rank r waits on; rank p writes column p of every row (cs_flag_barrier: peer_flags[p] = row p,
+    local_flags = row r).  The GPU front ends write and poll it with stream memory operations, so a
+    barrier still occupies no SM.  Because the host can write the segment directly, a watchdog can
+    release every rank's pending waits without issuing GPU work (:meth:`release`), which a wait on
+    device memory behind a blocked stream could not guarantee.
+    """
+
+    def __init__(self, rank: int, world: int):
+        import torch.distributed as dist
+        from multiprocessing import shared_memory
+
+        import numpy as np
+
+        from .errors import ConfigError
+
+        self.rank, self.world = rank, world
+        nbytes = 4 * world * world
+        self._size = max(4096, nbytes)
+        self._shm = None
+        name = [None]
+        error = ""
+        if rank == 0:
+            try:
+                self._shm = shared_memory.SharedMemory(create=True, size=self._size)
+                name[0] = self._shm.name
+            except OSError as exc:
+                error = f"rank 0: cannot create the flag segment: {exc}"
+        dist.broadcast_object_list(name, src=0)
+        if name[0] is not None and rank != 0:
+            try:
+                self._shm = shared_memory.SharedMemory(name=name[0], create=False)
+                # rank 0 owns (and unlinks) the segment; keep this process's resource tracker
+                # from unlinking it a second time at exit
+                from multiprocessing import resource_tracker
+
+                resource_tracker.unregister(self._shm._name, "shared_memory")
+            except OSError as exc:
+                error = f"rank {rank}: cannot attach the flag segment: {exc}"
+        self._dev = 0
+        if self._shm is not None and not error:
+            self._host = np.ndarray((world, world), dtype=np.uint32, buffer=self._shm.buf)
+            if rank == 0:
+                self._host[:] = 0
+            addr = ctypes.addressof(ctypes.c_char.from_buffer(self._shm.buf))
+            dev = ctypes.c_void_p()
+            rc = _lib.lib.cs_host_register(addr, self._size, ctypes.byref(dev))
+            if rc:
+                error = f"rank {rank}: cs_host_register failed: {_lib.lib.cs_last_error().decode()}"
+            else:
+                self._addr = addr
+                self._dev = int(dev.value)
+        ok = all_ranks_agree(not error)
+        if rank == 0 and self._shm is not None:
+            self._shm.unlink()            # every rank has attached (or failed): no /dev/shm leak
+        if not ok:
+            self.close()
+            raise ConfigError("flag segment setup failed on some rank" + (f" ({error})" if error else ""))
+        self.peer_rows = np.asarray([self._dev + 4 * world * p for p in range(world)], dtype=np.uint64)
+        self.local_row = self._dev + 4 * world * rank
+
+    def release(self, epoch: int) -> None:
+        """Satisfy every pending wait of every rank: write an epoch far ahead (cyclic compare) of
+        anything enqueued into the whole matrix.  Only for failure handling -- afterwards the flags
+        no longer order anything, so the owning transport must not be used again."""
+        if self._dev:
+            self._host[:] = (int(epoch) + (1 << 30)) & 0xFFFFFFFF
+
+    def close(self) -> None:
+        if getattr(self, "_dev", 0):
+            _lib.check("cs_host_unregister", _lib.lib.cs_host_unregister(self._addr))
+            self._dev = 0
+        if self._shm is not None:
+            self._host = None
+            try:
+                self._shm.close()
+            except BufferError:
+                pass
+            self._shm = None

@@ -28,6 +28,7 @@ returned as a measured ``Trace``.
 
 from __future__ import annotations
 
+import collections
 import contextlib
 import gc
 import time
@@ -240,6 +241,9 @@ class CrossoverScheduler:
         self._started = False
         self._slot = 0
         self.tuner: _TransportTuner | None = None
+        self.failed = False
+        self._last_compute_start = None
+        self._inflight: collections.deque = collections.deque()
 
     # -- registration (≙ building a SchedulePlan of JobProfiles) -------------
     def register(self, app: App) -> JobRuntimeState:
@@ -323,25 +327,16 @@ class CrossoverScheduler:
         if not self.states:
             raise ConfigError("no apps registered")
         if not self._started:
-            self._started = True
-            self.recorder.start(self.compute_stream)
-            adaptive = [s.sync.mode == "adaptive" for s in self.states]
-            if all(adaptive):
-                self.tuner = _TransportTuner([s.app.iterations for s in self.states], self.comm,
-                                             self.device)
-            elif any(adaptive):
-                raise ConfigError("adaptive transport must be used by every app or none")
+            self._start()
         st = self._next_with_work()
         if st is None:
             return False
         app, t = st.app, st.next_iteration
         cs, ms = self.compute_stream, self.comm_stream
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-        slot = self._slot
         self._slot += 1
         if self.tuner is not None:
-            self.tuner.before_slot(slot, ms)
-            st.sync.set_transport(self.tuner.transport_for(slot))
+            st.sync.set_transport(self.tuner.transport)
 
         with torch.cuda.stream(cs):
             # Alg. 1 readiness (scheduler.py:158): compute (j, t) after sync (j, t-1).
@@ -358,8 +353,7 @@ class CrossoverScheduler:
             batches = [self._to_device(app.data(t, w)) for w in workers]
             e_f0 = ev()
             e_f0.record(cs)
-            if self.tuner is not None:
-                self.tuner.mark(slot, e_f0)
+            self._last_compute_start = e_f0
             amp = (torch.autocast("cuda", dtype=app.autocast_dtype, cache_enabled=app.autocast_cache)
                    if app.autocast_dtype else contextlib.nullcontext())
             losses = []
@@ -389,6 +383,11 @@ class CrossoverScheduler:
             e_s1.record(ms)
         st.update_done = e_s1
         self._last_update = e_s1
+        # syncs still in flight, oldest first (failure reports name the oldest unfinished one);
+        # only the head is queried, so this stays O(1) per step
+        self._inflight.append((st.job_id, t, e_s1))
+        while len(self._inflight) > 1 and self._inflight[0][2].query():
+            self._inflight.popleft()
 
         self.recorder.add(GPU_LANE_ID, st.job_id, Phase.FORWARD, t, e_f0, e_f1)
         self.recorder.add(GPU_LANE_ID, st.job_id, Phase.BACKWARD, t, e_f1, e_b1)
@@ -396,6 +395,49 @@ class CrossoverScheduler:
         st.next_iteration = t + 1
         self.cursor = (self.cursor + 1) % len(self.states)
         return True
+
+    def _start(self) -> None:
+        self._started = True
+        self.recorder.start(self.compute_stream)
+        adaptive = [s.sync.mode == "adaptive" for s in self.states]
+        if all(adaptive):
+            self.tuner = _TransportTuner()
+        elif any(adaptive):
+            raise ConfigError("adaptive transport must be used by every app or none")
+
+    def calibrate(self, rotations: int = 4) -> dict | None:
+        """Measured choice of the adaptive transport (copy engines vs the fused P2P kernel).
+
+        Steps ``rotations`` rotations over the copy engines and ``rotations + 1`` with the P2P
+        kernel -- real training iterations: both transports sum the W shards in rank order with the
+        same update rule, so the weights are bitwise those of either transport -- then waits for the
+        device (here, outside ``step()``, which never blocks), takes each transport's median
+        rotation period between compute starts (the first rotation of each window is a warm-up),
+        sums the medians over the ranks and keeps the faster transport on every rank.  Returns the
+        tuner summary, or None when the plan is not adaptive or too short (stays on the copy
+        engines).  ``run()`` calls it first when every budget allows."""
+        if not self._started:
+            self._start()
+        if self.tuner is None or self.tuner.decided:
+            return None if self.tuner is None else self.tuner.summary()
+        need = 2 * rotations + 1
+        if rotations < 2 or any(st.app.iterations - st.next_iteration + 1 < need for st in self.states):
+            return None
+        starts = {}
+        for k in range(need):
+            self.tuner.transport = "ce" if k < rotations else "p2p"
+            for j in range(len(self.states)):
+                self.step()
+                if j == 0:
+                    starts[k] = self._last_compute_start
+        # one more rotation boundary: the first compute after the last p2p rotation is enqueued by
+        # the caller's next step(); the window's last start is that of rotation 2R (already issued)
+        starts[need - 1].synchronize()
+        ce = sorted(starts[k].elapsed_time(starts[k + 1]) for k in range(1, rotations))
+        p2p = sorted(starts[k].elapsed_time(starts[k + 1]) for k in range(rotations + 1, need - 1))
+        medians = [ce[len(ce) // 2], p2p[len(p2p) // 2]]
+        self.tuner.decide(medians, self.comm)
+        return self.tuner.summary()
 
     def _range(self, name: str):
         """NVTX range around a phase (visible in Nsight Systems) when nvtx=True."""
@@ -435,10 +477,24 @@ class CrossoverScheduler:
             self.comm.check_async_error()
 
     def _fail(self, detail: str) -> None:
-        waiting = [(st.job_id, st.sync_of_iteration) for st in self.states if st.awaiting_sync]
-        job, it = waiting[0] if waiting else (self.states[0].job_id, self.states[0].next_iteration)
+        """Failure path: unblock the device, then raise DeadlockError(job, iteration).
+
+        NCCL kernels waiting for a dead peer end with ncclCommAbort; flag-barrier waits (stream
+        memory operations, which no abort can cancel) are satisfied by writing a final epoch into
+        the shared flag segments from the host.  The queued work then drains (its results are
+        garbage and the syncs are marked failed), so later synchronize / teardown calls return."""
+        pending = [(j, t) for j, t, e in self._inflight if not e.query()]
+        job, it = pending[0] if pending else (self.states[0].job_id, self.states[0].next_iteration)
         if self.comm is not None:
             self.comm.abort()
+        for st in self.states:
+            st.sync.release_waits()
+        done = torch.cuda.Event()
+        done.record(self.comm_stream)
+        t0 = time.monotonic()
+        while not done.query() and time.monotonic() - t0 < 30.0:
+            time.sleep(0.001)
+        self.failed = True
         raise DeadlockError(job, it, f"policy={self.policy.value}; {detail}")
 
     def run(self) -> Trace:
@@ -451,6 +507,10 @@ class CrossoverScheduler:
         gc.collect()
         gc.disable()
         try:
+            if not self._started:
+                self._start()
+            if self.tuner is not None and self._slot == 0:
+                self.calibrate()
             while self.step():
                 pass
         finally:
@@ -480,75 +540,44 @@ class CrossoverScheduler:
 
 
 class _TransportTuner:
-    """Measured choice between the copy-engine and the fused-P2P-kernel transport (adaptive).
+    """State of the adaptive transport (measured by :meth:`CrossoverScheduler.calibrate`).
 
-    With n apps, slots [0, 4n) sync over the copy engines and slots [4n, 8n) with the P2P kernel
-    (32 CTAs).  Each transport's rotation period is the median of its last three rotations,
-    measured on the device between compute starts (slots n, 2n, 3n, 4n and 5n, 6n, 7n, 8n), so
-    every measured compute waits on syncs of its own transport and a one-off spike (first launch,
-    allocator growth) does not decide.  At slot 9n every rank sums its two medians over the ranks
-    (NCCL all-reduce on the comm stream, at the same position of the collective sequence on every
-    rank) and at slot 10n every rank reads the sums and keeps the faster transport for the rest of
-    the run -- the same decision everywhere, without a host barrier.  Plans too short to afford
-    the calibration (any budget < 12) stay on the copy engines.  The windows must not contain a
-    host-side drain (bench.py calibrates in a separate untimed run for that reason).
-    """
+    Until calibrated every sync runs over the copy engines; ``decide`` sums the per-rank median
+    rotation periods of both transports over the ranks (host-side, after the device reached the
+    end of the calibration window) so every rank keeps the same transport."""
 
-    MIN_BUDGET = 12
-
-    def __init__(self, budgets: list[int], comm, device):
-        self.n = len(budgets)
-        self.active = min(budgets) >= self.MIN_BUDGET and comm is not None and comm.world > 1
-        self.comm = comm
-        self.device = device
-        self.choice = "ce"
-        self.marks: dict[int, torch.cuda.Event] = {}
+    def __init__(self):
+        self.transport = "ce"
+        self.decided = False
         self.periods_ms: dict[str, float] | None = None
-        self._host = torch.zeros(2, dtype=torch.float32).pin_memory() if self.active else None
-        self._dev = torch.zeros(32, dtype=torch.float32, device=device) if self.active else None
-        self._done: torch.cuda.Event | None = None
 
-    def transport_for(self, slot: int) -> str:
-        if not self.active:
-            return "ce"
-        if slot < 4 * self.n:
-            return "ce"
-        if slot < 8 * self.n:
-            return "p2p"
-        return self.choice
+    def decide(self, medians: list[float], comm) -> None:
+        import torch.distributed as dist
 
-    def mark(self, slot: int, event) -> None:
-        if self.active and slot % self.n == 0 and 1 <= slot // self.n <= 8:
-            self.marks[slot] = event
+        world = comm.world if comm is not None else 1
+        t = torch.tensor(medians, dtype=torch.float64)
+        if world > 1 and dist.is_initialized():
+            if dist.get_backend() == "nccl":
+                d = t.to(torch.cuda.current_device())
+                dist.all_reduce(d)
+                t = d.cpu()
+            else:
+                dist.all_reduce(t)
+        ce, p2p = (float(x) / world for x in t)
+        self.periods_ms = {"ce": ce, "p2p": p2p}
+        self.transport = "ce" if ce <= p2p else "p2p"
+        self.decided = True
 
-    def _median_period(self, first: int) -> float:
-        n = self.n
-        p = sorted(self.marks[k * n].elapsed_time(self.marks[(k + 1) * n])
-                   for k in range(first, first + 3))
-        return p[1]
+    @property
+    def choice(self) -> str:
+        return self.transport
 
-    def before_slot(self, slot: int, comm_stream) -> None:
-        if not self.active:
-            return
-        n = self.n
-        if slot == 9 * n:
-            self.marks[8 * n].synchronize()          # one rotation old: already reached
-            ce, p2p = self._median_period(1), self._median_period(5)
-            self._host.copy_(torch.tensor([ce, p2p]))
-            with torch.cuda.stream(comm_stream):
-                self._dev[:2].copy_(self._host, non_blocking=True)
-                self.comm.all_reduce_(self._dev.data_ptr(), 2, comm_stream.cuda_stream)
-                self._host.copy_(self._dev[:2], non_blocking=True)
-            self._done = torch.cuda.Event()
-            self._done.record(comm_stream)
-        elif slot == 10 * n:
-            self._done.synchronize()
-            ce, p2p = (float(x) / self.comm.world for x in self._host)
-            self.periods_ms = {"ce": ce, "p2p": p2p}
-            self.choice = "ce" if ce <= p2p else "p2p"
+    @property
+    def active(self) -> bool:
+        return self.decided
 
     def summary(self) -> dict:
-        return {"active": self.active, "choice": self.choice,
+        return {"active": self.decided, "choice": self.transport,
                 "calibration_period_ms": self.periods_ms}
 
 

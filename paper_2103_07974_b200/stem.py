@@ -61,19 +61,24 @@ class _StemGemm(torch.autograd.Function):
             else:
                 torch.mm(p, wm.t(), out=y2d)
         ctx.save_for_backward(p)
-        ctx.meta = (o, c, kh, kw, k, weight.dtype, bias is not None)
+        fmt = (torch.channels_last if weight.is_contiguous(memory_format=torch.channels_last)
+               and not weight.is_contiguous() else torch.contiguous_format)
+        ctx.meta = (o, c, kh, kw, k, weight.dtype, bias is not None, fmt)
         return y
 
     @staticmethod
     def backward(ctx, dy):
         (p,) = ctx.saved_tensors
-        o, c, kh, kw, k, wdt, has_bias = ctx.meta
+        o, c, kh, kw, k, wdt, has_bias, fmt = ctx.meta
         dy = dy.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
         dym = dy.permute(0, 2, 3, 1).reshape(-1, o)
         with torch.autocast("cuda", enabled=False):
             # fp32 output straight from the bf16 GEMM's fp32 accumulator (no bf16 rounding of dW)
             dwm = torch.mm(dym.t(), p, out_dtype=torch.float32)
-            dw = dwm[:, :k].reshape(o, kh, kw, c).permute(0, 3, 1, 2).to(wdt)
+            # dW in the weight's own layout (a [o, kp] slice would carry the padded row stride),
+            # so the fused update reads it in place without a re-layout copy
+            dw = dwm[:, :k].reshape(o, kh, kw, c).permute(0, 3, 1, 2).to(wdt).contiguous(
+                memory_format=fmt)
             db = dym.sum(0, dtype=torch.float32).to(wdt) if has_bias else None
         return None, dw, db, None, None
 

@@ -16,17 +16,10 @@ pytestmark = pytest.mark.gpu
 RAGGED = [0, 1, 3, 4, 5, 17, 64, 4095, 4096, 4097, 12345, 200704, 256, 2560, 10]
 
 
-@pytest.fixture(autouse=True, params=["tma", "register"])
-def variant(request):
-    """Every kernel test runs against both implementations (bit-identical by contract)."""
-    from paper_2103_07974_b200 import _lib
-
+@pytest.fixture(autouse=True)
+def _needs_cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    old = _lib.kernel_variant()
-    _lib.set_kernel_variant(_lib.CS_VARIANT_TMA if request.param == "tma" else _lib.CS_VARIANT_REGISTER)
-    yield request.param
-    _lib.set_kernel_variant(old)
 
 
 def _bits(a) -> np.ndarray:

@@ -1,0 +1,112 @@
+"""Timing-level check of Alg. 1 on the device: measured spans vs the reference's recurrences.
+
+The emitted *order* of spans is the host's enqueue order, so the bit-exact schedule key alone cannot
+catch a device pipeline that serialises everything.  These tests give the apps compute phases of
+known device duration (cs_spin_ns: one SM, no memory traffic) and a real sync (K2 over a bucket
+sized to take about one unit) and compare the *measured* CUDA-event spans with the reference:
+
+* the golden plan (tests/test_scheduler.py:42-97 in the reference): N = 2, comp = 2, comm = 1,
+  T = 3 -> makespans 13 (crossover) and 18 (sequential), speedup 18/13;
+* every measured span start against the queue-free recurrence of scheduler.py:151-193
+  (oracle/schedule.py) fed with the measured phase durations;
+* head-of-line blocking (scheduler.py:162-164 + the FIFO NIC lane,
+  SPEC.md:317): A (comp 1, comm 10), B and C (comp 1, comm 0), T = 2 -- B's and C's syncs start only
+  after A's ends and the GPU idles on A meanwhile.
+"""
+
+import statistics
+
+import pytest
+import torch
+
+from oracle import schedule as osched
+
+pytestmark = pytest.mark.gpu
+
+TOL = 0.05
+BYTES_PER_UNIT = 1_200_000_000     # K2 with momentum moves 5 x bucket bytes: ~1 ms on B200
+
+
+def _run(policy, specs, dev, T):
+    """specs: (job_id, forward_ns, backward_ns, bucket_bytes).  Returns the measured spans with
+    times relative to the first compute start, and the apps (for reuse)."""
+    from paper_2103_07974_b200.apps import fixed_time_app
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler
+
+    s = CrossoverScheduler(policy)
+    for k, (job, fwd, bwd, nbytes) in enumerate(specs):
+        s.register(fixed_time_app(job, fwd, bwd, nbytes, T, dev, seed=k))
+    tr = s.run()
+    t0 = min(sp.start for sp in tr.spans if sp.phase.value == "forward")
+    spans = [(sp.lane_id, sp.job_id, sp.phase.value, sp.iteration, sp.start - t0, sp.end - t0)
+             for sp in tr.spans]
+    del s
+    torch.cuda.empty_cache()
+    return spans
+
+
+def _sync_ns(spans, job):
+    return statistics.median(e - s for lane, j, ph, t, s, e in spans if j == job and ph == "sync")
+
+
+def _makespan(spans):
+    return max(s[5] for s in spans)
+
+
+def _check_against_recurrence(spans, predicted, scale):
+    assert [s[:4] for s in spans] == [p[:4] for p in predicted]
+    worst = max(abs(m[4] - p[4]) for m, p in zip(spans, predicted)) / scale
+    assert worst <= TOL, worst
+    return worst
+
+
+def test_golden_plan_timing_18_over_13(cuda_device):
+    from paper_2103_07974_b200.scheduler import Policy
+
+    T = 3
+    # calibration: the sync (K2 over the unit bucket) sets the unit; compute = 2 units
+    probe = [("j1", 200_000, 200_000, BYTES_PER_UNIT), ("j2", 200_000, 200_000, BYTES_PER_UNIT)]
+    _run(Policy.SEQUENTIAL, probe, cuda_device, T)             # warm-up: module loads, allocator
+    cal = _run(Policy.SEQUENTIAL, probe, cuda_device, T)
+    unit = statistics.median([_sync_ns(cal, "j1"), _sync_ns(cal, "j2")])
+    specs = [(j, unit // 2, 3 * unit // 2, BYTES_PER_UNIT) for j in ("j1", "j2")]
+    cross = _run(Policy.CROSSOVER, specs, cuda_device, T)
+    seq = _run(Policy.SEQUENTIAL, specs, cuda_device, T)
+    ratio = _makespan(seq) / _makespan(cross)
+    assert abs(ratio / (18 / 13) - 1) <= TOL, (ratio, _makespan(seq) / unit, _makespan(cross) / unit)
+    assert abs(_makespan(cross) / unit - 13) <= 13 * TOL
+    assert abs(_makespan(seq) / unit - 18) <= 18 * TOL
+    # span starts vs the recurrence with the measured durations
+    for pol, measured in ((osched.crossover, cross), (osched.sequential, seq)):
+        jobs = [(j, unit // 2, 3 * unit // 2, _sync_ns(measured, j), T) for j in ("j1", "j2")]
+        pred, pred_ms = pol(jobs)
+        _check_against_recurrence(measured, pred, pred_ms)
+    # the crossover overlap itself: sync (j1, t) runs while j2 computes
+    s1 = [s for s in cross if s[1] == "j1" and s[2] == "sync" and s[3] == 1][0]
+    c2 = [s for s in cross if s[1] == "j2" and s[2] == "backward" and s[3] == 1][0]
+    assert s1[4] < c2[5] and c2[4] < s1[5]
+
+
+def test_head_of_line_blocking_timing(cuda_device):
+    from paper_2103_07974_b200.scheduler import Policy
+
+    T = 2
+    probe = [("A", 100_000, 100_000, BYTES_PER_UNIT // 2)]
+    _run(Policy.SEQUENTIAL, probe, cuda_device, T)
+    cal = _run(Policy.SEQUENTIAL, probe, cuda_device, T)
+    unit = _sync_ns(cal, "A")                                   # ~0.5 ms
+    specs = [("A", unit // 2, unit // 2, 5 * BYTES_PER_UNIT), ("B", unit // 2, unit // 2, 1024),
+             ("C", unit // 2, unit // 2, 1024)]
+    cross = _run(Policy.CROSSOVER, specs, cuda_device, T)
+    get = {(s[1], s[2], s[3]): s for s in cross}
+    a_sync = get[("A", "sync", 1)]
+    assert a_sync[5] - a_sync[4] >= 5 * unit                     # A's sync is long (~10 units)
+    for j in ("B", "C"):                                         # FIFO NIC lane: queued behind A
+        assert get[(j, "sync", 1)][4] >= a_sync[5] - 20_000
+    # strict head-of-line: A's second compute waits for its sync, B/C do not skip ahead of it
+    assert get[("A", "forward", 2)][4] >= a_sync[5] - 20_000
+    for j in ("B", "C"):
+        assert get[(j, "forward", 2)][4] >= get[("A", "backward", 2)][5] - 20_000
+    jobs = [(j, unit // 2, unit // 2, _sync_ns(cross, j), T) for j in ("A", "B", "C")]
+    pred, pred_ms = osched.crossover(jobs)
+    _check_against_recurrence(cross, pred, pred_ms)

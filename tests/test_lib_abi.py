@@ -49,7 +49,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(_lib.P2PDesc) == 8 * 8 * 2 + 8 + 8 + 8 + 8
     assert _lib.UPDATE_DESC.itemsize == 40
     assert ctypes.sizeof(_lib.SgdHyper) == 32
-    assert _lib.lib.cs_abi_version() == 1
+    assert _lib.lib.cs_abi_version() == 2
 
 
 def test_argument_errors_without_gpu():
