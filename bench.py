@@ -500,7 +500,7 @@ def run_ours(args):
         base = list(sc.device_plan(dev, 1, batch={"resnet50": args.batch, "vgg16": args.batch},
                                    time_scale=args.scenario_time_scale, workers=world, flat=flat,
                                    graphed=not args.no_graphs, fast_bn=not args.aten_bn,
-                                   seed=1000 * rank).jobs)
+                                   seed=0, data_seed=1000 * rank).jobs)
         args.mix = f"scenario {sc.name}"
         args.no_e2e, args.no_cpu_baseline = True, True
     elif args.mix:
@@ -508,16 +508,17 @@ def run_ours(args):
         for j, item in enumerate(args.mix.split(",")):
             name, b = item.split(":")
             if name == "bert":
-                base.append(apps.bert_app(f"bert_{j}", int(b), 128, 1, dev, seed=1000 * j + rank,
+                base.append(apps.bert_app(f"bert_{j}", int(b), 128, 1, dev, seed=1000 * j,
+                                          data_seed=1000 * j + rank,
                                           flat=flat))
             else:
                 fn = apps.resnet50_app if name == "resnet50" else apps.vgg16_app
-                base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j + rank,
+                base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
                                graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
                                stem="cudnn" if args.cudnn_stem else "gemm"))
         args.no_e2e, args.no_cpu_baseline = True, True
     else:
-        base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j + rank,
+        base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
                       graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
                       stem="cudnn" if args.cudnn_stem else "gemm")
             for j in range(args.jobs)]

@@ -115,8 +115,12 @@ CS_API int cs_event_query(void* event);
 CS_API int cs_event_elapsed_ns(void* start, void* end, int64_t* ns);
 
 /* K1: gather n tensors into the bucket (128-bit vector path when src and dst
- * are 16-byte aligned, scalar otherwise).  Bit-exact copy. */
-CS_API int cs_pack(const cs_pack_desc* descs, int n, void* stream);
+ * are 16-byte aligned, scalar otherwise).  Bit-exact copy.
+ * max_ctas: 0 = one CTA per 4096-element chunk (or the cs_tune("sync_ctas") cap); > 0 = a
+ * persistent grid of at most max_ctas CTAs -- what a sync overlapping another app's compute on a
+ * high-priority stream should use, so the other stream's CTAs are not held back behind thousands of
+ * pending high-priority ones.  Results never depend on it (same for cs_unpack_sgd). */
+CS_API int cs_pack(const cs_pack_desc* descs, int n, int max_ctas, void* stream);
 
 /* K2: for every tensor i and element k
  *     acc  = 0 + g_0 + g_1 + ... + g_{S-1}   (left to right over sources)
@@ -129,7 +133,7 @@ CS_API int cs_pack(const cs_pack_desc* descs, int n, void* stream);
  * If snapshot != NULL the updated parameter is also written to
  * snapshot + snap_offset (per-iteration weight capture for parity). */
 CS_API int cs_unpack_sgd(const cs_update_desc* descs, int n, const uint64_t* sources,
-                  int n_sources, float* snapshot, const cs_sgd_hyper* hyper,
+                  int n_sources, float* snapshot, const cs_sgd_hyper* hyper, int max_ctas,
                   void* stream);
 
 /* Gradient health over a contiguous fp32 range: out[0] += sum of squares

@@ -66,9 +66,10 @@ EXPORTS = {
     "cs_stream_wait_event": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "cs_event_query": ([ctypes.c_void_p], ctypes.c_int),
     "cs_event_elapsed_ns": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
-    "cs_pack": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "cs_pack": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
     "cs_unpack_sgd": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
-                       ctypes.c_void_p, ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),
+                       ctypes.c_void_p, ctypes.POINTER(SgdHyper), ctypes.c_int, ctypes.c_void_p],
+                      ctypes.c_int),
     "cs_spin_ns": ([ctypes.c_uint64, ctypes.c_void_p], ctypes.c_int),
     "cs_gradient_stats_workspace_bytes": ([ctypes.c_int64], ctypes.c_size_t),
     "cs_gradient_stats": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
@@ -143,20 +144,20 @@ def check(fn: str, rc: int) -> None:
         raise CrossoverLibError(fn, rc, msg.decode() if msg else "")
 
 
-def pack(descs: np.ndarray, stream: int) -> None:
-    """K1 over a PACK_DESC array (host memory)."""
+def pack(descs: np.ndarray, stream: int, max_ctas: int = 0) -> None:
+    """K1 over a PACK_DESC array (host memory); max_ctas > 0 = persistent grid cap."""
     assert descs.dtype == PACK_DESC and descs.flags.c_contiguous
-    check("cs_pack", lib.cs_pack(descs.ctypes.data, len(descs), stream))
+    check("cs_pack", lib.cs_pack(descs.ctypes.data, len(descs), max_ctas, stream))
 
 
 def unpack_sgd(descs: np.ndarray, sources: np.ndarray, snapshot: int, hyper: SgdHyper,
-               stream: int) -> None:
+               stream: int, max_ctas: int = 0) -> None:
     """K2 over an UPDATE_DESC array with `sources` (uint64 device addresses)."""
     assert descs.dtype == UPDATE_DESC and descs.flags.c_contiguous
     assert sources.dtype == np.uint64 and 1 <= len(sources) <= CS_MAX_SOURCES
     check("cs_unpack_sgd", lib.cs_unpack_sgd(descs.ctypes.data, len(descs), sources.ctypes.data,
                                              len(sources), snapshot or None,
-                                             ctypes.byref(hyper), stream))
+                                             ctypes.byref(hyper), max_ctas, stream))
 
 
 def gradient_stats_workspace_bytes(numel: int) -> int:

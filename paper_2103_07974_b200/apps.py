@@ -339,36 +339,42 @@ VGG_SGD = SgdSettings(lr=0.01, momentum=0.9, weight_decay=5e-4)
 def resnet50_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = DEFAULT_IMAGE_SGD,
                  graphed: bool = False, flat: bool = False, fast_bn: bool = False,
-                 stem: str = "gemm") -> App:
+                 stem: str = "gemm", data_seed: int | None = None) -> App:
+    """``seed`` initialises the weights -- the same on every rank (data-parallel replicas);
+    ``data_seed`` (default ``seed``) draws this worker's synthetic batches -- per rank."""
     import torchvision
 
     torch.manual_seed(seed)
-    return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn, stem=stem)
+    return _image_app(torchvision.models.resnet50(), job_id, batch, iterations, device,
+                      seed if data_seed is None else data_seed, host_data, sgd, graphed=graphed,
+                      flat=flat, fast_bn=fast_bn, stem=stem)
 
 
 def vgg16_app(job_id: str, batch: int, iterations: int, device: torch.device, seed: int = 0,
                  host_data: bool = False, sgd: SgdSettings = VGG_SGD,
                  graphed: bool = False, flat: bool = False, fast_bn: bool = False,
-                 stem: str = "gemm") -> App:
+                 stem: str = "gemm", data_seed: int | None = None) -> App:
+    """Weights from ``seed`` (identical replicas), batches from ``data_seed`` (per rank)."""
     import torchvision
 
     torch.manual_seed(seed)
-    return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device, seed,
-                      host_data, sgd, graphed=graphed, flat=flat, fast_bn=fast_bn, stem=stem)
+    return _image_app(torchvision.models.vgg16(), job_id, batch, iterations, device,
+                      seed if data_seed is None else data_seed, host_data, sgd, graphed=graphed,
+                      flat=flat, fast_bn=fast_bn, stem=stem)
 
 
 def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: torch.device,
              seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-4, momentum=0.9),
-             flat=False) -> App:
-    """BERT-base encoder (transformers BertModel defaults) with a masked-token-style loss."""
+             flat=False, data_seed: int | None = None) -> App:
+    """BERT-base encoder (transformers BertModel defaults) with a masked-token-style loss.
+    Weights from ``seed`` (identical replicas), token batches from ``data_seed`` (per rank)."""
     from transformers import BertConfig, BertModel
 
     torch.manual_seed(seed)
     cfg = BertConfig()
     model = BertModel(cfg, add_pooling_layer=True).to(device)
     head = torch.nn.Linear(cfg.hidden_size, cfg.vocab_size, bias=False).to(device)
-    g = torch.Generator(device="cpu").manual_seed(seed)
+    g = torch.Generator(device="cpu").manual_seed(seed if data_seed is None else data_seed)
     ids = torch.randint(0, cfg.vocab_size, (batch, seq_len), generator=g).to(device)
     labels = torch.randint(0, cfg.vocab_size, (batch, seq_len), generator=g).to(device)
 

@@ -39,7 +39,7 @@ int cuda_status(cudaError_t e, const char* where) {
 static int64_t chunks_of(int64_t numel, int chunk) { return (numel + chunk - 1) / chunk; }
 
 template <int CAP>
-static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
+static int pack_batch(const cs_pack_desc* d, int n, int max_ctas, cudaStream_t s) {
   static thread_local PackArgs<CAP> a;  // ~28 KB for the large capacity: keep off the stack
   a.n = n;
   const int chunk = reg_pack_chunk();
@@ -54,12 +54,12 @@ static int pack_batch(const cs_pack_desc* d, int n, cudaStream_t s) {
   a.chunk_begin[n] = (int)c;
   if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_pack: %lld chunks exceed grid limit", (long long)c);
   a.total_chunks = (int)c;
-  return cuda_status(launch_pack<CAP>(a, s), "cs_pack launch");
+  return cuda_status(launch_pack<CAP>(a, max_ctas, s), "cs_pack launch");
 }
 
 template <int CAP>
 static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources, int nsrc,
-                        float* snapshot, const cs_sgd_hyper* h, cudaStream_t s) {
+                        float* snapshot, const cs_sgd_hyper* h, int max_ctas, cudaStream_t s) {
   static thread_local UpdateArgs<CAP> a;
   a.n = n;
   a.nsrc = nsrc;
@@ -82,7 +82,7 @@ static int update_batch(const cs_update_desc* d, int n, const uint64_t* sources,
   a.chunk_begin[n] = (int)c;
   if (c > INT32_MAX) return set_error(CS_ERR_ARG, "cs_unpack_sgd: %lld chunks exceed grid limit", (long long)c);
   a.total_chunks = (int)c;
-  return cuda_status(launch_unpack_sgd<CAP>(a, mom, s), "cs_unpack_sgd launch");
+  return cuda_status(launch_unpack_sgd<CAP>(a, mom, max_ctas, s), "cs_unpack_sgd launch");
 }
 
 }  // namespace cs
@@ -107,9 +107,10 @@ int cs_tune(const char* key, int value) {
   return 0;
 }
 
-int cs_pack(const cs_pack_desc* descs, int n, void* stream) {
+int cs_pack(const cs_pack_desc* descs, int n, int max_ctas, void* stream) {
   if (n < 0 || (n > 0 && descs == nullptr))
     return set_error(CS_ERR_ARG, "cs_pack: invalid descriptor array (n=%d)", n);
+  if (max_ctas < 0) return set_error(CS_ERR_ARG, "cs_pack: max_ctas < 0");
   for (int i = 0; i < n; ++i) {
     if (descs[i].numel < 0)
       return set_error(CS_ERR_ARG, "cs_pack: tensor %d has negative numel", i);
@@ -119,19 +120,20 @@ int cs_pack(const cs_pack_desc* descs, int n, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   for (int b = 0; b < n; b += kCapLarge) {
     const int m = std::min(kCapLarge, n - b);
-    int rc = m <= kCapSmall ? pack_batch<kCapSmall>(descs + b, m, s)
-           : m <= kCapMid   ? pack_batch<kCapMid>(descs + b, m, s)
-                            : pack_batch<kCapLarge>(descs + b, m, s);
+    int rc = m <= kCapSmall ? pack_batch<kCapSmall>(descs + b, m, max_ctas, s)
+           : m <= kCapMid   ? pack_batch<kCapMid>(descs + b, m, max_ctas, s)
+                            : pack_batch<kCapLarge>(descs + b, m, max_ctas, s);
     if (rc) return rc;
   }
   return 0;
 }
 
 int cs_unpack_sgd(const cs_update_desc* descs, int n, const uint64_t* sources,
-                  int n_sources, float* snapshot, const cs_sgd_hyper* hyper,
+                  int n_sources, float* snapshot, const cs_sgd_hyper* hyper, int max_ctas,
                   void* stream) {
   if (n < 0 || (n > 0 && descs == nullptr))
     return set_error(CS_ERR_ARG, "cs_unpack_sgd: invalid descriptor array (n=%d)", n);
+  if (max_ctas < 0) return set_error(CS_ERR_ARG, "cs_unpack_sgd: max_ctas < 0");
   if (hyper == nullptr) return set_error(CS_ERR_ARG, "cs_unpack_sgd: hyper is NULL");
   if (n_sources < 1 || n_sources > CS_MAX_SOURCES || sources == nullptr)
     return set_error(CS_ERR_ARG, "cs_unpack_sgd: n_sources=%d outside [1, %d]", n_sources,
@@ -158,9 +160,9 @@ int cs_unpack_sgd(const cs_update_desc* descs, int n, const uint64_t* sources,
   cudaStream_t s = (cudaStream_t)stream;
   for (int b = 0; b < n; b += kCapLarge) {
     const int m = std::min(kCapLarge, n - b);
-    int rc = m <= kCapSmall ? update_batch<kCapSmall>(descs + b, m, sources, n_sources, snapshot, hyper, s)
-           : m <= kCapMid   ? update_batch<kCapMid>(descs + b, m, sources, n_sources, snapshot, hyper, s)
-                            : update_batch<kCapLarge>(descs + b, m, sources, n_sources, snapshot, hyper, s);
+    int rc = m <= kCapSmall ? update_batch<kCapSmall>(descs + b, m, sources, n_sources, snapshot, hyper, max_ctas, s)
+           : m <= kCapMid   ? update_batch<kCapMid>(descs + b, m, sources, n_sources, snapshot, hyper, max_ctas, s)
+                            : update_batch<kCapLarge>(descs + b, m, sources, n_sources, snapshot, hyper, max_ctas, s);
     if (rc) return rc;
   }
   return 0;

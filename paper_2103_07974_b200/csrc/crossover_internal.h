@@ -46,9 +46,9 @@ static_assert(sizeof(PackArgs<kCapLarge>) < 32000, "pack args exceed kernel para
 static_assert(sizeof(UpdateArgs<kCapLarge>) < 32000, "update args exceed kernel param space");
 
 template <int CAP>
-cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s);
+cudaError_t launch_pack(const PackArgs<CAP>& a, int max_ctas, cudaStream_t s);
 template <int CAP>
-cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s);
+cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, int max_ctas, cudaStream_t s);
 int reg_pack_chunk();
 int reg_update_chunk();
 extern int g_tune_reg_shape;

@@ -29,9 +29,15 @@ namespace cs {
 int g_tune_reg_shape = 1;
 int g_tune_sync_ctas = 0;   // 0: one CTA per chunk; >0: persistent grid capped at this many CTAs
 
-static int sync_grid(int chunks) {
-  return g_tune_sync_ctas > 0 && chunks > g_tune_sync_ctas ? g_tune_sync_ctas : chunks;
-}  // U=4, 3 CTAs/SM: best measured K2 shape (kbench sweep)
+// grid of K1 / K2: one CTA per chunk, or a persistent grid of at most `cap` CTAs (per-launch cap,
+// else the process-wide cs_tune("sync_ctas")).  A sync that overlaps another app's compute on a
+// high-priority stream should be persistent: a one-CTA-per-chunk grid keeps thousands of
+// high-priority CTAs pending, and the block scheduler dispatches none of the other stream's CTAs
+// until the last of them has been placed.
+static int sync_grid(int chunks, int cap) {
+  if (cap <= 0) cap = g_tune_sync_ctas;
+  return cap > 0 && chunks > cap ? cap : chunks;
+}
 
 // ---------------------------------------------------------------------------
 // 128-bit memory helpers (inline PTX so the cache policy is explicit)
@@ -290,17 +296,17 @@ int reg_pack_chunk() { return kThreads * 4 * (g_tune_reg_shape == 3 ? 8 : 4); }
 int reg_update_chunk() { return kThreads * 4 * shape_unroll(g_tune_reg_shape); }
 
 template <int CAP>
-cudaError_t launch_pack(const PackArgs<CAP>& a, cudaStream_t s) {
+cudaError_t launch_pack(const PackArgs<CAP>& a, int cap, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
-  const int g = sync_grid(a.total_chunks);
+  const int g = sync_grid(a.total_chunks, cap);
   if (g_tune_reg_shape == 3) pack_kernel<CAP, 8><<<g, kThreads, 0, s>>>(a);
   else pack_kernel<CAP, 4><<<g, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int CAP, bool kMom>
-static void launch_update_shape(const UpdateArgs<CAP>& a, cudaStream_t s) {
-  const int g = sync_grid(a.total_chunks);
+static void launch_update_shape(const UpdateArgs<CAP>& a, int cap, cudaStream_t s) {
+  const int g = sync_grid(a.total_chunks, cap);
   switch (g_tune_reg_shape) {
     case 1: unpack_sgd_kernel<CAP, kMom, 4, 3><<<g, kThreads, 0, s>>>(a); break;
     case 2: unpack_sgd_kernel<CAP, kMom, 2, 4><<<g, kThreads, 0, s>>>(a); break;
@@ -311,10 +317,10 @@ static void launch_update_shape(const UpdateArgs<CAP>& a, cudaStream_t s) {
 }
 
 template <int CAP>
-cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, cudaStream_t s) {
+cudaError_t launch_unpack_sgd(const UpdateArgs<CAP>& a, bool mom, int cap, cudaStream_t s) {
   if (a.total_chunks == 0) return cudaSuccess;
-  if (mom) launch_update_shape<CAP, true>(a, s);
-  else launch_update_shape<CAP, false>(a, s);
+  if (mom) launch_update_shape<CAP, true>(a, cap, s);
+  else launch_update_shape<CAP, false>(a, cap, s);
   return cudaGetLastError();
 }
 
@@ -351,11 +357,11 @@ cudaError_t launch_stats(const float* data, int64_t numel, double* out, void* ws
   return cudaGetLastError();
 }
 
-template cudaError_t launch_pack<kCapSmall>(const PackArgs<kCapSmall>&, cudaStream_t);
-template cudaError_t launch_pack<kCapMid>(const PackArgs<kCapMid>&, cudaStream_t);
-template cudaError_t launch_pack<kCapLarge>(const PackArgs<kCapLarge>&, cudaStream_t);
-template cudaError_t launch_unpack_sgd<kCapSmall>(const UpdateArgs<kCapSmall>&, bool, cudaStream_t);
-template cudaError_t launch_unpack_sgd<kCapMid>(const UpdateArgs<kCapMid>&, bool, cudaStream_t);
-template cudaError_t launch_unpack_sgd<kCapLarge>(const UpdateArgs<kCapLarge>&, bool, cudaStream_t);
+template cudaError_t launch_pack<kCapSmall>(const PackArgs<kCapSmall>&, int, cudaStream_t);
+template cudaError_t launch_pack<kCapMid>(const PackArgs<kCapMid>&, int, cudaStream_t);
+template cudaError_t launch_pack<kCapLarge>(const PackArgs<kCapLarge>&, int, cudaStream_t);
+template cudaError_t launch_unpack_sgd<kCapSmall>(const UpdateArgs<kCapSmall>&, bool, int, cudaStream_t);
+template cudaError_t launch_unpack_sgd<kCapMid>(const UpdateArgs<kCapMid>&, bool, int, cudaStream_t);
+template cudaError_t launch_unpack_sgd<kCapLarge>(const UpdateArgs<kCapLarge>&, bool, int, cudaStream_t);
 
 }  // namespace cs

@@ -116,7 +116,7 @@ class FusedGradientSync:
                  comm: NcclCommunicator | None = None, local_workers: int = 1,
                  align: int = 32, mode: str = "auto", snapshot_rows: int = 0,
                  flat_params: torch.Tensor | None = None, p2p_ctas: int = 0,
-                 barrier: str = "auto"):
+                 barrier: str = "auto", sync_ctas: int = 0):
         if not params:
             raise ConfigError("an app needs at least one trainable parameter")
         dev = params[0].device
@@ -127,6 +127,7 @@ class FusedGradientSync:
                 raise ConfigError("parameters must be dense fp32 tensors on one device")
         self.params = list(params)
         self.settings = settings
+        self.sync_ctas = int(sync_ctas)     # K1 / K2 persistent grid cap (0: one CTA per chunk)
         self.comm = comm
         self.ranks = comm.world if comm is not None else 1
         self.local_workers = int(local_workers)
@@ -356,7 +357,7 @@ class FusedGradientSync:
             raise ValueError(f"expected gradients of {self.local_workers} worker(s)")
         for w, grads in enumerate(grads_per_worker):
             self._pack["src"][w * n:(w + 1) * n] = _grad_ptrs(grads, self.params)
-        _lib.pack(self._pack, stream)
+        _lib.pack(self._pack, stream, self.sync_ctas)
         self.kernel_launches += 1
 
     def all_reduce(self, stream: int) -> None:
@@ -377,7 +378,7 @@ class FusedGradientSync:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
             snap = self.snapshot[snapshot_row].data_ptr()
         self._hyper.first_step = int(self.first_step)
-        _lib.unpack_sgd(self._upd, self._sources, snap, self._hyper, stream)
+        _lib.unpack_sgd(self._upd, self._sources, snap, self._hyper, stream, self.sync_ctas)
         self.first_step = False
         self.kernel_launches += 1
 

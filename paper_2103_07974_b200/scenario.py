@@ -67,14 +67,17 @@ class Scenario:
                     batch: Mapping[str, int] | None = None, time_scale: float = 1.0,
                     workers: int | None = None, policy: Policy | None = None,
                     flat: Any = False, graphed: bool = True, fast_bn: bool = True,
-                    gemm_n: int = 4096, seed: int = 0) -> SchedulePlan:
+                    gemm_n: int = 4096, seed: int = 0,
+                    data_seed: int | None = None) -> SchedulePlan:
         """The scenario's jobs as device Apps (see module docstring).
 
         ``workers`` (default ``cluster.workers``) is either the process group's world size (one
         worker per GPU) or, on a single GPU, up to 8 workers simulated back to back per job (the
         reference's own emulation, equivalence.py:171-174).  ``time_scale`` multiplies inline
         jobs' compute times before calibration (P100-era milliseconds are long); ``batch``
-        sets the per-worker batch of profile jobs (default resnet50 256, vgg16 64).
+        sets the per-worker batch of profile jobs (default resnet50 256, vgg16 64).  ``seed``
+        initialises the weights (identical on every rank), ``data_seed`` (default ``seed``) the
+        per-rank batches.
         """
         from . import apps as _apps
 
@@ -91,6 +94,7 @@ class Scenario:
             if prof is not None:
                 make = {"resnet50": _apps.resnet50_app, "vgg16": _apps.vgg16_app}[prof]
                 app = make(job.job_id, sizes[prof], job.iterations, device, seed=seed + k,
+                           data_seed=(seed if data_seed is None else data_seed) + k,
                            graphed=graphed and local == 1, flat=flat, fast_bn=fast_bn)
             else:
                 if gemm_ms is None:

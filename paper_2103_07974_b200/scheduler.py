@@ -209,7 +209,8 @@ class CrossoverScheduler:
                  record_weights: bool = False, align: int = 32, sync_mode: str = "auto",
                  time_kernels: bool = False, comm_priority: int = -1,
                  perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0,
-                 nvtx: bool = False, p2p_ctas: int | None = None, barrier: str = "auto"):
+                 nvtx: bool = False, p2p_ctas: int | None = None, barrier: str = "auto",
+                 sync_ctas: int | None = None):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -226,6 +227,7 @@ class CrossoverScheduler:
         self.watchdog_s = watchdog_s
         self.nvtx = nvtx
         self.p2p_ctas = p2p_ctas
+        self.sync_ctas = sync_ctas
         self.barrier = barrier
         with torch.cuda.device(self.device):
             self.compute_stream = torch.cuda.Stream(self.device)
@@ -262,10 +264,20 @@ class CrossoverScheduler:
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
                                  self._mode_for(app), app.iterations if self.record_weights else 0,
                                  flat_params=app.flat_params, p2p_ctas=p2p_ctas,
-                                 barrier=self.barrier)
+                                 barrier=self.barrier, sync_ctas=self._sync_grid())
         st = JobRuntimeState(app.job_id, app=app, sync=sync)
         self.states.append(st)
         return st
+
+    def _sync_grid(self) -> int:
+        """K1 / K2 grid cap.  Explicit value, else: one CTA per chunk (0).  A persistent cap
+        (e.g. 2 x SM count) keeps a high-priority sync from holding back the other app's CTAs
+        (see cs_pack in include/crossover.h); ``sync_ctas=-1`` asks for 2 CTAs per SM."""
+        if self.sync_ctas is None:
+            return 0
+        if self.sync_ctas < 0:
+            return 2 * torch.cuda.get_device_properties(self.device).multi_processor_count
+        return int(self.sync_ctas)
 
     def _mode_for(self, app: App) -> str:
         """Transport per policy when the caller left it to us.

@@ -54,7 +54,7 @@ int main(void) {
       CK(cs_event_record(bwd_done[j], cs));
       CK(cs_stream_wait_event(ms, bwd_done[j]));
       cs_pack_desc pd[2] = {{grad[j][0], bucket[j], N0}, {grad[j][1], bucket[j] + 1024, N1}};
-      CK(cs_pack(pd, 2, ms));
+      CK(cs_pack(pd, 2, 0, ms));
       cs_update_desc ud[2];
       memset(ud, 0, sizeof(ud));
       ud[0].param = param[j][0]; ud[0].grad_offset = 0; ud[0].numel = N0;
@@ -63,7 +63,7 @@ int main(void) {
       cs_sgd_hyper h;
       memset(&h, 0, sizeof(h));
       h.lr = lr; h.dampening_complement = 1.0f; h.divisor = 1; h.rounding = CS_ROUND_REFERENCE;
-      CK(cs_unpack_sgd(ud, 2, &src, 1, NULL, &h, ms));
+      CK(cs_unpack_sgd(ud, 2, &src, 1, NULL, &h, 0, ms));
       CK(cs_event_record(update_done[j], ms));
     }
   }

@@ -204,7 +204,8 @@ def case_resnet(rank, world, dev, comm, res):
     from paper_2103_07974_b200.apps import DEFAULT_IMAGE_SGD, resnet50_app
 
     steps, batch = 3, 32
-    apps = [resnet50_app(f"r{j}", batch, steps, dev, seed=1000 * j + rank, graphed=True, flat="ipc",
+    apps = [resnet50_app(f"r{j}", batch, steps, dev, seed=1000 * j, data_seed=1000 * j + rank,
+                         graphed=True, flat="ipc",
                          fast_bn=True) for j in range(2)]
     s = CrossoverScheduler(Policy.CROSSOVER, comm=comm, sync_mode="ce")
     for a in apps:

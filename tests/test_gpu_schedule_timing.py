@@ -33,7 +33,9 @@ def _run(policy, specs, dev, T):
     from paper_2103_07974_b200.apps import fixed_time_app
     from paper_2103_07974_b200.scheduler import CrossoverScheduler
 
-    s = CrossoverScheduler(policy)
+    # persistent K2 grid (2 CTAs per SM): a one-CTA-per-chunk high-priority K2 keeps thousands of
+    # CTAs pending and the other app's compute kernel is not dispatched until they are placed
+    s = CrossoverScheduler(policy, sync_ctas=-1)
     for k, (job, fwd, bwd, nbytes) in enumerate(specs):
         s.register(fixed_time_app(job, fwd, bwd, nbytes, T, dev, seed=k))
     tr = s.run()

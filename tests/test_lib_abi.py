@@ -56,7 +56,7 @@ def test_argument_errors_without_gpu():
     """Invalid calls fail in host validation with a message; nothing reaches CUDA."""
     from paper_2103_07974_b200 import _lib
 
-    assert _lib.lib.cs_pack(None, -1, None) == _lib.CS_ERR_ARG
+    assert _lib.lib.cs_pack(None, -1, 0, None) == _lib.CS_ERR_ARG
     assert b"invalid descriptor" in _lib.lib.cs_last_error()
     d = np.zeros(1, dtype=_lib.PACK_DESC)
     d["numel"] = 5
@@ -70,7 +70,7 @@ def test_argument_errors_without_gpu():
     with pytest.raises(_lib.CrossoverLibError, match="reference rounding"):
         _lib.unpack_sgd(u, np.zeros(1, dtype=np.uint64), 0, h, 0)
     assert _lib.lib.cs_unpack_sgd(u.ctypes.data, 1, np.zeros(9, dtype=np.uint64).ctypes.data, 9,
-                                  None, ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=1)), None) == _lib.CS_ERR_ARG
+                                  None, ctypes.byref(_lib.SgdHyper(lr=0.1, divisor=1)), 0, None) == _lib.CS_ERR_ARG
     assert _lib.lib.cs_nccl_init(None, 0, 0, None, 0, 0) == _lib.CS_ERR_ARG
     # BN: channel counts the kernels do not support are rejected before any launch
     assert _lib.lib.cs_bn_workspace_bytes(100, 7) == 0
