@@ -33,8 +33,15 @@ def _next_job(jobs, done, cursor):
     return None
 
 
-def crossover(jobs):
-    """Spans (in emission order) and makespan of the Alg. 1 schedule."""
+def _dur(durations, job_id, phase, t, default):
+    return default if durations is None else durations.get((job_id, phase, t), default)
+
+
+def crossover(jobs, durations=None):
+    """Spans (in emission order) and makespan of the Alg. 1 schedule.
+
+    ``durations`` optionally overrides single phases: {(job_id, phase, t): ns} (e.g. measured
+    span lengths, to predict the start times a device run must have had)."""
     gpu_free = nic_free = 0
     sync_end = [0] * len(jobs)
     done = [0] * len(jobs)
@@ -46,6 +53,8 @@ def crossover(jobs):
             break
         job_id, fwd, bwd, comm, _ = jobs[i]
         t = done[i] + 1
+        fwd, bwd = _dur(durations, job_id, "forward", t, fwd), _dur(durations, job_id, "backward", t, bwd)
+        comm = _dur(durations, job_id, "sync", t, comm)
         start = max(gpu_free, sync_end[i] if t > 1 else 0)
         mid, end = start + fwd, start + fwd + bwd
         spans += [(GPU, job_id, "forward", t, start, mid), (GPU, job_id, "backward", t, mid, end)]
@@ -58,8 +67,8 @@ def crossover(jobs):
     return spans, max((s[5] for s in spans), default=0)
 
 
-def sequential(jobs):
-    """Spans and makespan of the non-overlapped baseline."""
+def sequential(jobs, durations=None):
+    """Spans and makespan of the non-overlapped baseline (``durations`` as in crossover)."""
     now = 0
     done = [0] * len(jobs)
     spans = []
@@ -70,6 +79,8 @@ def sequential(jobs):
             break
         job_id, fwd, bwd, comm, _ = jobs[i]
         t = done[i] + 1
+        fwd, bwd = _dur(durations, job_id, "forward", t, fwd), _dur(durations, job_id, "backward", t, bwd)
+        comm = _dur(durations, job_id, "sync", t, comm)
         spans += [(GPU, job_id, "forward", t, now, now + fwd),
                   (GPU, job_id, "backward", t, now + fwd, now + fwd + bwd),
                   (NIC, job_id, "sync", t, now + fwd + bwd, now + fwd + bwd + comm)]

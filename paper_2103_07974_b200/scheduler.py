@@ -235,6 +235,13 @@ class CrossoverScheduler:
             prio = max(hi, min(lo, comm_priority))
             self.comm_stream = torch.cuda.Stream(self.device, priority=prio)
             self.h2d_stream = torch.cuda.Stream(self.device)
+            # the caching allocator keeps per-stream pools: give each stream a small- and a
+            # large-block segment now, so the first iteration's allocations do not stall the host
+            # in cudaMalloc while the device idles (it would stretch the first forward's span)
+            for st_ in (self.compute_stream, self.comm_stream, self.h2d_stream):
+                with torch.cuda.stream(st_):
+                    torch.empty(256, dtype=torch.uint8, device=self.device)
+                    torch.empty(4 << 20, dtype=torch.uint8, device=self.device)
         self.recorder = SpanRecorder(torch, record_spans)
         self.timer = _KernelTimer(self.comm_stream) if time_kernels else None
         self.states: list[JobRuntimeState] = []

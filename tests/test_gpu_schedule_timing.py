@@ -55,9 +55,13 @@ def _makespan(spans):
     return max(s[5] for s in spans)
 
 
-def _check_against_recurrence(spans, predicted, scale):
+def _check_against_recurrence(spans, rec, jobs):
+    """Every measured span start vs the reference recurrence fed with the measured durations of
+    the same spans: the device must start each phase when the reference's dependencies allow."""
+    dur = {(s[1], s[2], s[3]): s[5] - s[4] for s in spans}
+    predicted, makespan = rec(jobs, dur)
     assert [s[:4] for s in spans] == [p[:4] for p in predicted]
-    worst = max(abs(m[4] - p[4]) for m, p in zip(spans, predicted)) / scale
+    worst = max(abs(m[4] - p[4]) for m, p in zip(spans, predicted)) / makespan
     assert worst <= TOL, worst
     return worst
 
@@ -79,10 +83,9 @@ def test_golden_plan_timing_18_over_13(cuda_device):
     assert abs(_makespan(cross) / unit - 13) <= 13 * TOL
     assert abs(_makespan(seq) / unit - 18) <= 18 * TOL
     # span starts vs the recurrence with the measured durations
-    for pol, measured in ((osched.crossover, cross), (osched.sequential, seq)):
-        jobs = [(j, unit // 2, 3 * unit // 2, _sync_ns(measured, j), T) for j in ("j1", "j2")]
-        pred, pred_ms = pol(jobs)
-        _check_against_recurrence(measured, pred, pred_ms)
+    for rec, measured in ((osched.crossover, cross), (osched.sequential, seq)):
+        jobs = [(j, unit // 2, 3 * unit // 2, unit, T) for j in ("j1", "j2")]
+        _check_against_recurrence(measured, rec, jobs)
     # the crossover overlap itself: sync (j1, t) runs while j2 computes
     s1 = [s for s in cross if s[1] == "j1" and s[2] == "sync" and s[3] == 1][0]
     c2 = [s for s in cross if s[1] == "j2" and s[2] == "backward" and s[3] == 1][0]
@@ -110,5 +113,4 @@ def test_head_of_line_blocking_timing(cuda_device):
     for j in ("B", "C"):
         assert get[(j, "forward", 2)][4] >= get[("A", "backward", 2)][5] - 20_000
     jobs = [(j, unit // 2, unit // 2, _sync_ns(cross, j), T) for j in ("A", "B", "C")]
-    pred, pred_ms = osched.crossover(jobs)
-    _check_against_recurrence(cross, pred, pred_ms)
+    _check_against_recurrence(cross, osched.crossover, jobs)
