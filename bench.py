@@ -1,19 +1,20 @@
-"""Benchmark of the crossover step: two co-located ResNet-50 jobs (BASELINE.json config 2).
+"""Benchmark of the crossover step (BASELINE.json config 2 by default; --config mlp = config 1).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config resnet50|mlp]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
 
 A *step* is one rotation: every co-located job does one iteration (forward,
-backward, fused-gradient sync: K1 pack -> NCCL all-reduce -> K2 average + SGD).
+backward, fused-gradient sync: K1 pack -> bucket exchange -> K2 average + SGD).
 Rank 0 prints ONE JSON line:
 
-  value       combined images/s of both jobs under crossover, all ranks, inputs
+  value       combined samples/s of the jobs under crossover, all ranks, inputs
               resident in HBM (device-timed with CUDA events, max over ranks)
-  e2e         the same through the public API with pinned-host uint8 batches
-              copied H2D every step and every loss read back D2H
-  sequential  the back-to-back baseline with the same kernels -> speedup
-  roofline    K2 (fused average + SGD update) achieved HBM GB/s vs the measured peak
-  cpu_baseline the reference CPU path (oracle port) on a bounded sample
+  e2e         the same through the public API with pinned-host batches copied H2D
+              every step and every loss read back D2H
+  sequential  the back-to-back baseline with the same sync transport -> speedup_vs_sequential
+  roofline    the dominant sync kernel (K2 / fused P2P kernel) vs the measured peak
+  cpu_baseline the reference's CPU path on the host cores (oracle port) on a bounded sample
+              of the same workload; --impl reference prints that arm alone with the same config
 """
 
 from __future__ import annotations
@@ -43,6 +44,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="resnet50", choices=["resnet50", "mlp"],
+                    help="resnet50: BASELINE config 2 (default); mlp: config 1 (2 x MLP 784-256-10, "
+                         "W = 2 workers, batch 64; at N = 1 the two workers are simulated on one GPU)")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--jobs", type=int, default=2)
     ap.add_argument("--model", default="resnet50", choices=["resnet50", "vgg16"])
@@ -57,7 +61,9 @@ def parse():
                     help="cross-rank barrier of the p2p / ce transports: SM-free stream-memory-op "
                          "flags (auto when supported) or a 1-element NCCL all-reduce")
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
-    ap.add_argument("--sync-ctas", type=int, default=0, help="persistent grid cap of K1/K2")
+    ap.add_argument("--sync-ctas", type=int, default=None,
+                    help="persistent grid cap of K1/K2 (-1 = 2 CTAs per SM, 0 = one CTA per chunk; "
+                         "default: the scheduler's)")
     ap.add_argument("--comm-priority", default="high", choices=["high", "low"],
                     help="comm stream priority (low: the sync fills gaps left by the compute)")
     ap.add_argument("--mix", default="", help="co-located mix, e.g. resnet50:256,vgg16:32,bert:16 "
@@ -226,25 +232,81 @@ def cpu_crossover(model_name: str, jobs: int, batch: int, steps: int, warmup: in
     return jobs * batch * steps / wall, cores, wall
 
 
+def cpu_mlp(workers: int, steps: int, warmup: int):
+    """Config 1 on the host: the oracle's MLP restatement of run_crossover (fp64 numpy, the
+    reference's seeding / fixed-order averaging / sgd_step, equivalence.py:129-232) for 2 jobs x
+    `workers` workers x batch 64.  Returns (samples/s, wall s)."""
+    from oracle import sgd as osgd
+
+    specs = [(11, 0), (12, 1)]
+    osgd.run_mlp_crossover(specs, warmup, workers=workers)         # untimed (BLAS warm-up)
+    t0 = time.perf_counter()
+    osgd.run_mlp_crossover(specs, steps, workers=workers)
+    wall = time.perf_counter() - t0
+    return len(specs) * workers * 64 * steps / wall, wall
+
+
+def host_threads() -> dict:
+    import torch
+
+    info = {"cores": len(os.sched_getaffinity(0)), "torch_threads": torch.get_num_threads()}
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas"] = [{"api": d.get("internal_api"), "threads": d.get("num_threads")}
+                        for d in threadpool_info()]
+    except Exception:  # pragma: no cover - threadpoolctl is in the image
+        pass
+    return info
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` object of the bench line -- identical for both arms (ours / reference)."""
+    if args.config == "mlp":
+        w = max(2, world)
+        return {"workload": f"2x MLP 784-256-10 co-located, crossover, {w} data-parallel workers, "
+                            "batch 64/worker, SGD lr 0.05 (BASELINE config 1)",
+                "jobs": 2, "model": "mlp784-256-10", "workers": w, "batch_per_worker": 64,
+                "parallelism": f"dp{world}"}
+    return {"workload": (f"{args.jobs}x {args.model} co-located, crossover, batch {args.batch}/GPU, "
+                         "SGD momentum 0.9 (BASELINE config 2; arithmetic type in `dtype`)"),
+            "jobs": args.jobs, "model": args.model, "batch_per_gpu": args.batch,
+            "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    val, cores, wall = cpu_crossover(args.model, args.jobs, args.cpu_batch, args.steps, args.warmup)
-    sample = (f"{args.jobs} x {args.model} jobs, batch {args.cpu_batch}/job (bounded sample of "
-              f"batch {args.batch}), {args.steps} timed rotations, torch-CPU fwd/bwd + oracle "
-              f"numpy fusion/average/SGD-momentum, {wall:.1f} s")
-    line = {"metric": METRIC, "value": round(val, 3), "unit": UNIT, "impl": "reference",
+    host = host_threads()
+    if args.config == "mlp":
+        w = max(2, world)
+        val, wall = cpu_mlp(w, args.steps, args.warmup)
+        sample = (f"the whole workload: 2 MLP jobs x {w} workers (simulated serially, "
+                  f"equivalence.py:171-174) x batch 64 x {args.steps} rotations after {args.warmup} "
+                  f"warm-up, oracle fp64 numpy ({wall:.2f} s)")
+        dtype = "f64"
+    else:
+        val, _, wall = cpu_crossover(args.model, args.jobs, args.cpu_batch, args.steps, args.warmup)
+        sample = (f"{args.jobs} x {args.model} jobs, batch {args.cpu_batch}/job per rotation (bounded "
+                  f"sample of batch {args.batch}), {args.steps} timed rotations after {args.warmup} "
+                  f"warm-up, torch-CPU fwd/bwd + oracle numpy fusion/average/SGD-momentum ({wall:.1f} s)")
+        dtype = "f32"
+    line = {"metric": METRIC, "value": round(val, 3), "unit": unit_of(args), "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.jobs}x {args.model} crossover, batch {args.batch}/GPU",
-                       "jobs": args.jobs, "batch_per_gpu": args.batch, "cpu_batch": args.cpu_batch},
-            "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": round(val, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": workload_config(args, world),
+            "cpu_baseline": {"value": round(val, 3), "unit": unit_of(args), "cores": host["cores"],
+                             "kind": "port", "sample": sample, "threads": host},
+            "e2e": {"value": round(val, 3), "unit": unit_of(args), "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
     print(json.dumps(line), flush=True)
+
+
+def unit_of(args) -> str:
+    return "samples/s" if args.config == "mlp" else UNIT
 
 
 # ---------------------------------------------------------------------------
@@ -324,11 +386,13 @@ class Harness:
 
 
 P2P_CTAS: int | None = None   # --p2p-ctas; None = the scheduler's per-policy default
+SYNC_CTAS: int | None = None  # --sync-ctas; None = the scheduler's default K1 / K2 grid
 BARRIER = "auto"              # --barrier: cross-rank barrier of the p2p / ce transports
 
 
 def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
-              time_kernels: bool = True, sync_mode: str = "auto", comm_priority: int = -1):
+              time_kernels: bool = True, sync_mode: str = "auto", comm_priority: int = -1,
+              p2p_ctas: int | None = None):
     """W untimed rotations, drain + barrier, then K timed rotations (CUDA events, max over ranks).
 
     A rotation = every app in `base` steps once.  With `host_data` every step's batch is copied
@@ -340,7 +404,9 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
 
     mode = sync_mode if h.world > 1 else "auto"
     sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
-                               comm_priority=comm_priority, p2p_ctas=P2P_CTAS, barrier=BARRIER)
+                               comm_priority=comm_priority,
+                               p2p_ctas=P2P_CTAS if p2p_ctas is None else p2p_ctas,
+                               barrier=BARRIER, sync_ctas=SYNC_CTAS)
     for j, a in enumerate(base):
         sched.register(dataclasses.replace(a, iterations=W + K,
                                            data=host_data[j] if host_data else a.data))
@@ -383,9 +449,28 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     sched.drain()
     sched.close()
     out = {"ms": ms_total, "trace": trace, "timed_spans": trace.spans[n_spans0:],
+           "replicas_identical": replicas_identical(h, base),
            "kernels": sched.timer.summary() if sched.timer is not None else {},
            "launches": sched.kernel_launches - launches0, "clocks": clk_info, "sched": sched}
     return out
+
+
+def replicas_identical(h: Harness, base) -> bool | None:
+    """Data-parallel replicas must hold bitwise the same weights after every sync: compare a
+    hash of every app's parameter bits across the ranks (None at world 1)."""
+    if h.world == 1:
+        return None
+    import hashlib
+
+    import torch
+
+    dig = hashlib.sha256()
+    for a in base:
+        for p in a.params:
+            dig.update(p.detach().contiguous().view(torch.int32).cpu().numpy().tobytes())
+    allh = [None] * h.world
+    h.dist.all_gather_object(allh, dig.hexdigest())
+    return len(set(allh)) == 1
 
 
 def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
@@ -403,7 +488,8 @@ def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
         return sm, sm, None
     try:
         sched = CrossoverScheduler(Policy.CROSSOVER, comm=h.comm, sync_mode=sm, comm_priority=prio,
-                                   p2p_ctas=P2P_CTAS, barrier=BARRIER, record_spans=False)
+                                   p2p_ctas=P2P_CTAS, barrier=BARRIER, record_spans=False,
+                                   sync_ctas=SYNC_CTAS)
         for a in base:
             sched.register(dataclasses.replace(a, iterations=9))
         summary = sched.calibrate(4) if sm == "auto" else None
@@ -467,31 +553,42 @@ def kernel_summary(kern: dict, sync) -> dict:
     return out
 
 
-def run_ours(args):
-    from paper_2103_07974_b200 import apps
-    from paper_2103_07974_b200.engine import schedule_key, trace_to_chrome_json, validate_trace
-    from paper_2103_07974_b200.scheduler import Policy, overlap_roofline, rotation_schedule
+class _HostBatches:
+    """data(t, worker) -> pinned host copies of the app's device batches (the e2e path copies
+    them H2D every step through the scheduler's H2D stream)."""
 
-    h = Harness(args.nccl_max_ctas)
+    def __init__(self, device_data, iterations: int, workers):
+        self.b = {(t, w): tuple(x.cpu().pin_memory() for x in device_data(t, w))
+                  for t in range(1, iterations + 1) for w in workers}
+
+    def __call__(self, t: int, worker: int):
+        return self.b[(t, worker)]
+
+
+def build_apps(args, h):
+    """(apps, host-data callables for e2e or None, h2d bytes per step, per-app kernel launches
+    per iteration that replay inside CUDA graphs) for the selected workload."""
+    import torch
+
+    from paper_2103_07974_b200 import apps
+
     rank, world, dev = h.rank, h.world, h.dev
-    from paper_2103_07974_b200 import _lib
-    global P2P_CTAS, BARRIER
-    if args.p2p_ctas:   # override the scheduler's policy-dependent cap, both arms
-        P2P_CTAS = args.p2p_ctas
-    BARRIER = args.barrier
-    if args.sync_ctas:
-        _lib.tune("sync_ctas", args.sync_ctas)
-    if args.bn_no_pdl:
-        _lib.tune("bn_no_pdl", 1)
-    if args.side_grads:
-        from paper_2103_07974_b200 import bn as _bn
-        _bn._SIDE_GRADS = True
-    K, W = args.steps, args.warmup
-    build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
     # auto at W > 1: IPC flat parameters, and the scheduler picks the transport per policy
-    # (copy engines under crossover, the fused P2P kernel for the sequential baseline)
     flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc"}.get(args.sync_mode, False)
             if world > 1 else False)
+    if args.config == "mlp":
+        w = max(2, world)
+        local = w // world
+        iters = max(args.warmup + args.steps, 9)     # >= the transport calibration's 9 rotations
+        base = [apps.mlp_app(apps.MlpConfig(dataset_seed=11 + k, workers=w), f"mlp{k}", k, iters, dev,
+                             local_workers=local, worker_count=w, flat=flat) for k in range(2)]
+        host = None
+        h2d = 0
+        if not args.no_e2e:
+            workers = [rank * local + i for i in range(local)]
+            host = [_HostBatches(a.data, iters, workers) for a in base]
+            h2d = 2 * local * (64 * 784 * 4 + 64 * 8)
+        return base, host, h2d, 0
     if args.scenario:
         # a reference scenario file (colosim JSON) as device apps: profile jobs -> the model,
         # inline jobs -> exact tensor split + calibrated GEMM compute (paper_2103_07974_b200.scenario)
@@ -509,8 +606,7 @@ def run_ours(args):
             name, b = item.split(":")
             if name == "bert":
                 base.append(apps.bert_app(f"bert_{j}", int(b), 128, 1, dev, seed=1000 * j,
-                                          data_seed=1000 * j + rank,
-                                          flat=flat))
+                                          data_seed=1000 * j + rank, flat=flat))
             else:
                 fn = apps.resnet50_app if name == "resnet50" else apps.vgg16_app
                 base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
@@ -518,21 +614,62 @@ def run_ours(args):
                                stem="cudnn" if args.cudnn_stem else "gemm"))
         args.no_e2e, args.no_cpu_baseline = True, True
     else:
+        build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
         base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
                       graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
                       stem="cudnn" if args.cudnn_stem else "gemm")
-            for j in range(args.jobs)]
-    host_data = None if args.no_e2e else [
-        apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + j, dev, host_uint8=True))
+                for j in range(args.jobs)]
+    host = None if args.no_e2e else [
+        apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + 1000 * j + rank, dev,
+                                                     host_uint8=True))
         for j in range(args.jobs)]
-    samples_per_rot = sum(a.samples_per_batch for a in base) * world
+    h2d = args.jobs * (args.batch * 224 * 224 * 3 + args.batch * 8)
+    # NHWC BN kernels: 3 forward + 3 backward launches per BN layer per iteration, 2 per max-pool,
+    # one im2col per RGB stem (they replay inside the CUDA graphs, so they are counted from the
+    # model structure, not from Python calls)
+    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d, CrossoverMaxPool2d
+    n_bn = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverBatchNorm2d)) for a in base)
+    n_pool = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverMaxPool2d)) for a in base)
+    n_stem = 0 if args.cudnn_stem else sum(
+        sum(1 for m in a.model.modules() if isinstance(m, torch.nn.Conv2d) and m.in_channels == 3)
+        for a in base)
+    return base, host, h2d, 6 * n_bn + 2 * n_pool + n_stem
 
-    sm = args.sync_mode
+
+def run_ours(args):
+    from paper_2103_07974_b200 import _lib
+    from paper_2103_07974_b200.engine import schedule_key, trace_to_chrome_json, validate_trace
+    from paper_2103_07974_b200.scheduler import Policy, overlap_roofline, rotation_schedule
+
+    h = Harness(args.nccl_max_ctas)
+    rank, world = h.rank, h.world
+    global P2P_CTAS, BARRIER, SYNC_CTAS
+    if args.p2p_ctas:   # override the scheduler's policy-dependent cap, both arms
+        P2P_CTAS = args.p2p_ctas
+    BARRIER = args.barrier
+    SYNC_CTAS = args.sync_ctas
+    if args.bn_no_pdl:
+        _lib.tune("bn_no_pdl", 1)
+    if args.side_grads:
+        from paper_2103_07974_b200 import bn as _bn
+        _bn._SIDE_GRADS = True
+    K, W = args.steps, args.warmup
+    base, host_data, h2d_bytes, graph_launches = build_apps(args, h)
+    samples_per_rot = sum(a.samples_per_batch * a.local_workers for a in base) * world
+    unit = unit_of(args)
+
     prio = -1 if args.comm_priority == "high" else 0
-    sm, sm_seq, tuner = calibrate_transport(h, base, sm, prio)
+    sm, sm_seq_best, tuner = calibrate_transport(h, base, args.sync_mode, prio)
     args.sync_mode = sm
     cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio)
-    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq, comm_priority=prio)
+    # the same transport with the same launch caps for the sequential arm: the speedup measures
+    # the schedule alone (crossover vs back-to-back, same kernels)
+    p2p_cap = cross["sched"].states[0].sync._p2p.max_ctas if hasattr(cross["sched"].states[0].sync, "_p2p") else None
+    seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio,
+                    p2p_ctas=p2p_cap)
+    # and the fastest back-to-back configuration (full-grid P2P kernel at W > 1)
+    seq_best = seq if (sm_seq_best == sm and p2p_cap is None) else timed_run(
+        h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq_best, comm_priority=prio)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
                                              time_kernels=False, sync_mode=sm, comm_priority=prio)
 
@@ -543,84 +680,87 @@ def run_ours(args):
 
     # legality + bit-exact schedule of the measured runs
     order = [a.job_id for a in base]
-    for r in (cross, seq):
+    for r in (cross, seq, seq_best):
         assert validate_trace(r["trace"]) == [], validate_trace(r["trace"])[:3]
         assert schedule_key(r["trace"]) == rotation_schedule(order, [W + K] * len(order))
 
     comp, comm_t = phase_medians(seq["timed_spans"], order)
     roof = overlap_roofline(comp, comm_t)
-    rot_cross = cross["ms"] / K
-    rot_seq = seq["ms"] / K
+    rot_cross, rot_seq, rot_best = cross["ms"] / K, seq["ms"] / K, seq_best["ms"] / K
     value = samples_per_rot * K / (cross["ms"] / 1e3)
-    seq_value = samples_per_rot * K / (seq["ms"] / 1e3)
-
-    # NHWC BN kernels: 3 forward + 3 backward launches per BN layer per iteration (they replay
-    # inside the CUDA graphs, so they are counted from the model structure, not from Python calls)
-    from paper_2103_07974_b200.bn import CrossoverBatchNorm2d, CrossoverMaxPool2d
-    n_bn = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverBatchNorm2d)) for a in base)
-    n_pool = sum(sum(1 for m in a.model.modules() if isinstance(m, CrossoverMaxPool2d)) for a in base)
-    n_stem = 0 if args.cudnn_stem else sum(
-        sum(1 for m in a.model.modules() if isinstance(m, _torch.nn.Conv2d) and m.in_channels == 3)
-        for a in base)
-    bn_launches = 6 * n_bn + 2 * n_pool + n_stem           # + one im2col per RGB stem
     hbm_peak, peak_kind = peaks()
     sync0 = cross["sched"].states[0].sync
     kernels = kernel_summary(cross["kernels"], sync0)
-    sync_seq = seq["sched"].states[0].sync
-    kernels_isolated = kernel_summary(seq["kernels"], sync_seq)
+    sync_seq = seq_best["sched"].states[0].sync
+    kernels_isolated = kernel_summary(seq_best["kernels"], sync_seq)
 
     out = None
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            rot = 20   # ~10 s of host work on the pool's boxes
-            cv, cores, wall = cpu_crossover(args.model, args.jobs, args.cpu_batch, rot, 1)
-            cpu = {"value": round(cv, 3), "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"{args.jobs} x {args.model}, batch {args.cpu_batch}/job (bounded sample of "
-                             f"batch {args.batch}), {rot} rotations after 1 warm-up, torch-CPU fwd/bwd + "
-                             f"oracle rotation / fusion / average / SGD-momentum ({wall:.1f} s)"}
+            host = host_threads()
+            if args.config == "mlp":
+                cv, wall = cpu_mlp(2, 200, 5)
+                sample = (f"2 MLP jobs x 2 workers (simulated serially) x batch 64, 200 rotations, "
+                          f"oracle fp64 numpy ({wall:.2f} s)")
+            else:
+                rot = 20   # ~10-20 s of host work on the pool's boxes
+                cv, _, wall = cpu_crossover(args.model, args.jobs, args.cpu_batch, rot, 1)
+                sample = (f"{args.jobs} x {args.model}, batch {args.cpu_batch}/job per rotation (bounded "
+                          f"sample of batch {args.batch}), {rot} rotations after 1 warm-up, torch-CPU "
+                          f"fwd/bwd + oracle rotation / fusion / average / SGD-momentum ({wall:.1f} s)")
+            cpu = {"value": round(cv, 3), "unit": unit, "cores": host["cores"], "kind": "port",
+                   "sample": sample, "threads": host}
         e2e_line = None
         if e2e is not None:
             ev = samples_per_rot * K / (e2e["ms"] / 1e3)
-            h2d = args.jobs * (args.batch * 224 * 224 * 3 + args.batch * 8)
-            e2e_line = {"value": round(ev, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                        "d2h_bytes_per_step": args.jobs * 4}
+            e2e_line = {"value": round(ev, 2), "unit": unit, "h2d_bytes_per_step": h2d_bytes,
+                        "d2h_bytes_per_step": len(base) * 4}
+        impl = {"precision": ("fp32" if args.config == "mlp" else "bf16 autocast, fp32 params / grads / update"),
+                "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
+                              {"crossover": sync0.mode, "sequential_best": sync_seq.mode}),
+                "rank_barrier": sync0.barrier_kind, "k1_k2_grid_cap": sync0.sync_ctas or "one CTA per chunk"}
+        if args.config != "mlp":
+            impl["model_compute"] = (("fwd/bwd as CUDA graphs" if not args.no_graphs else "eager fwd/bwd")
+                                     + ("" if args.aten_bn else ", NHWC BN(+ReLU/+residual) and max-pool kernels")
+                                     + ("" if args.cudnn_stem else ", RGB stem as im2col + GEMMs"))
+        if args.mix:
+            impl["mix"] = args.mix
         out = {
-            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": round(rot_cross, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (random-init weights, N(0,1) images / random labels)",
-            "config": {"workload": (f"{args.mix} co-located, crossover" if args.scenario else
-                                    f"mix {args.mix} co-located, crossover" if args.mix else
-                                    f"{args.jobs}x {args.model} co-located, crossover, batch "
-                                    f"{args.batch}/GPU")
-                                   + ", bf16 autocast, fp32 params/grads, SGD momentum 0.9"
-                                   + ("" if args.no_graphs else ", fwd/bwd as CUDA graphs")
-                                   + ("" if args.aten_bn else ", NHWC BN(+ReLU/+residual) and max-pool kernels")
-                                   + ("" if args.cudnn_stem else ", RGB stem as im2col + GEMMs"),
-                       "jobs": len(base), "model": args.mix or args.model, "batch_per_gpu": args.batch,
-                       "parallelism": f"dp{world}", "l2": "inputs + activations >> 126 MB L2",
-                       "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
-                                     {"crossover": sync0.mode, "sequential": sync_seq.mode}),
-                       "rank_barrier": sync0.barrier_kind},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.config == "mlp" else "bf16",
+            "data": ("synthetic (seeded N(0,1) dataset, reference batch-index seeding)" if args.config == "mlp"
+                     else "synthetic (random-init weights, N(0,1) images / random labels)"),
+            "config": workload_config(args, world),
+            "impl_config": impl,
             "transport_tuner": tuner,
             "weights_finite": weights_finite,
+            "replicas_identical": cross["replicas_identical"],
             "speedup_vs_sequential": round(rot_seq / rot_cross, 4),
-            "sequential": {"value": round(seq_value, 2), "ms_per_step": round(rot_seq, 3)},
+            "sequential": {"value": round(samples_per_rot * K / (seq["ms"] / 1e3), 2),
+                           "ms_per_step": round(rot_seq, 3), "sync_mode": seq["sched"].states[0].sync.mode,
+                           "note": "same transport and launch caps as the crossover arm"},
+            "speedup_vs_best_sequential": round(rot_best / rot_cross, 4),
+            "sequential_best": {"value": round(samples_per_rot * K / (seq_best["ms"] / 1e3), 2),
+                                "ms_per_step": round(rot_best, 3), "sync_mode": sync_seq.mode},
             "rho": round(sum(comm_t) / sum(comp), 5) if sum(comp) else None,
+            "predicted_speedup": (round((sum(comp) + sum(comm_t)) / max(sum(comp), sum(comm_t)), 4)
+                                  if sum(comp) else None),
             "overlap_roofline": {"per_rotation_ms": {k: round(v, 4) for k, v in roof.items()},
                                  "measured_ms": round(rot_cross, 4),
                                  "frac": round(roof["north_star"] / rot_cross, 4),
                                  "frac_tight": round(roof["tight"] / rot_cross, 4),
                                  "comp_ms": [round(c, 4) for c in comp],
                                  "comm_ms": [round(c, 4) for c in comm_t]},
-            "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind, args.model,
+            "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind,
+                                      "mlp" if args.config == "mlp" else args.model,
                                       kernels_isolated, sync_seq),
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
-            "gpu_launches": cross["launches"] + bn_launches * K,
+            "gpu_launches": cross["launches"] + graph_launches * K,
             "gpu_launches_breakdown": {"k1_k2_p2p": cross["launches"],
-                                       "bn_and_pool_kernels": bn_launches * K},
+                                       "bn_and_pool_kernels": graph_launches * K},
             "clocks": cross["clocks"],
             "e2e": e2e_line,
             "cpu_baseline": cpu,

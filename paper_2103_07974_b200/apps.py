@@ -444,55 +444,60 @@ def synthetic_app(job_id: str, bucket_bytes: int, iterations: int, device: torch
 # apps of known compute duration (timing-level schedule tests, comm/comp sweeps)
 # ---------------------------------------------------------------------------
 class _FixedTimePhase(torch.autograd.Function):
-    """Forward and backward that each take a fixed device time (cs_spin_ns) and hand back a
-    preallocated gradient: the app's compute is exactly `forward_ns + backward_ns` of device time
+    """Forward and backward that each take a fixed device time (cs_spin_ns) and hand back
+    preallocated gradients: the app's compute is exactly `forward_ns + backward_ns` of device time
     on one SM, with no memory traffic, so measured schedules can be compared with the reference's
     recurrences in its own units (JobProfile.forward_time / backward_time, workload.py:43-56)."""
 
     @staticmethod
-    def forward(ctx, weight, forward_ns, backward_ns, grad):
+    def forward(ctx, forward_ns, backward_ns, grads, *weights):
         from . import _lib
 
-        _lib.spin_ns(forward_ns, torch.cuda.current_stream(weight.device).cuda_stream)
-        ctx.backward_ns, ctx.grad = backward_ns, grad
-        return weight.new_zeros(())
+        _lib.spin_ns(forward_ns, torch.cuda.current_stream(weights[0].device).cuda_stream)
+        ctx.backward_ns, ctx.grads = backward_ns, grads
+        return weights[0].new_zeros(())
 
     @staticmethod
     def backward(ctx, _dloss):
         from . import _lib
 
-        _lib.spin_ns(ctx.backward_ns, torch.cuda.current_stream(ctx.grad.device).cuda_stream)
-        return ctx.grad, None, None, None
+        _lib.spin_ns(ctx.backward_ns, torch.cuda.current_stream(ctx.grads[0].device).cuda_stream)
+        return (None, None, None, *ctx.grads)
 
 
 class _FixedTimeModel(torch.nn.Module):
-    def __init__(self, numel: int, device, seed: int):
+    def __init__(self, numels: list[int], device, seed: int):
         super().__init__()
         g = torch.Generator(device="cpu").manual_seed(seed)
-        base = min(numel, 1 << 20)
-        reps = (numel + base - 1) // base
 
-        def tile(scale):   # small seeded block on the host, tiled on the device
+        def tile(numel, scale):   # small seeded block on the host, tiled on the device
+            base = min(numel, 1 << 20)
+            reps = (numel + base - 1) // base
             return (torch.randn(base, generator=g) * scale).to(device).repeat(reps)[:numel].clone()
 
-        self.weight = torch.nn.Parameter(tile(0.01))
-        self.grad = tile(1e-3)      # the gradient K2 consumes every iteration (fixed address)
+        self.weights = torch.nn.ParameterList([torch.nn.Parameter(tile(n, 0.01)) for n in numels])
+        # the gradients K1 / K2 consume every iteration (fixed values, fixed addresses)
+        self.grads = tuple(tile(n, 1e-3) for n in numels)
 
 
 def fixed_time_app(job_id: str, forward_ns: int, backward_ns: int, bucket_bytes: int, iterations: int,
                    device: torch.device, seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-3, momentum=0.9),
-                   flat=False, samples_per_batch: int = 1) -> App:
+                   flat=False, samples_per_batch: int = 1,
+                   tensor_bytes: Sequence[int] | None = None) -> App:
     """An app whose forward / backward take `forward_ns` / `backward_ns` of device time and whose
-    fused gradient is `bucket_bytes` of fp32 (one tensor).  The sync is the real one (K1 / NVLink
-    transport / K2 over the bucket), so its duration is dialed by the bucket size the way
-    cli._payload_for_ratio (cli.py:79-98) dials the payload against a fixed compute time."""
-    numel = max(1, int(bucket_bytes) // 4)
-    model = _FixedTimeModel(numel, device, seed)
-    flat_params = _flatten([model.weight], flat)
+    fused gradient is `bucket_bytes` of fp32 (one tensor, or the exact split ``tensor_bytes`` of a
+    scenario job, scenario.py:114-119).  The sync is the real one (K1 / NVLink transport / K2 over
+    the bucket), so its duration is dialed by the bucket size the way cli._payload_for_ratio
+    (cli.py:79-98) dials the payload against a fixed compute time."""
+    sizes = ([max(1, (int(b) + 3) // 4) for b in tensor_bytes] if tensor_bytes is not None
+             else [max(1, int(bucket_bytes) // 4)])
+    model = _FixedTimeModel(sizes, device, seed)
+    params = list(model.weights)
+    flat_params = _flatten(params, flat)
     fwd, bwd = int(forward_ns), int(backward_ns)
 
     def loss_fn(m, batch):
-        return _FixedTimePhase.apply(m.weight, fwd, bwd, m.grad)
+        return _FixedTimePhase.apply(fwd, bwd, m.grads, *m.weights)
 
     return App(job_id, model, loss_fn, lambda t, w: (), sgd, iterations,
-               params=[model.weight], samples_per_batch=samples_per_batch, flat_params=flat_params)
+               params=params, samples_per_batch=samples_per_batch, flat_params=flat_params)
