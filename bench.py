@@ -268,6 +268,11 @@ def workload_config(args, world: int) -> dict:
                             "batch 64/worker, SGD lr 0.05 (BASELINE config 1)",
                 "jobs": 2, "model": "mlp784-256-10", "workers": w, "batch_per_worker": 64,
                 "parallelism": f"dp{world}"}
+    if args.mix or args.scenario:
+        return {"workload": f"{args.scenario or args.mix} co-located, crossover",
+                "jobs": len((args.mix or "").split(",")) if args.mix and not args.scenario else None,
+                "model": args.mix or args.scenario, "parallelism": f"dp{world}",
+                "l2": "inputs + activations >> 126 MB L2"}
     return {"workload": (f"{args.jobs}x {args.model} co-located, crossover, batch {args.batch}/GPU, "
                          "SGD momentum 0.9 (BASELINE config 2; arithmetic type in `dtype`)"),
             "jobs": args.jobs, "model": args.model, "batch_per_gpu": args.batch,

@@ -324,11 +324,12 @@ class FusedGradientSync:
         (all-gather half).  No SM moves a byte across NVLink."""
         sb = self.shard * 4
         self._recv = torch.empty(self.layout.total, dtype=torch.float32, device=self.flat.device)
-        self._ce_rs = [(self._recv.data_ptr() + s * sb, bmap.addresses[s] + off)
-                       for s in range(self.ranks) if s != self.rank]
+        # rank r pulls from r+1, r+2, ... (mod W): at every moment each GPU serves exactly one
+        # reader; pulling in rank order would make every rank read rank 0 first (one hot source)
+        peers = [(self.rank + k) % self.ranks for k in range(1, self.ranks)]
+        self._ce_rs = [(self._recv.data_ptr() + s * sb, bmap.addresses[s] + off) for s in peers]
         f = self.flat.data_ptr()
-        self._ce_ag = [(f + s * sb, fmap.addresses[s] + s * sb)
-                       for s in range(self.ranks) if s != self.rank]
+        self._ce_ag = [(f + s * sb, fmap.addresses[s] + s * sb) for s in peers]
         self._upd = np.zeros(1, dtype=_lib.UPDATE_DESC)
         self._upd["param"] = f + off
         if self.momentum_bufs is not None:

@@ -1,0 +1,156 @@
+"""The reference's speedup band and the comm/comp sweep on hardware, rho dialed like the CLI.
+
+    torchrun --nproc-per-node W tools/band.py --rho 0.1,0.15,0.2 [--compute spin|gemm]
+        [--comp-ms 4] [--sync-mode ce] [--steps 30] [--warmup 3] [--scenario-band] [--out f.json]
+
+Reference: the acceptance criterion "ratios 0.10-0.20 give 1.09x-1.21x, within 1 % of the closed
+form 1 + rho" (tests/test_acceptance.py:96-117) and the sweep's payload-for-ratio inversion
+(cli._payload_for_ratio, cli.py:79-98): for every target rho the bucket is sized so the measured
+sync takes rho x the fixed compute time.  Here the "price" of a payload is measured, not assumed:
+the sync time of the chosen transport is fitted as t(S) = a + S / B from two calibration buckets
+(sequential runs, sync alone on the GPU), and S(rho) = (rho * comp - a) * B.
+
+Two co-located apps per run (fixed_time_app: compute = spin kernel of known duration on one SM,
+or --compute gemm: a bf16 GEMM chain of the same duration), crossover and sequential with the same
+transport and launch caps.  Per rho: measured rho (sequential medians), speedup T_seq / T_cross, the
+closed form (1 + rho) / max(1, rho) (pkg/README.md:69-70), and the overlap-roofline fractions.
+--scenario-band adds the reference's own speedup_band.json jobs (124.75 MB in 4 tensors, forward :
+backward = 30 : 70) with the compute dialed to the scenario's priced rho = 3/20.
+"""
+import argparse
+import dataclasses
+import json
+import statistics
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+from bench import Harness, kernel_summary, phase_medians, timed_run  # noqa: E402
+
+MB = 2**20
+
+
+def make_apps(h, compute, comp_ns, nbytes, split=None, fwd_frac=1 / 3, gemm_ms=None):
+    from paper_2103_07974_b200.apps import fixed_time_app, synthetic_app
+
+    flat = "ipc" if h.world > 1 else False
+    if compute == "spin":
+        fwd = int(comp_ns * fwd_frac)
+        return [fixed_time_app(f"band{j}", fwd, int(comp_ns) - fwd, nbytes, 1, h.dev, seed=j, flat=flat,
+                               tensor_bytes=split) for j in range(2)]
+    reps = max(1, round(comp_ns / 1e6 / gemm_ms))
+    return [synthetic_app(f"band{j}", nbytes, 1, h.dev, gemm_n=4096, gemm_reps=reps, seed=j, flat=flat,
+                          tensor_bytes=split) for j in range(2)]
+
+
+def measure(h, base, args, policy_runs=("crossover", "sequential")):
+    from paper_2103_07974_b200.scheduler import Policy, overlap_roofline
+
+    out = {}
+    cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=args.sync_mode)
+    p2p_cap = getattr(cross["sched"].states[0].sync, "_p2p", None)
+    seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=args.sync_mode,
+                    p2p_ctas=p2p_cap.max_ctas if p2p_cap is not None else None)
+    order = [a.job_id for a in base]
+    comp, comm = phase_medians(seq["timed_spans"], order)
+    rho = sum(comm) / sum(comp)
+    roof = overlap_roofline(comp, comm)
+    rx, rs = cross["ms"] / args.steps, seq["ms"] / args.steps
+    pred = (1 + rho) / max(1.0, rho)
+    out.update({"rho_measured": round(rho, 4), "speedup": round(rs / rx, 4), "predicted": round(pred, 4),
+                "speedup_over_predicted": round(rs / rx / pred, 4),
+                "rotation_ms": {"crossover": round(rx, 4), "sequential": round(rs, 4)},
+                "overlap_roofline_frac": round(roof["north_star"] / rx, 4),
+                "overlap_roofline_frac_tight": round(roof["tight"] / rx, 4),
+                "comp_ms": round(comp[0], 4), "comm_ms": round(comm[0], 4),
+                "sync_mode": cross["sched"].states[0].sync.mode,
+                "kernels_overlapped": kernel_summary(cross["kernels"], cross["sched"].states[0].sync),
+                "kernels_isolated": kernel_summary(seq["kernels"], seq["sched"].states[0].sync),
+                "replicas_identical": cross["replicas_identical"]})
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rho", default="0.1,0.15,0.2")
+    ap.add_argument("--compute", default="spin", choices=["spin", "gemm"])
+    ap.add_argument("--comp-ms", type=float, default=4.0, help="per-app compute per iteration")
+    ap.add_argument("--sync-mode", default="ce")
+    ap.add_argument("--sync-ctas", type=int, default=-1, help="K1/K2 grid cap (-1 = 2 CTAs per SM)")
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--scenario-band", action="store_true")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    import torch
+
+    from paper_2103_07974_b200.scheduler import Policy
+
+    h = Harness()
+    bench.SYNC_CTAS = args.sync_ctas
+    if h.world == 1 and args.sync_mode in ("ce", "p2p", "auto"):
+        args.sync_mode = "auto"          # W = 1: the sync is K2 alone (direct)
+    comp_ns = args.comp_ms * 1e6
+    gemm_ms = None
+    if args.compute == "gemm":
+        from paper_2103_07974_b200.scenario import calibrate_gemm_ms
+
+        gemm_ms = calibrate_gemm_ms(h.dev, 4096)
+
+    # calibration: sync time vs payload, sync alone on the GPU (sequential policy)
+    cal = []
+    for mb in (16, 256):
+        base = make_apps(h, "spin", 400_000, mb * MB)
+        r = timed_run(h, base, Policy.SEQUENTIAL, 2, 6, sync_mode=args.sync_mode)
+        _, comm = phase_medians(r["timed_spans"], [a.job_id for a in base])
+        cal.append((mb * MB, statistics.median(comm)))
+        del base, r
+        torch.cuda.empty_cache()
+    (s1, t1), (s2, t2) = cal
+    per_byte = (t2 - t1) / (s2 - s1)
+    alpha = t1 - s1 * per_byte
+    res = {"world": h.world, "compute": args.compute, "comp_ms": args.comp_ms, "sync_mode": args.sync_mode,
+           "sync_ctas": args.sync_ctas, "steps": args.steps,
+           "calibration": {"alpha_ms": round(alpha, 5), "GB_per_s": round(1e-6 / per_byte, 1),
+                           "points": [[s, round(t, 5)] for s, t in cal]},
+           "rows": []}
+    if h.rank == 0:
+        print(json.dumps({"calibration": res["calibration"]}), flush=True)
+    for rho in [float(x) for x in args.rho.split(",")]:
+        target = rho * args.comp_ms
+        nbytes = max(MB, int((target - alpha) / per_byte))
+        nbytes -= nbytes % (128 * h.world)
+        base = make_apps(h, args.compute, comp_ns, nbytes, gemm_ms=gemm_ms)
+        row = {"rho_target": rho, "bucket_MB": round(nbytes / MB, 2), **measure(h, base, args)}
+        row["within_3pct_of_closed_form"] = abs(row["speedup_over_predicted"] - 1) <= 0.03
+        res["rows"].append(row)
+        if h.rank == 0:
+            print(json.dumps(row), flush=True)
+        del base
+        torch.cuda.empty_cache()
+    if args.scenario_band:
+        doc = json.loads((ROOT / "tests" / "golden" / "scenarios.json").read_text())
+        band = doc["files"]["speedup_band.json"]
+        split = [b for _, b in band["parsed"]["jobs"][0][4]]
+        nbytes = sum(split)
+        comm_ms = alpha + nbytes * per_byte
+        rho_ref = band["parsed"]["comm_ns"][0] / (band["parsed"]["jobs"][0][1] + band["parsed"]["jobs"][0][2])
+        comp = comm_ms / rho_ref * 1e6
+        base = make_apps(h, args.compute, comp, 0, split=split, fwd_frac=0.3, gemm_ms=gemm_ms)
+        row = {"scenario": "speedup_band.json", "rho_reference": round(rho_ref, 5),
+               "tensor_bytes": split, "comp_ms_dialed": round(comp / 1e6, 4), **measure(h, base, args)}
+        row["within_3pct_of_closed_form"] = abs(row["speedup_over_predicted"] - 1) <= 0.03
+        row["reference_band_1.09_1.21"] = 1.09 <= row["speedup"] <= 1.21
+        res["rows"].append(row)
+        if h.rank == 0:
+            print(json.dumps(row), flush=True)
+    if h.rank == 0 and args.out:
+        Path(args.out).write_text(json.dumps(res, indent=1) + "\n")
+    h.close()
+
+
+if __name__ == "__main__":
+    main()

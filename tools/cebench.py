@@ -61,11 +61,11 @@ def main():
         rpeers = exchange_peer_addresses(recv, r, W)
         row = {"size_MB": mb}
 
-        def pulls(concurrent: bool, push: bool = False, split: int = 1):
+        def pulls(concurrent: bool, push: bool = False, split: int = 1, rotated: bool = False):
             fork = ev()
             fork.record(main_s)
             joins = []
-            others = [x for x in range(W) if x != r]
+            others = ([(r + k) % W for k in range(1, W)] if rotated else [x for x in range(W) if x != r])
             part = shard // split
             k = 0
             for src in others:
@@ -88,18 +88,21 @@ def main():
             for j in joins:
                 main_s.wait_event(j)
 
-        for name, conc, push, split in (("ce_pull_serial", False, False, 1),
-                                        ("ce_pull_concurrent", True, False, 1),
-                                        ("ce_pull_concurrent_split4", True, False, 4),
-                                        ("ce_push_serial", False, True, 1),
-                                        ("ce_push_concurrent", True, True, 1),
-                                        ("ce_push_concurrent_split4", True, True, 4)):
+        for name, conc, push, split, rot in (("ce_pull_serial", False, False, 1, False),
+                                             ("ce_pull_serial_rotated", False, False, 1, True),
+                                             ("ce_pull_concurrent", True, False, 1, False),
+                                             ("ce_pull_concurrent_rotated", True, False, 1, True),
+                                             ("ce_pull_concurrent_split4", True, False, 4, False),
+                                             ("ce_push_serial", False, True, 1, False),
+                                             ("ce_push_serial_rotated", False, True, 1, True),
+                                             ("ce_push_concurrent", True, True, 1, False),
+                                             ("ce_push_concurrent_split4", True, True, 4, False)):
             ts = []
             for it in range(args.iters + 2):
                 h.barrier()
                 a, b = ev(), ev()
                 a.record(main_s)
-                pulls(conc, push, split)
+                pulls(conc, push, split, rot)
                 b.record(main_s)
                 b.synchronize()
                 if it >= 2:
@@ -133,6 +136,7 @@ def main():
         ops = {
             "none": None,
             "ce_pull_concurrent": lambda: pulls(True),
+            "ce_pull_serial_rotated": lambda: pulls(False, False, 1, True),
             "ce_push_concurrent": lambda: pulls(True, True),
             "p2p_kernel_32ctas": lambda: syncs[32]._p2p_tail(main_s.cuda_stream, None, None),
             "p2p_kernel_full": lambda: syncs[0]._p2p_tail(main_s.cuda_stream, None, None),
