@@ -225,8 +225,11 @@ int cs_ipc_open_handle(const uint8_t* handle, void** ptr) {
 int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return 0;
   if (dst == nullptr || src == nullptr) return set_error(CS_ERR_ARG, "cs_copy_async: NULL pointer");
-  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream),
-                     "cs_copy_async");
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e == cudaSuccess) return 0;
+  cudaGetLastError();
+  return set_error((int)e, "cs_copy_async(dst=%p, src=%p, %zu bytes): %s", dst, src, bytes,
+                   cudaGetErrorString(e));
 }
 
 // ---------------------------------------------------------------------------

@@ -270,6 +270,7 @@ class FusedGradientSync:
         self._flag_peers = None
         self._flags = None
         self._epoch = 0
+        self._barrier_kind = "nccl"
         nccl = getattr(self.comm, "has_collectives", True)
         if barrier == "nccl":
             if not nccl:
@@ -283,6 +284,7 @@ class FusedGradientSync:
         self._flags = FlagArray(self.rank, self.ranks)      # host shared memory, zeroed
         self._flag_peers = self._flags.peer_rows
         self._flag_local = self._flags.local_row
+        self._barrier_kind = "flags"
 
     def _rank_barrier(self, stream: int) -> None:
         if self._flag_peers is None:
@@ -297,7 +299,7 @@ class FusedGradientSync:
     def barrier_kind(self) -> str | None:
         if self.mode not in ("p2p", "ce", "adaptive"):
             return None
-        return "flags" if self._flag_peers is not None else "nccl"
+        return self._barrier_kind
 
     def set_transport(self, transport: str) -> None:
         """Pick the NVLink transport of the next syncs (adaptive mode switches freely: both

@@ -106,7 +106,8 @@ def main():
         base = make_apps(h, "spin", 400_000, mb * MB)
         r = timed_run(h, base, Policy.SEQUENTIAL, 2, 6, sync_mode=args.sync_mode)
         _, comm = phase_medians(r["timed_spans"], [a.job_id for a in base])
-        cal.append((mb * MB, statistics.median(comm)))
+        # every rank must size its buckets identically: agree on the slowest rank's time
+        cal.append((mb * MB, h.max_over_ranks(statistics.median(comm))))
         del base, r
         torch.cuda.empty_cache()
     (s1, t1), (s2, t2) = cal
