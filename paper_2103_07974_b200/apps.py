@@ -450,19 +450,29 @@ class _FixedTimePhase(torch.autograd.Function):
     recurrences in its own units (JobProfile.forward_time / backward_time, workload.py:43-56)."""
 
     @staticmethod
-    def forward(ctx, forward_ns, backward_ns, grads, *weights):
-        from . import _lib
-
-        _lib.spin_ns(forward_ns, torch.cuda.current_stream(weights[0].device).cuda_stream)
-        ctx.backward_ns, ctx.grads = backward_ns, grads
+    def forward(ctx, forward_ns, backward_ns, grads, gemm, *weights):
+        ctx.backward_ns, ctx.grads, ctx.gemm = backward_ns, grads, gemm
+        _FixedTimePhase._compute(forward_ns, gemm, weights[0].device)
         return weights[0].new_zeros(())
 
     @staticmethod
     def backward(ctx, _dloss):
-        from . import _lib
+        _FixedTimePhase._compute(ctx.backward_ns, ctx.gemm, ctx.grads[0].device)
+        return (None, None, None, None, *ctx.grads)
 
-        _lib.spin_ns(ctx.backward_ns, torch.cuda.current_stream(ctx.grads[0].device).cuda_stream)
-        return (None, None, None, *ctx.grads)
+    @staticmethod
+    def _compute(amount, gemm, device):
+        """`amount` ns of spin on one SM, or (gemm = (a, b)) `amount` chained bf16 GEMMs."""
+        if gemm is None:
+            from . import _lib
+
+            _lib.spin_ns(amount, torch.cuda.current_stream(device).cuda_stream)
+            return
+        a, b = gemm
+        with torch.no_grad():
+            x = a
+            for _ in range(int(amount)):
+                x = x @ b
 
 
 class _FixedTimeModel(torch.nn.Module):
@@ -483,21 +493,30 @@ class _FixedTimeModel(torch.nn.Module):
 def fixed_time_app(job_id: str, forward_ns: int, backward_ns: int, bucket_bytes: int, iterations: int,
                    device: torch.device, seed: int = 0, sgd: SgdSettings = SgdSettings(lr=1e-3, momentum=0.9),
                    flat=False, samples_per_batch: int = 1,
-                   tensor_bytes: Sequence[int] | None = None) -> App:
+                   tensor_bytes: Sequence[int] | None = None, gemm_n: int = 0) -> App:
     """An app whose forward / backward take `forward_ns` / `backward_ns` of device time and whose
     fused gradient is `bucket_bytes` of fp32 (one tensor, or the exact split ``tensor_bytes`` of a
     scenario job, scenario.py:114-119).  The sync is the real one (K1 / NVLink transport / K2 over
     the bucket), so its duration is dialed by the bucket size the way cli._payload_for_ratio
-    (cli.py:79-98) dials the payload against a fixed compute time."""
+    (cli.py:79-98) dials the payload against a fixed compute time.
+
+    ``gemm_n > 0`` replaces the spin kernel by real tensor-core work of fixed size: forward_ns /
+    backward_ns are then COUNTS of chained bf16 [n, n] @ [n, n] GEMMs (the gradient stays the
+    preallocated one, so the compute does not grow with the bucket)."""
     sizes = ([max(1, (int(b) + 3) // 4) for b in tensor_bytes] if tensor_bytes is not None
              else [max(1, int(bucket_bytes) // 4)])
     model = _FixedTimeModel(sizes, device, seed)
     params = list(model.weights)
     flat_params = _flatten(params, flat)
     fwd, bwd = int(forward_ns), int(backward_ns)
+    gemm = None
+    if gemm_n:
+        g = torch.Generator(device=device).manual_seed(seed)
+        gemm = (torch.randn(gemm_n, gemm_n, device=device, dtype=torch.bfloat16, generator=g),
+                torch.randn(gemm_n, gemm_n, device=device, dtype=torch.bfloat16, generator=g) / gemm_n ** 0.5)
 
     def loss_fn(m, batch):
-        return _FixedTimePhase.apply(fwd, bwd, m.grads, *m.weights)
+        return _FixedTimePhase.apply(fwd, bwd, m.grads, gemm, *m.weights)
 
     return App(job_id, model, loss_fn, lambda t, w: (), sgd, iterations,
                params=params, samples_per_batch=samples_per_batch, flat_params=flat_params)

@@ -34,16 +34,18 @@ MB = 2**20
 
 
 def make_apps(h, compute, comp_ns, nbytes, split=None, fwd_frac=1 / 3, gemm_ms=None):
-    from paper_2103_07974_b200.apps import fixed_time_app, synthetic_app
+    """Two apps of fixed compute: a spin kernel of comp_ns, or (gemm) the number of chained bf16
+    4096^3 GEMMs that takes comp_ns -- either way independent of the bucket size."""
+    from paper_2103_07974_b200.apps import fixed_time_app
 
     flat = "ipc" if h.world > 1 else False
     if compute == "spin":
-        fwd = int(comp_ns * fwd_frac)
-        return [fixed_time_app(f"band{j}", fwd, int(comp_ns) - fwd, nbytes, 1, h.dev, seed=j, flat=flat,
-                               tensor_bytes=split) for j in range(2)]
-    reps = max(1, round(comp_ns / 1e6 / gemm_ms))
-    return [synthetic_app(f"band{j}", nbytes, 1, h.dev, gemm_n=4096, gemm_reps=reps, seed=j, flat=flat,
-                          tensor_bytes=split) for j in range(2)]
+        fwd, total, n = int(comp_ns * fwd_frac), int(comp_ns), 0
+    else:
+        total = max(2, round(comp_ns / 1e6 / gemm_ms))
+        fwd, n = max(1, round(total * fwd_frac)), 4096
+    return [fixed_time_app(f"band{j}", fwd, total - fwd, nbytes, 1, h.dev, seed=j, flat=flat,
+                           tensor_bytes=split, gemm_n=n) for j in range(2)]
 
 
 def measure(h, base, args, policy_runs=("crossover", "sequential")):
