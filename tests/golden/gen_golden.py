@@ -91,7 +91,7 @@ def main() -> None:
     arrays = {}
     meta = []
     for n_jobs in (1, 2, 3):
-        for workers in (1, 2, 4):
+        for workers in (1, 2, 4, 8):
             for seed in (0, 3):
                 iters = 30
                 cfgs = [SgdConfig(learning_rate=0.05, workers=workers, loss=losses[j % 2],

@@ -34,7 +34,7 @@ def _launch(tmp_path, world: int, case: str, port: int, timeout: int = 900):
     return res
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_peer_transports_parity_one_gpu(tmp_path, world):
     """p2p / ce / adaptive at W ranks: reference golden within 1e-5 + 1e-4|w|, bitwise == W
     simulated workers (rank-order sum), bitwise across transports, ranks identical."""
