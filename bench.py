@@ -61,6 +61,9 @@ def parse():
                     help="cross-rank barrier of the p2p / ce transports: SM-free stream-memory-op "
                          "flags (auto when supported) or a 1-element NCCL all-reduce")
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
+    ap.add_argument("--rotation-graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each rotation as one CUDA graph (graphs.RotationGraph); auto = on for "
+                         "--config mlp (launch-bound), off for the image models")
     ap.add_argument("--sync-ctas", type=int, default=None,
                     help="persistent grid cap of K1/K2 (-1 = 2 CTAs per SM, 0 = one CTA per chunk; "
                          "default: the scheduler's)")
@@ -397,7 +400,7 @@ BARRIER = "auto"              # --barrier: cross-rank barrier of the p2p / ce tr
 
 def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
               time_kernels: bool = True, sync_mode: str = "auto", comm_priority: int = -1,
-              p2p_ctas: int | None = None):
+              p2p_ctas: int | None = None, graph: bool = False):
     """W untimed rotations, drain + barrier, then K timed rotations (CUDA events, max over ranks).
 
     A rotation = every app in `base` steps once.  With `host_data` every step's batch is copied
@@ -407,6 +410,8 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
 
     from paper_2103_07974_b200.scheduler import CrossoverScheduler
 
+    if graph:
+        return timed_run_graph(h, base, policy, W, K, host_data, clocks, sync_mode, comm_priority)
     mode = sync_mode if h.world > 1 else "auto"
     sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
                                comm_priority=comm_priority,
@@ -457,6 +462,83 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
            "replicas_identical": replicas_identical(h, base),
            "kernels": sched.timer.summary() if sched.timer is not None else {},
            "launches": sched.kernel_launches - launches0, "clocks": clk_info, "sched": sched}
+    return out
+
+
+def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
+                    sync_mode: str = "bucket", comm_priority: int = -1):
+    """timed_run in graph mode (paper_2103_07974_b200.graphs): W eager rotations, the graph-layout
+    rotation + capture, two untimed replays, then K timed replays (one launch per rotation).
+    With `host_data` every replay is preceded by the H2D copies of that rotation's batches into the
+    graph's static inputs (pinned host -> device) and followed by the D2H of every loss."""
+    import torch
+
+    from paper_2103_07974_b200.graphs import RotationGraph
+    from paper_2103_07974_b200.scheduler import CrossoverScheduler
+
+    mode = "bucket" if h.world == 1 else ("sharded" if sync_mode == "sharded" else "bucket")
+    sched = CrossoverScheduler(policy, comm=h.comm, sync_mode=mode, comm_priority=comm_priority,
+                               sync_ctas=SYNC_CTAS)
+    total = W + 1 + 2 + K
+    static = {}
+    regs = []
+    for j, a in enumerate(base):
+        app = dataclasses.replace(a, iterations=total)
+        if host_data:
+            workers = [h.rank * a.local_workers + w for w in range(a.local_workers)]
+            for w in workers:
+                static[(j, w)] = tuple(torch.empty_like(x, device=h.dev) for x in host_data[j](1, w))
+            app = dataclasses.replace(app, data=host_data[j],
+                                      data_graph=(lambda jj: (lambda t_dev, w: static[(jj, w)]))(j))
+        regs.append(app)
+        sched.register(app)
+    cs, ms = sched.compute_stream, sched.comm_stream
+    loss_host = torch.zeros(len(base), dtype=torch.float32).pin_memory()
+    for _ in range(W):
+        for _j in range(len(base)):
+            sched.step()
+    rg = RotationGraph(sched)
+
+    def feed(t):
+        if host_data:
+            with torch.cuda.stream(cs):
+                for (j, w), bufs in static.items():
+                    for dst, src in zip(bufs, host_data[j](t, w)):
+                        dst.copy_(src, non_blocking=True)
+
+    feed(W + 1)
+    rg.begin()
+    for _ in range(2):
+        feed(rg.t + 1)
+        rg.replay()
+    sched.drain()
+    h.barrier()
+    gc.collect()
+    gc.disable()
+    clk = Clocks(h.local) if clocks else None
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(cs)
+    for _ in range(K):
+        feed(rg.t + 1)
+        rg.replay()
+        if host_data:   # D2H of every app's loss of this rotation
+            with torch.cuda.stream(cs):
+                for j, st in enumerate(sched.states):
+                    loss_host[j:j + 1].copy_(st.graph_loss.float().view(1), non_blocking=True)
+    join = torch.cuda.Event()
+    join.record(ms)
+    cs.wait_event(join)
+    end.record(cs)
+    end.synchronize()
+    gc.enable()
+    clk_info = clk.stop() if clk else None
+    ms_total = h.max_over_ranks(start.elapsed_time(end))
+    rg.end()
+    sched.drain()
+    trace = sched.recorder.resolve()
+    out = {"ms": ms_total, "trace": trace, "timed_spans": [], "graph": rg,
+           "replicas_identical": replicas_identical(h, regs), "kernels": {},
+           "launches": K, "clocks": clk_info, "sched": sched}
     return out
 
 
@@ -584,7 +666,7 @@ def build_apps(args, h):
     if args.config == "mlp":
         w = max(2, world)
         local = w // world
-        iters = max(args.warmup + args.steps, 9)     # >= the transport calibration's 9 rotations
+        iters = max(args.warmup + args.steps + 8, 9)   # >= calibration / graph-mode prologue
         base = [apps.mlp_app(apps.MlpConfig(dataset_seed=11 + k, workers=w), f"mlp{k}", k, iters, dev,
                              local_workers=local, worker_count=w, flat=flat) for k in range(2)]
         host = None
@@ -664,40 +746,58 @@ def run_ours(args):
     unit = unit_of(args)
 
     prio = -1 if args.comm_priority == "high" else 0
-    sm, sm_seq_best, tuner = calibrate_transport(h, base, args.sync_mode, prio)
+    graph = args.rotation_graph == "on" or (args.rotation_graph == "auto" and args.config == "mlp")
+    if graph:
+        # whole-rotation CUDA graphs (graphs.RotationGraph): the bucket transport (NCCL at W > 1,
+        # simulated workers at W = 1), one graph launch per rotation for both arms
+        sm = sm_seq_best = "sharded" if args.sync_mode == "sharded" else "bucket"
+        tuner = None
+        W = max(W, 2)
+    else:
+        sm, sm_seq_best, tuner = calibrate_transport(h, base, args.sync_mode, prio)
     args.sync_mode = sm
-    cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio)
+    cross = timed_run(h, base, Policy.CROSSOVER, W, K, clocks=True, sync_mode=sm, comm_priority=prio,
+                      graph=graph)
     # the same transport with the same launch caps for the sequential arm: the speedup measures
     # the schedule alone (crossover vs back-to-back, same kernels)
     p2p_cap = cross["sched"].states[0].sync._p2p.max_ctas if hasattr(cross["sched"].states[0].sync, "_p2p") else None
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio,
-                    p2p_ctas=p2p_cap)
+                    p2p_ctas=p2p_cap, graph=graph)
     # and the fastest back-to-back configuration (full-grid P2P kernel at W > 1)
     seq_best = seq if (sm_seq_best == sm and p2p_cap is None) else timed_run(
         h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq_best, comm_priority=prio)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
-                                             time_kernels=False, sync_mode=sm, comm_priority=prio)
+                                             time_kernels=False, sync_mode=sm, comm_priority=prio,
+                                             graph=graph)
 
     # the models must still be numerically healthy: a diverged model (NaN weights) changes the
     # kernels' speed and invalidates the measurement
     import torch as _torch
     weights_finite = all(bool(_torch.isfinite(p).all()) for a in base for p in a.params)
 
-    # legality + bit-exact schedule of the measured runs
+    # legality + bit-exact schedule of the measured runs (graph mode: the eager prefix; the replays
+    # record no per-phase spans -- their schedule is the captured one, graphs.py)
     order = [a.job_id for a in base]
     for r in (cross, seq, seq_best):
         assert validate_trace(r["trace"]) == [], validate_trace(r["trace"])[:3]
-        assert schedule_key(r["trace"]) == rotation_schedule(order, [W + K] * len(order))
+        assert schedule_key(r["trace"]) == rotation_schedule(order, [W if graph else W + K] * len(order))
 
-    comp, comm_t = phase_medians(seq["timed_spans"], order)
+    hbm_peak, peak_kind = peaks()
+    sync0 = cross["sched"].states[0].sync
+    sync_seq = seq_best["sched"].states[0].sync
+    if graph:
+        comp, comm_t = cross["graph"].phase_times()
+        kernels = kernels_isolated = {"sync_graph": {"ms": round(comm_t[0], 4), "bytes": sync0.k2_bytes(),
+                                                     "GB/s": round(sync0.k2_bytes() / (comm_t[0] / 1e3) / 1e9, 1)}}
+        if world == 1:   # the sync graph is K2 alone (two simulated workers' rows)
+            kernels["k2_update"] = kernels["sync_graph"]
+    else:
+        comp, comm_t = phase_medians(seq["timed_spans"], order)
+        kernels = kernel_summary(cross["kernels"], sync0)
+        kernels_isolated = kernel_summary(seq_best["kernels"], sync_seq)
     roof = overlap_roofline(comp, comm_t)
     rot_cross, rot_seq, rot_best = cross["ms"] / K, seq["ms"] / K, seq_best["ms"] / K
     value = samples_per_rot * K / (cross["ms"] / 1e3)
-    hbm_peak, peak_kind = peaks()
-    sync0 = cross["sched"].states[0].sync
-    kernels = kernel_summary(cross["kernels"], sync0)
-    sync_seq = seq_best["sched"].states[0].sync
-    kernels_isolated = kernel_summary(seq_best["kernels"], sync_seq)
 
     out = None
     if rank == 0:
@@ -721,7 +821,8 @@ def run_ours(args):
             ev = samples_per_rot * K / (e2e["ms"] / 1e3)
             e2e_line = {"value": round(ev, 2), "unit": unit, "h2d_bytes_per_step": h2d_bytes,
                         "d2h_bytes_per_step": len(base) * 4}
-        impl = {"precision": ("fp32" if args.config == "mlp" else "bf16 autocast, fp32 params / grads / update"),
+        impl = {"rotation_graph": graph,
+                "precision": ("fp32" if args.config == "mlp" else "bf16 autocast, fp32 params / grads / update"),
                 "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
                               {"crossover": sync0.mode, "sequential_best": sync_seq.mode}),
                 "rank_barrier": sync0.barrier_kind, "k1_k2_grid_cap": sync0.sync_ctas or "one CTA per chunk"}
@@ -763,7 +864,7 @@ def run_ours(args):
                                       kernels_isolated, sync_seq),
             "kernels": kernels,
             "kernels_isolated": kernels_isolated,
-            "gpu_launches": cross["launches"] + graph_launches * K,
+            "gpu_launches": (2 * len(base) * K if graph else cross["launches"]) + graph_launches * K,
             "gpu_launches_breakdown": {"k1_k2_p2p": cross["launches"],
                                        "bn_and_pool_kernels": graph_launches * K},
             "clocks": cross["clocks"],

@@ -150,6 +150,11 @@ class _GatherData:
         sel = self.idx[t - 1, worker]
         return self.x.index_select(0, sel), self.y.index_select(0, sel)
 
+    def graph(self, t_dev: torch.Tensor, worker: int):
+        """The same batch with the iteration read from a device tensor (CUDA-graph replays)."""
+        sel = self.idx[:, worker].index_select(0, t_dev - 1).view(-1)
+        return self.x.index_select(0, sel), self.y.index_select(0, sel)
+
 
 def linear_app(config: SgdConfig, job_id: str, rng_seed: int, iterations: int,
                device: torch.device, local_workers: int | None = None, momentum: float = 0.0,
@@ -165,7 +170,7 @@ def linear_app(config: SgdConfig, job_id: str, rng_seed: int, iterations: int,
     return App(job_id, model, _linear_loss(config.loss), data,
                SgdSettings(config.learning_rate, momentum=momentum), iterations,
                local_workers=config.workers if local_workers is None else local_workers,
-               samples_per_batch=config.batch_size, flat_params=flat_params)
+               samples_per_batch=config.batch_size, flat_params=flat_params, data_graph=data.graph)
 
 
 # ---------------------------------------------------------------------------
@@ -231,7 +236,7 @@ def mlp_app(config: MlpConfig, job_id: str, rng_seed: int, iterations: int,
     return App(job_id, model, _ce_loss, data,
                SgdSettings(config.learning_rate, momentum=config.momentum), iterations,
                local_workers=config.workers if local_workers is None else local_workers,
-               samples_per_batch=config.batch_size, flat_params=flat_params)
+               samples_per_batch=config.batch_size, flat_params=flat_params, data_graph=data.graph)
 
 
 # ---------------------------------------------------------------------------
@@ -519,4 +524,5 @@ def fixed_time_app(job_id: str, forward_ns: int, backward_ns: int, bucket_bytes:
         return _FixedTimePhase.apply(fwd, bwd, m.grads, gemm, *m.weights)
 
     return App(job_id, model, loss_fn, lambda t, w: (), sgd, iterations,
-               params=params, samples_per_batch=samples_per_batch, flat_params=flat_params)
+               params=params, samples_per_batch=samples_per_batch, flat_params=flat_params,
+               data_graph=lambda t_dev, w: ())

@@ -439,6 +439,17 @@ class FusedGradientSync:
         if timer is not None:
             timer.end("k2_update")
 
+    def sync_packed(self, stream: int) -> None:
+        """The sync phase after K1 already ran (graph mode packs on the compute stream right after
+        the backward): C1 -> K2 from the bucket (bucket mode) or RS -> K2 -> AG (sharded)."""
+        if self.mode == "sharded":
+            self._sharded_tail(stream, None, None)
+            return
+        if self.mode != "bucket":
+            raise ConfigError(f"sync_packed needs bucket or sharded mode (got {self.mode!r})")
+        self.all_reduce(stream)
+        self.update(stream, None, None)
+
     def _sharded_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
         """reduce-scatter -> K2 on this rank's shard -> all-gather into the flat parameters."""
         shard_bytes = self.shard * 4

@@ -91,6 +91,9 @@ class App:
     samples_per_batch: int = 0   # for samples/s accounting (per worker)
     autocast_cache: bool = True  # must be False when the model replays CUDA graphs
     flat_params: torch.Tensor | None = None   # set by fusion.flatten_parameters (sharded sync)
+    # data_graph(t_dev, worker): the same batch as data(t, worker) with t read from a 1-element
+    # int64 device tensor -- what lets a rotation be captured once and replayed (graphs.py)
+    data_graph: Callable[[torch.Tensor, int], Sequence[torch.Tensor]] | None = None
 
     def __post_init__(self):
         if self.iterations < 1:
