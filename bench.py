@@ -535,8 +535,10 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
     ms_total = h.max_over_ranks(start.elapsed_time(end))
     rg.end()
     sched.drain()
+    phases = rg.phase_times() if policy.value == "crossover" and not host_data else None
+    rg.release()            # before the NCCL communicator goes away (graphs hold NCCL work)
     trace = sched.recorder.resolve()
-    out = {"ms": ms_total, "trace": trace, "timed_spans": [], "graph": rg,
+    out = {"ms": ms_total, "trace": trace, "timed_spans": [], "phases": phases,
            "replicas_identical": replicas_identical(h, regs), "kernels": {},
            "launches": K, "clocks": clk_info, "sched": sched}
     return out
@@ -786,7 +788,7 @@ def run_ours(args):
     sync0 = cross["sched"].states[0].sync
     sync_seq = seq_best["sched"].states[0].sync
     if graph:
-        comp, comm_t = cross["graph"].phase_times()
+        comp, comm_t = cross["phases"]
         kernels = kernels_isolated = {"sync_graph": {"ms": round(comm_t[0], 4), "bytes": sync0.k2_bytes(),
                                                      "GB/s": round(sync0.k2_bytes() / (comm_t[0] / 1e3) / 1e9, 1)}}
         if world == 1:   # the sync graph is K2 alone (two simulated workers' rows)

@@ -201,6 +201,16 @@ class RotationGraph:
             st.held = None
         sched._last_update = done
 
+    def release(self) -> None:
+        """Destroy the captured graph (and the references it keeps).  Required before the NCCL
+        communicator it captured collectives of is destroyed: ncclCommDestroy waits for graphs
+        that still hold NCCL work."""
+        if self.graph is not None:
+            torch.cuda.synchronize()
+            self.graph.reset()
+            self.graph = None
+        self._keep.clear()
+
     # -- measurement ----------------------------------------------------------------------------
     def phase_times(self, reps: int = 20) -> tuple[list[float], list[float]]:
         """Device time (ms, median of `reps` back-to-back replays) of every app's compute graph
