@@ -38,6 +38,10 @@ METRIC = "combined samples/sec of co-located jobs; crossover-vs-sequential speed
 UNIT = "images/s"
 
 
+def _grid_arg(v: str):
+    return v if v == "auto" else int(v)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -64,9 +68,9 @@ def parse():
     ap.add_argument("--rotation-graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each rotation as one CUDA graph (graphs.RotationGraph); auto = on for "
                          "--config mlp (launch-bound), off for the image models")
-    ap.add_argument("--sync-ctas", type=int, default=None,
-                    help="persistent grid cap of K1/K2 (-1 = 2 CTAs per SM, 0 = one CTA per chunk; "
-                         "default: the scheduler's)")
+    ap.add_argument("--sync-ctas", type=_grid_arg, default=None,
+                    help="persistent grid cap of K1/K2 (-1 = 2 CTAs per SM, 0 = one CTA per chunk, "
+                         "auto = measured in the untimed probe; default: the scheduler's)")
     ap.add_argument("--comm-priority", default="high", choices=["high", "low"],
                     help="comm stream priority (low: the sync fills gaps left by the compute)")
     ap.add_argument("--mix", default="", help="co-located mix, e.g. resnet50:256,vgg16:32,bert:16 "
@@ -573,8 +577,23 @@ def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
     from paper_2103_07974_b200.errors import ConfigError
     from paper_2103_07974_b200.scheduler import CrossoverScheduler, Policy
 
+    global SYNC_CTAS
+    grid = None
+    if SYNC_CTAS == "auto":
+        # measured K1 / K2 grid cap (CrossoverScheduler.calibrate_grid) in an untimed probe; both
+        # timed arms then use the chosen cap (same kernels)
+        probe = CrossoverScheduler(Policy.CROSSOVER, comm=h.comm, sync_mode=sm if h.world > 1 else "auto",
+                                   comm_priority=prio, p2p_ctas=P2P_CTAS, barrier=BARRIER,
+                                   record_spans=False, sync_ctas="auto")
+        for a in base:
+            probe.register(dataclasses.replace(a, iterations=17))
+        grid = probe.calibrate_grid(3)
+        probe.drain()
+        probe.close()
+        h.barrier()
+        SYNC_CTAS = grid["choice"] if grid else 0
     if h.world < 2 or sm not in ("p2p", "ce", "auto"):
-        return sm, sm, None
+        return sm, sm, ({"grid": grid} if grid else None)
     try:
         sched = CrossoverScheduler(Policy.CROSSOVER, comm=h.comm, sync_mode=sm, comm_priority=prio,
                                    p2p_ctas=P2P_CTAS, barrier=BARRIER, record_spans=False,
@@ -588,8 +607,8 @@ def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
         sched.close()
         h.barrier()
         if summary is not None and summary["active"]:
-            return summary["choice"], "p2p", summary
-        return sm, sm, None
+            return summary["choice"], "p2p", dict(summary, grid=grid)
+        return sm, sm, ({"grid": grid} if grid else None)
     except ConfigError as exc:
         if h.rank == 0:
             print(f"{sm} sync unavailable ({exc}); using the bucket all-reduce", file=sys.stderr)

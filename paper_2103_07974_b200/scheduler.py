@@ -213,7 +213,7 @@ class CrossoverScheduler:
                  time_kernels: bool = False, comm_priority: int = -1,
                  perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0,
                  nvtx: bool = False, p2p_ctas: int | None = None, barrier: str = "auto",
-                 sync_ctas: int | None = None):
+                 sync_ctas: int | str | None = None):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -254,6 +254,7 @@ class CrossoverScheduler:
         self._slot = 0
         self.tuner: _TransportTuner | None = None
         self.failed = False
+        self.grid_choice: dict | None = None
         self._last_compute_start = None
         self._inflight: collections.deque = collections.deque()
 
@@ -282,8 +283,9 @@ class CrossoverScheduler:
     def _sync_grid(self) -> int:
         """K1 / K2 grid cap.  Explicit value, else: one CTA per chunk (0).  A persistent cap
         (e.g. 2 x SM count) keeps a high-priority sync from holding back the other app's CTAs
-        (see cs_pack in include/crossover.h); ``sync_ctas=-1`` asks for 2 CTAs per SM."""
-        if self.sync_ctas is None:
+        (see cs_pack in include/crossover.h); ``sync_ctas=-1`` asks for 2 CTAs per SM;
+        ``sync_ctas="auto"`` starts at 0 and lets :meth:`calibrate_grid` measure the choice."""
+        if self.sync_ctas is None or self.sync_ctas == "auto":
             return 0
         if self.sync_ctas < 0:
             return 2 * torch.cuda.get_device_properties(self.device).multi_processor_count
@@ -461,6 +463,63 @@ class CrossoverScheduler:
         self.tuner.decide(medians, self.comm)
         return self.tuner.summary()
 
+    def calibrate_grid(self, rotations: int = 3, candidates: Sequence[int] | None = None) -> dict | None:
+        """Measured K1 / K2 grid cap for ``sync_ctas="auto"``.
+
+        A sync kernel on the high-priority comm stream with one CTA per chunk grabs every SM as
+        the other app's CTAs retire, so a tensor-core GEMM pays almost its whole duration; a
+        persistent grid of a few dozen CTAs co-resides with the GEMM's CTAs (a B200 SM holding
+        one 256-thread, 168-register GEMM CTA still has room for one K2 CTA) and costs the GEMM
+        ~10 % of K2's time, but runs 3-6x longer -- the right choice only while the sync has
+        slack under the other apps' compute (tools/k2_interference.py).  So it is measured like
+        the transport: every candidate cap (default: one CTA per chunk, one CTA per SM, 64, 32)
+        runs ``rotations + 1`` real rotations (the grid never changes the results), the median
+        period of each window's last ``rotations`` rotations is summed over the ranks, and every
+        rank keeps the fastest cap.  Host waits only here, outside ``step()``."""
+        if not self._started:
+            self._start()
+        if self.sync_ctas != "auto" or self.grid_choice is not None:
+            return self.grid_choice
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        cands = list(candidates) if candidates is not None else [0, sms, 64, 32]
+        per = rotations + 1
+        need = len(cands) * per + 1
+        if rotations < 2 or any(st.app.iterations - st.next_iteration + 1 < need for st in self.states):
+            return None
+        starts = []
+        for k in range(need):
+            cap = cands[min(k // per, len(cands) - 1)]
+            for st in self.states:
+                st.sync.sync_ctas = cap
+            for j in range(len(self.states)):
+                self.step()
+                if j == 0:
+                    starts.append(self._last_compute_start)
+        starts[-1].synchronize()
+        medians = []
+        for i in range(len(cands)):
+            r0 = i * per
+            p = sorted(starts[k].elapsed_time(starts[k + 1]) for k in range(r0 + 1, r0 + per))
+            medians.append(p[len(p) // 2])
+        import torch.distributed as dist
+
+        t = torch.tensor(medians, dtype=torch.float64)
+        world = self.comm.world if self.comm is not None else 1
+        if world > 1 and dist.is_initialized():
+            if dist.get_backend() == "nccl":
+                d = t.to(self.device)
+                dist.all_reduce(d)
+                t = d.cpu()
+            else:
+                dist.all_reduce(t)
+        periods = [float(x) / world for x in t]
+        best = min(range(len(cands)), key=lambda i: periods[i])
+        for st in self.states:
+            st.sync.sync_ctas = cands[best]
+        self.grid_choice = {"choice": cands[best], "candidates": cands,
+                            "period_ms": [round(x, 4) for x in periods]}
+        return self.grid_choice
+
     def _range(self, name: str):
         """NVTX range around a phase (visible in Nsight Systems) when nvtx=True."""
         return torch.cuda.nvtx.range(name) if self.nvtx else contextlib.nullcontext()
@@ -533,6 +592,8 @@ class CrossoverScheduler:
                 self._start()
             if self.tuner is not None and self._slot == 0:
                 self.calibrate()
+            if self.sync_ctas == "auto" and self.grid_choice is None:
+                self.calibrate_grid()
             while self.step():
                 pass
         finally:

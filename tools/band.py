@@ -52,6 +52,10 @@ def measure(h, base, args, policy_runs=("crossover", "sequential")):
     from paper_2103_07974_b200.scheduler import Policy, overlap_roofline
 
     out = {}
+    if args.sync_ctas == "auto":        # measured K1 / K2 grid for this point, then both arms use it
+        bench.SYNC_CTAS = "auto"
+        bench.calibrate_transport(h, base, args.sync_mode if h.world > 1 else "auto")
+        out["grid_cap"] = bench.SYNC_CTAS
     cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=args.sync_mode)
     p2p_cap = getattr(cross["sched"].states[0].sync, "_p2p", None)
     seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=args.sync_mode,
@@ -81,7 +85,9 @@ def main():
     ap.add_argument("--compute", default="spin", choices=["spin", "gemm"])
     ap.add_argument("--comp-ms", type=float, default=4.0, help="per-app compute per iteration")
     ap.add_argument("--sync-mode", default="ce")
-    ap.add_argument("--sync-ctas", type=int, default=-1, help="K1/K2 grid cap (-1 = 2 CTAs per SM)")
+    ap.add_argument("--sync-ctas", default="-1",
+                    help="K1/K2 grid cap (-1 = 2 CTAs per SM; auto = measured per rho point by "
+                         "CrossoverScheduler.calibrate_grid in an untimed probe)")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scenario-band", action="store_true")
@@ -92,7 +98,8 @@ def main():
     from paper_2103_07974_b200.scheduler import Policy
 
     h = Harness()
-    bench.SYNC_CTAS = args.sync_ctas
+    args.sync_ctas = args.sync_ctas if args.sync_ctas == "auto" else int(args.sync_ctas)
+    bench.SYNC_CTAS = -1 if args.sync_ctas == "auto" else args.sync_ctas
     if h.world == 1 and args.sync_mode in ("ce", "p2p", "auto"):
         args.sync_mode = "auto"          # W = 1: the sync is K2 alone (direct)
     comp_ns = args.comp_ms * 1e6
