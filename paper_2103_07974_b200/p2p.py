@@ -11,6 +11,7 @@ to torch zero-copy through ``__cuda_array_interface__``, and opened in the peers
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import torch
 
@@ -18,11 +19,17 @@ from . import _lib
 
 __all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping", "all_ranks_agree", "FlagArray"]
 
-_live: dict[int, "DeviceBuffer"] = {}
+# ptr -> DeviceBuffer, weakly: a buffer lives exactly as long as a tensor viewing it (torch keeps
+# the __cuda_array_interface__ provider alive as the storage's owner), then cudaFree runs
+_live: "weakref.WeakValueDictionary[int, DeviceBuffer]" = weakref.WeakValueDictionary()
 
 
 class DeviceBuffer:
-    """A zero-filled fp32 cudaMalloc allocation shown to torch as a 1-D tensor."""
+    """A zero-filled fp32 cudaMalloc allocation shown to torch as a 1-D tensor.
+
+    Ownership: the tensor owns the buffer (the buffer only keeps a weak reference back), so
+    dropping every view frees the memory; :meth:`close` frees it explicitly (after which the
+    tensor must not be used)."""
 
     def __init__(self, numel: int, device: torch.device):
         if numel <= 0:
@@ -35,9 +42,19 @@ class DeviceBuffer:
         self.device = torch.device(device)
         self.__cuda_array_interface__ = {"shape": (self.numel,), "typestr": "<f4",
                                          "data": (self.ptr, False), "version": 3, "strides": None}
-        self.tensor = torch.as_tensor(self, device=self.device)
-        assert self.tensor.data_ptr() == self.ptr
+        t = torch.as_tensor(self, device=self.device)
+        assert t.data_ptr() == self.ptr
+        self._tensor = weakref.ref(t)
+        self._first = t          # handed to the creator by the first .tensor access
         _live[self.ptr] = self
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        first, self._first = self._first, None
+        t = first if first is not None else self._tensor()
+        if t is None:
+            raise RuntimeError("DeviceBuffer: every tensor view was dropped")
+        return t
 
     def ipc_handle(self) -> bytes:
         out = (ctypes.c_uint8 * _lib.CS_IPC_HANDLE_BYTES)()
@@ -47,8 +64,16 @@ class DeviceBuffer:
     def close(self) -> None:
         if self.ptr:
             _live.pop(self.ptr, None)
-            self.tensor = None
+            self._first = None
             _lib.check("cs_device_free", _lib.lib.cs_device_free(self.ptr))
+            self.ptr = 0
+
+    def __del__(self):
+        if getattr(self, "ptr", 0):
+            try:
+                _lib.lib.cs_device_free(self.ptr)
+            except Exception:   # interpreter shutdown: the context may already be gone
+                pass
             self.ptr = 0
 
 

@@ -188,7 +188,7 @@ def main():
             for t in range(T):
                 for i, o in enumerate(lay.offsets):
                     r = ref[k][t][i].reshape(-1)
-                    worst = max(worst, float(np.max(np.abs(w[t, o:o + r.size] - r) / (1e-5 + 1e-3 * np.abs(r)))))
+                    worst = max(worst, float(np.max(np.abs(w[t, o:o + r.size] - r) / (1e-5 + 1e-4 * np.abs(r)))))
         res["checks"].append({"name": "mlp_vs_oracle", "ok": worst <= 1.0, "worst_ratio": worst})
 
         jobs = [osgd.LinearJob(0.05, world, c.loss.value, c.dataset_seed, 40 + k) for k, c in enumerate(lcfg)]

@@ -247,10 +247,14 @@ def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum):
         acc = acc + sr.cpu()                              # rank order, fp32, one rounding per add
     avg = acc / world
     if momentum:
-        buf = m0 * 0.9 + avg                              # mul rounded, then the add (fma(1, g, t))
-        want = torch.addcmul(p0, buf, torch.full_like(buf, -0.05))   # fused p - lr * buf
-        assert torch.equal(mom.cpu(), buf)
-        torch.testing.assert_close(dsts[0].cpu(), want, rtol=0, atol=1e-6)
+        # torch.optim.SGD itself on the CPU (foreach=False): buf = 0.9 buf + g, p -= lr buf
+        q = torch.nn.Parameter(p0.clone())
+        opt = torch.optim.SGD([q], lr=0.05, momentum=0.9, foreach=False)
+        opt.state[q]["momentum_buffer"] = m0.clone()
+        q.grad = avg
+        opt.step()
+        assert torch.equal(mom.cpu(), opt.state[q]["momentum_buffer"])
+        assert torch.equal(dsts[0].cpu(), q.detach())
     else:
         want = p0 - torch.tensor(0.05, dtype=torch.float32) * avg
         assert torch.equal(dsts[0].cpu(), want)

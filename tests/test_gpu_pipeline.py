@@ -144,7 +144,7 @@ def test_mlp_config1_matches_oracle(cuda_device):
             for i, o in enumerate(lay.offsets):
                 r = ref[k][t][i].reshape(-1)
                 g = w[t, o:o + r.size]
-                ratio = np.abs(g - r) / (1e-5 + 1e-3 * np.abs(r))
+                ratio = np.abs(g - r) / (1e-5 + 1e-4 * np.abs(r))   # the L3 bar
                 worst = max(worst, float(ratio.max()))
     assert worst <= 1.0, worst
 
