@@ -183,23 +183,27 @@ CS_API int cs_ipc_close_handle(void* ptr);
  * local or peer-mapped (IPC) device memory, so a pull from a peer crosses NVLink without
  * occupying any SM -- the transport of the "ce" sync mode. */
 CS_API int cs_copy_async(void* dst, const void* src, size_t bytes, void* stream);
-/* Cross-rank barrier without SMs: stream memory operations on uint32 flag arrays (device memory
- * mapped over IPC, or host shared memory registered with cs_host_register).
- * Rank r writes `epoch` into slot r of every peer's array (peer_flags[p] = rank p's array as
- * mapped here; a system-scope fence orders all earlier work of the stream before each write),
- * then the stream waits until every peer's slot in its own array (local_flags) is >= epoch
- * (cyclic compare).  Every rank must call it with the same epoch sequence.  Replaces the
- * 1-element NCCL all-reduce barriers of the p2p / ce transports, whose kernels need a free SM
- * while the other app's GEMMs occupy them. */
+/* Cross-rank barrier without SMs: stream memory operations on uint32 flag rows (host shared
+ * memory registered with cs_host_register, or IPC-mapped device memory), constant values only, so
+ * the same sequence can be captured into a CUDA graph and replayed:
+ *   arrive  write 1 into slot `rank` of every peer's row (peer_rows[p] = rank p's row as mapped
+ *           here; a system-scope fence orders all earlier work of the stream before each write)
+ *   wait    until every peer's slot in this rank's row (local_row) is 1
+ *   reset   write 0 into this rank's row
+ * A transport that needs two barriers per sync (p2p, ce) uses two separate rows ("phases") per
+ * rank and always passes them in the same order: a peer can only arrive at phase X again after
+ * passing the other phase, which this rank enters only after it reset phase X -- so no arrival
+ * is lost and no reset erases a fresh one.  Replaces the 1-element NCCL all-reduce barriers, whose
+ * kernels need a free SM while the other app's GEMMs occupy them. */
 CS_API int cs_stream_memops_supported(void);
 /* Page-locked, device-mapped host memory for the flag arrays (cudaHostRegister, mapped +
  * portable).  The p2p / ce transports keep their barrier flags in one host shared-memory segment
  * mapped by every rank of the node, so a host can release every rank's pending waits on failure
- * (write a final epoch into the segment) without issuing any GPU work. */
+ * (keep writing 1 into the segment until the streams drained) without issuing any GPU work. */
 CS_API int cs_host_register(void* ptr, size_t bytes, void** dev_ptr);
 CS_API int cs_host_unregister(void* ptr);
-CS_API int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, int nranks,
-                           uint32_t epoch, void* stream);
+CS_API int cs_flag_barrier(const uint64_t* peer_rows, uint64_t local_row, int rank, int nranks,
+                           void* stream);
 
 /* channels_last BatchNorm2d (training) for the apps' compute: x / y / dy / dx / residual are
  * bf16 [M, C] row-major (M = N*H*W, C % 8 == 0, C <= 256 or C % 256 == 0), weight / bias /

@@ -85,8 +85,8 @@ EXPORTS = {
     "cs_stream_memops_supported": ([], ctypes.c_int),
     "cs_host_register": ([ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "cs_host_unregister": ([ctypes.c_void_p], ctypes.c_int),
-    "cs_flag_barrier": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
-                         ctypes.c_void_p], ctypes.c_int),
+    "cs_flag_barrier": ([ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p],
+                        ctypes.c_int),
     "cs_bn_workspace_bytes": ([ctypes.c_int64, ctypes.c_int], ctypes.c_size_t),
     "cs_bn_forward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float, ctypes.c_float,

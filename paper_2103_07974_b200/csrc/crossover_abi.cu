@@ -266,11 +266,14 @@ int cs_stream_memops_supported(void) {
   return g_memops_status == 0 ? 1 : 0;
 }
 
-int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, int nranks,
-                    uint32_t epoch, void* stream) {
-  if (peer_flags == nullptr || local_flags == 0 || nranks < 1 || nranks > CS_MAX_SOURCES ||
+int cs_flag_barrier(const uint64_t* peer_rows, uint64_t local_row, int rank, int nranks,
+                    void* stream) {
+  if (peer_rows == nullptr || local_row == 0 || nranks < 1 || nranks > CS_MAX_SOURCES ||
       rank < 0 || rank >= nranks)
     return set_error(CS_ERR_ARG, "cs_flag_barrier: invalid arguments");
+  for (int p = 0; p < nranks; ++p)
+    if (p != rank && peer_rows[p] == 0)
+      return set_error(CS_ERR_ARG, "cs_flag_barrier: NULL flag row of rank %d", p);
   std::call_once(g_memops_once, load_memops);
   if (g_memops_status)
     return set_error(g_memops_status, "cs_flag_barrier: stream memory operations unavailable");
@@ -292,20 +295,26 @@ int cs_flag_barrier(const uint64_t* peer_flags, uint64_t local_flags, int rank, 
     }
     can_flush = flush_cache[dev] == 2;
   }
-  const unsigned int wait_flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
-  // announce: my slot in every peer's flag array (a system-scope fence precedes each write, so
+  const unsigned int wait_flags = CU_STREAM_WAIT_VALUE_EQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+  // arrive: 1 into my slot of every peer's row (a system-scope fence precedes each write, so
   // everything this stream did before is visible to the peer that observes the flag)
   for (int p = 0; p < nranks; ++p) {
     if (p == rank) continue;
-    if (peer_flags[p] == 0) return set_error(CS_ERR_ARG, "cs_flag_barrier: NULL flag array of rank %d", p);
-    CUresult r = g_write32(s, (CUdeviceptr)(peer_flags[p] + 4u * (uint64_t)rank), epoch, 0);
+    CUresult r = g_write32(s, (CUdeviceptr)(peer_rows[p] + 4u * (uint64_t)rank), 1u, 0);
     if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: write to rank %d failed (%d)", p, (int)r);
   }
-  // wait: every peer's slot in my array has reached this epoch (cyclic >=)
+  // wait: every peer's slot in my row is 1
   for (int p = 0; p < nranks; ++p) {
     if (p == rank) continue;
-    CUresult r = g_wait32(s, (CUdeviceptr)(local_flags + 4u * (uint64_t)p), epoch, wait_flags);
+    CUresult r = g_wait32(s, (CUdeviceptr)(local_row + 4u * (uint64_t)p), 1u, wait_flags);
     if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: wait on rank %d failed (%d)", p, (int)r);
+  }
+  // reset my row (no fence needed: only this rank reads it, in stream order)
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) continue;
+    CUresult r = g_write32(s, (CUdeviceptr)(local_row + 4u * (uint64_t)p), 0u,
+                           CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER);
+    if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: reset of slot %d failed (%d)", p, (int)r);
   }
   return 0;
 }

@@ -269,7 +269,6 @@ class FusedGradientSync:
             raise ConfigError(f"unknown barrier {barrier!r}")
         self._flag_peers = None
         self._flags = None
-        self._epoch = 0
         self._barrier_kind = "nccl"
         nccl = getattr(self.comm, "has_collectives", True)
         if barrier == "nccl":
@@ -282,18 +281,19 @@ class FusedGradientSync:
                 raise ConfigError("stream memory operations are not supported on every rank")
             return
         self._flags = FlagArray(self.rank, self.ranks)      # host shared memory, zeroed
-        self._flag_peers = self._flags.peer_rows
-        self._flag_local = self._flags.local_row
+        self._flag_peers = self._flags.peer_rows               # per phase
+        self._flag_local = self._flags.local_rows
         self._barrier_kind = "flags"
 
-    def _rank_barrier(self, stream: int) -> None:
+    def _rank_barrier(self, stream: int, phase: int) -> None:
+        """Barrier `phase` (0: every rank's K1 landed; 1: every shard updated and every bucket
+        read) of one sync.  The flag protocol is constant-valued and self-resetting (graph-safe)."""
         if self._flag_peers is None:
             self.comm.all_reduce_(self._barrier.data_ptr(), 1, stream)
             return
-        self._epoch = (self._epoch + 1) & 0xFFFFFFFF
+        peers = self._flag_peers[phase]
         _lib.check("cs_flag_barrier", _lib.lib.cs_flag_barrier(
-            self._flag_peers.ctypes.data, self._flag_local, self.rank, self.ranks, self._epoch,
-            stream))
+            peers.ctypes.data, self._flag_local[phase], self.rank, self.ranks, stream))
 
     @property
     def barrier_kind(self) -> str | None:
@@ -441,14 +441,19 @@ class FusedGradientSync:
 
     def sync_packed(self, stream: int) -> None:
         """The sync phase after K1 already ran (graph mode packs on the compute stream right after
-        the backward): C1 -> K2 from the bucket (bucket mode) or RS -> K2 -> AG (sharded)."""
+        the backward): C1 -> K2 from the bucket (bucket), RS -> K2 -> AG (sharded), or the peer
+        transports' barrier / exchange / update / barrier (p2p, ce)."""
         if self.mode == "sharded":
             self._sharded_tail(stream, None, None)
-            return
-        if self.mode != "bucket":
-            raise ConfigError(f"sync_packed needs bucket or sharded mode (got {self.mode!r})")
-        self.all_reduce(stream)
-        self.update(stream, None, None)
+        elif self.transport == "p2p":
+            self._p2p_tail(stream, None, None)
+        elif self.transport == "ce":
+            self._ce_tail(stream, None, None)
+        elif self.mode == "bucket":
+            self.all_reduce(stream)
+            self.update(stream, None, None)
+        else:
+            raise ConfigError(f"sync_packed has no {self.mode!r} path (direct / unfused read the gradients)")
 
     def _sharded_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
         """reduce-scatter -> K2 on this rank's shard -> all-gather into the flat parameters."""
@@ -476,7 +481,7 @@ class FusedGradientSync:
 
     def _p2p_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
         """barrier -> fused reduce + update + all-gather over NVLink -> barrier."""
-        self._rank_barrier(stream)                     # every rank's K1 has landed
+        self._rank_barrier(stream, 0)                  # every rank's K1 has landed
         if timer is not None:
             timer.begin("k2_p2p_fused")
         self._hyper.first_step = int(self.first_step)
@@ -486,7 +491,7 @@ class FusedGradientSync:
         self.kernel_launches += 1
         if timer is not None:
             timer.end("k2_p2p_fused")
-        self._rank_barrier(stream)                     # every rank's parameter writes landed
+        self._rank_barrier(stream, 1)                  # every rank's parameter writes landed
         if snapshot_row is not None:
             if self.snapshot is None:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
@@ -506,7 +511,7 @@ class FusedGradientSync:
         pulls it, every peer has finished reading my bucket before my next K1 rewrites it, and
         (by stream order on each peer) a peer's all-gather pulls of iteration t complete before
         it enters iteration t+1's first barrier, so my K2 at t+1 never races them."""
-        self._rank_barrier(stream)                     # every rank's K1 has landed
+        self._rank_barrier(stream, 0)                  # every rank's K1 has landed
         if timer is not None:
             timer.begin("c1_ce_reduce_scatter")
         self._ce_copies(self._ce_rs, stream)
@@ -516,7 +521,7 @@ class FusedGradientSync:
         self.update(stream, None, None)
         if timer is not None:
             timer.end("k2_update")
-        self._rank_barrier(stream)                     # every shard updated, every bucket read
+        self._rank_barrier(stream, 1)                  # every shard updated, every bucket read
         if timer is not None:
             timer.begin("c1_ce_all_gather")
         self._ce_copies(self._ce_ag, stream)
@@ -531,9 +536,10 @@ class FusedGradientSync:
     def release_waits(self) -> None:
         """Failure path: satisfy every pending flag-barrier wait of every rank (host writes into
         the shared flag segment, no GPU work), so no comm stream stays blocked behind a peer that
-        stopped.  The transport is unusable afterwards."""
+        stopped.  Each released wait resets its row, so the caller repeats this until the device
+        drained.  The transport is unusable afterwards."""
         if self._flags is not None:
-            self._flags.release(self._epoch)
+            self._flags.release()
             self.failed = True
 
     def close(self) -> None:

@@ -24,8 +24,10 @@ Graph layout differences from eager ``step()``: K1 (pack) runs on the compute st
 the backward -- so the deferred sync reads the app's own bucket (a fixed address) instead of the
 graph's gradient buffers -- and the sync is C1 + K2 (``FusedGradientSync.sync_packed``).  Batches come
 from ``App.data_graph(t_dev, worker)`` with the iteration in a device counter incremented by the
-graph itself.  Transports with host-side barrier epochs (p2p / ce) are not capturable; bucket
-(NCCL all-reduce, or W simulated workers on one GPU) and sharded (NCCL RS/AG) are.  Spans are not
+graph itself.  Every transport is capturable: bucket (NCCL all-reduce, or W simulated workers on one
+GPU), sharded (NCCL RS/AG), and the peer transports p2p / ce, whose flag barriers are constant-valued
+and self-resetting stream memory operations (cs_flag_barrier) and whose copy-engine pulls become
+memcpy nodes; the adaptive transport is frozen at its calibrated choice.  Spans are not
 recorded per phase inside replays (one graph launch per rotation); :meth:`phase_times` measures
 each app's compute and sync as separate graphs instead.
 """
@@ -56,9 +58,9 @@ class RotationGraph:
         for st in sched.states:
             if st.app.data_graph is None:
                 raise ConfigError(f"job {st.job_id!r}: graph mode needs App.data_graph")
-            if st.sync.mode not in ("bucket", "sharded"):
-                raise ConfigError(f"job {st.job_id!r}: graph mode needs the bucket or sharded sync "
-                                  f"(got {st.sync.mode!r}; p2p / ce barriers carry host epochs)")
+            if st.sync.mode not in ("bucket", "sharded", "p2p", "ce", "adaptive"):
+                raise ConfigError(f"job {st.job_id!r}: graph mode needs a bucket transport "
+                                  f"(got {st.sync.mode!r})")
             if st.sync.snapshot is not None:
                 raise ConfigError("graph mode does not record per-iteration weights")
         if sched.timer is not None:

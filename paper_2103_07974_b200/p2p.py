@@ -142,14 +142,18 @@ def all_ranks_agree(ok: bool) -> bool:
 class FlagArray:
     """The barrier flags of one app's p2p / ce transport, shared by every rank of the node.
 
-    A W x W uint32 matrix in one POSIX shared-memory segment (rank 0 creates it, the others attach
-    by name, every rank page-locks and device-maps it with cs_host_register).  Row r holds the flags
-    rank r waits on; rank p writes column p of every row (cs_flag_barrier: peer_flags[p] = row p,
-    local_flags = row r).  The GPU front ends write and poll it with stream memory operations, so a
-    barrier still occupies no SM.  Because the host can write the segment directly, a watchdog can
-    release every rank's pending waits without issuing GPU work (:meth:`release`), which a wait on
-    device memory behind a blocked stream could not guarantee.
+    Two phases (a sync passes two barriers: every rank's K1 landed; every shard updated / every
+    bucket read), each a W x W uint32 matrix, in one POSIX shared-memory segment (rank 0 creates
+    it, the others attach by name, every rank page-locks and device-maps it with
+    cs_host_register).  Row r of a phase holds the flags rank r waits on; rank p writes column p
+    of every row (cs_flag_barrier).  The GPU front ends write, poll and reset it with constant-value
+    stream memory operations, so a barrier occupies no SM and can be captured into a CUDA graph.
+    Because the host can write the segment directly, a watchdog can release every rank's pending
+    waits without issuing GPU work (:meth:`release`), which a wait on device memory behind a
+    blocked stream could not guarantee.
     """
+
+    PHASES = 2
 
     def __init__(self, rank: int, world: int):
         import torch.distributed as dist
@@ -160,7 +164,7 @@ class FlagArray:
         from .errors import ConfigError
 
         self.rank, self.world = rank, world
-        nbytes = 4 * world * world
+        nbytes = 4 * self.PHASES * world * world
         self._size = max(4096, nbytes)
         self._shm = None
         name = [None]
@@ -184,7 +188,7 @@ class FlagArray:
                 error = f"rank {rank}: cannot attach the flag segment: {exc}"
         self._dev = 0
         if self._shm is not None and not error:
-            self._host = np.ndarray((world, world), dtype=np.uint32, buffer=self._shm.buf)
+            self._host = np.ndarray((self.PHASES, world, world), dtype=np.uint32, buffer=self._shm.buf)
             if rank == 0:
                 self._host[:] = 0
             addr = ctypes.addressof(ctypes.c_char.from_buffer(self._shm.buf))
@@ -201,15 +205,17 @@ class FlagArray:
         if not ok:
             self.close()
             raise ConfigError("flag segment setup failed on some rank" + (f" ({error})" if error else ""))
-        self.peer_rows = np.asarray([self._dev + 4 * world * p for p in range(world)], dtype=np.uint64)
-        self.local_row = self._dev + 4 * world * rank
+        w2 = world * world
+        self.peer_rows = [np.asarray([self._dev + 4 * (ph * w2 + p * world) for p in range(world)],
+                                     dtype=np.uint64) for ph in range(self.PHASES)]
+        self.local_rows = [self._dev + 4 * (ph * w2 + rank * world) for ph in range(self.PHASES)]
 
-    def release(self, epoch: int) -> None:
-        """Satisfy every pending wait of every rank: write an epoch far ahead (cyclic compare) of
-        anything enqueued into the whole matrix.  Only for failure handling -- afterwards the flags
-        no longer order anything, so the owning transport must not be used again."""
+    def release(self) -> None:
+        """Satisfy every pending wait of every rank: write 1 into every slot.  A released wait is
+        followed by its own reset, so the caller repeats this until the streams drained.  Only for
+        failure handling -- afterwards the flags order nothing, so the transport is retired."""
         if self._dev:
-            self._host[:] = (int(epoch) + (1 << 30)) & 0xFFFFFFFF
+            self._host[:] = 1
 
     def close(self) -> None:
         if getattr(self, "_dev", 0):

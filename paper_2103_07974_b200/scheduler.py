@@ -561,19 +561,21 @@ class CrossoverScheduler:
         """Failure path: unblock the device, then raise DeadlockError(job, iteration).
 
         NCCL kernels waiting for a dead peer end with ncclCommAbort; flag-barrier waits (stream
-        memory operations, which no abort can cancel) are satisfied by writing a final epoch into
-        the shared flag segments from the host.  The queued work then drains (its results are
+        memory operations, which no abort can cancel) are satisfied by writing 1 into the shared
+        flag segments from the host, repeatedly until the comm stream drained.  The queued work then drains (its results are
         garbage and the syncs are marked failed), so later synchronize / teardown calls return."""
         pending = [(j, t) for j, t, e in self._inflight if not e.query()]
         job, it = pending[0] if pending else (self.states[0].job_id, self.states[0].next_iteration)
         if self.comm is not None:
             self.comm.abort()
-        for st in self.states:
-            st.sync.release_waits()
         done = torch.cuda.Event()
         done.record(self.comm_stream)
         t0 = time.monotonic()
-        while not done.query() and time.monotonic() - t0 < 30.0:
+        while True:
+            for st in self.states:          # a released wait resets its row: keep releasing
+                st.sync.release_waits()
+            if done.query() or time.monotonic() - t0 > 30.0:
+                break
             time.sleep(0.001)
         self.failed = True
         raise DeadlockError(job, it, f"policy={self.policy.value}; {detail}")

@@ -18,6 +18,8 @@ CASE parity   golden linear jobs (reference fp64 trajectories, equivalence.py:15
 CASE fail     rank 1 stops issuing work after two slots; rank 0's watchdog must raise
               DeadlockError(job, iteration) and its device must drain (no stream stays blocked
               in a flag-barrier wait), all within seconds.
+CASE graph    whole-rotation CUDA graphs over ce and p2p (captured flag barriers, CE memcpy nodes,
+              the P2P kernel): final weights bitwise equal to the eager run.
 CASE resnet   two ResNet-50 apps (bf16 autocast, CUDA graphs, momentum 0.9, weight decay 1e-4)
               through ce for 3 iterations: every rank's update equals torch.optim.SGD
               (foreach=False) on the CPU applied to the rank-order average of the W ranks'
@@ -198,6 +200,43 @@ def case_fail(rank, world, dev, comm, res):
     dist.barrier()
 
 
+def case_graph(rank, world, dev, comm, res):
+    """Whole-rotation CUDA graphs over the peer transports: the flag barriers (constant-valued,
+    self-resetting stream memory operations), the copy-engine pulls and the P2P kernel captured
+    once and replayed; final weights bitwise equal to the eager run of the same transport."""
+    from paper_2103_07974_b200.graphs import RotationGraph
+
+    T = 12
+    specs = [(11, 0), (12, 1)]
+    for mode in ("ce", "p2p"):
+        finals = {}
+        for graph in (False, True):
+            apps = [mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"g{k}", rs, T, dev,
+                            local_workers=1, worker_count=world, flat="ipc") for k, (ds, rs) in enumerate(specs)]
+            s = CrossoverScheduler(Policy.CROSSOVER, comm=comm, sync_mode=mode)
+            for a in apps:
+                s.register(a)
+            if graph:
+                for _ in range(2 * len(apps)):
+                    s.step()
+                rg = RotationGraph(s)
+                rg.begin()
+                while rg.t < T:
+                    rg.replay()
+                rg.end()
+                s.drain()
+                rg.release()
+            else:
+                s.run()
+            finals[graph] = [torch.cat([p.detach().reshape(-1) for p in a.params]).cpu() for a in apps]
+            s.close()
+        same = all(torch.equal(a.view(torch.int32), b.view(torch.int32))
+                   for a, b in zip(finals[False], finals[True]))
+        res["checks"].append({"name": f"graph_{mode}_bitwise_eq_eager_w{world}", "ok": same})
+        res["checks"].append({"name": f"graph_{mode}_ranks_identical",
+                              "ok": _gather_equal(torch.cat(finals[True]), rank, world)})
+
+
 def case_resnet(rank, world, dev, comm, res):
     """Config-2 update path at W ranks: 161 tensors, channels_last conv weights, CUDA-graph static
     gradients, IPC flat parameters, copy-engine transport; bitwise vs torch.optim.SGD."""
@@ -261,7 +300,8 @@ def main():
     dist.init_process_group("gloo", rank=rank, world_size=world)
     comm = PeerGroup(rank, world)
     res = {"world": world, "case": case, "ok": True, "checks": []}
-    {"parity": case_parity, "fail": case_fail, "resnet": case_resnet}[case](rank, world, dev, comm, res)
+    {"parity": case_parity, "fail": case_fail, "resnet": case_resnet,
+     "graph": case_graph}[case](rank, world, dev, comm, res)
     res["ok"] = all(c["ok"] for c in res["checks"])
     oks = [None] * world
     dist.all_gather_object(oks, res["ok"])

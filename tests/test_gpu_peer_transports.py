@@ -55,3 +55,10 @@ def test_resnet50_update_parity_ce_two_ranks(tmp_path):
     copy-engine transport at W = 2: bitwise torch.optim.SGD(foreach=False) on the rank-order
     average of both ranks' gradients, 3 iterations x 2 apps."""
     _launch(tmp_path, 2, "resnet", 29740)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_rotation_graph_over_peer_transports(tmp_path, world):
+    """graphs.RotationGraph with ce / p2p: barriers, CE pulls and the P2P kernel captured into one
+    graph per rotation -- bitwise equal to eager, ranks identical."""
+    _launch(tmp_path, world, "graph", 29750 + world)

@@ -80,9 +80,9 @@ def test_argument_errors_without_gpu():
     # copy-engine transport and the SM-free flag barrier validate before touching CUDA
     assert _lib.lib.cs_copy_async(None, None, 0, None) == 0
     assert _lib.lib.cs_copy_async(None, None, 16, None) == _lib.CS_ERR_ARG
-    assert _lib.lib.cs_flag_barrier(None, 0, 0, 2, 1, None) == _lib.CS_ERR_ARG
+    assert _lib.lib.cs_flag_barrier(None, 0, 0, 2, None) == _lib.CS_ERR_ARG
     peers = np.zeros(2, dtype=np.uint64)
-    assert _lib.lib.cs_flag_barrier(peers.ctypes.data, 64, 2, 2, 1, None) == _lib.CS_ERR_ARG   # rank out of range
+    assert _lib.lib.cs_flag_barrier(peers.ctypes.data, 64, 2, 2, None) == _lib.CS_ERR_ARG   # rank out of range
     assert _lib.lib.cs_stream_memops_supported() in (0, 1)
     p2p = _lib.P2PDesc()
     p2p.nranks = 9
