@@ -309,11 +309,11 @@ int cs_flag_barrier(const uint64_t* peer_rows, uint64_t local_row, int rank, int
     CUresult r = g_wait32(s, (CUdeviceptr)(local_row + 4u * (uint64_t)p), 1u, wait_flags);
     if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: wait on rank %d failed (%d)", p, (int)r);
   }
-  // reset my row (no fence needed: only this rank reads it, in stream order)
+  // reset my row (only this rank reads it, in stream order; the v2 write API has no
+  // no-barrier flag, so each reset carries the default fence)
   for (int p = 0; p < nranks; ++p) {
     if (p == rank) continue;
-    CUresult r = g_write32(s, (CUdeviceptr)(local_row + 4u * (uint64_t)p), 0u,
-                           CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER);
+    CUresult r = g_write32(s, (CUdeviceptr)(local_row + 4u * (uint64_t)p), 0u, 0);
     if (r != CUDA_SUCCESS) return set_error((int)r, "cs_flag_barrier: reset of slot %d failed (%d)", p, (int)r);
   }
   return 0;
