@@ -480,9 +480,9 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
     from paper_2103_07974_b200.graphs import RotationGraph
     from paper_2103_07974_b200.scheduler import CrossoverScheduler
 
-    mode = "bucket" if h.world == 1 else ("sharded" if sync_mode == "sharded" else "bucket")
+    mode = "bucket" if h.world == 1 or sync_mode == "auto" else sync_mode
     sched = CrossoverScheduler(policy, comm=h.comm, sync_mode=mode, comm_priority=comm_priority,
-                               sync_ctas=SYNC_CTAS)
+                               sync_ctas=SYNC_CTAS, p2p_ctas=P2P_CTAS, barrier=BARRIER)
     total = W + 1 + 2 + K
     static = {}
     regs = []
@@ -769,9 +769,10 @@ def run_ours(args):
     prio = -1 if args.comm_priority == "high" else 0
     graph = args.rotation_graph == "on" or (args.rotation_graph == "auto" and args.config == "mlp")
     if graph:
-        # whole-rotation CUDA graphs (graphs.RotationGraph): the bucket transport (NCCL at W > 1,
-        # simulated workers at W = 1), one graph launch per rotation for both arms
-        sm = sm_seq_best = "sharded" if args.sync_mode == "sharded" else "bucket"
+        # whole-rotation CUDA graphs (graphs.RotationGraph), one graph launch per rotation for both
+        # arms; every transport is capturable -- `auto` = the NCCL bucket all-reduce (W simulated
+        # workers at W = 1)
+        sm = sm_seq_best = "bucket" if args.sync_mode == "auto" or world == 1 else args.sync_mode
         tuner = None
         W = max(W, 2)
     else:
