@@ -786,8 +786,8 @@ def run_ours(args):
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio,
                     p2p_ctas=p2p_cap, graph=graph)
     # and the fastest back-to-back configuration (full-grid P2P kernel at W > 1)
-    seq_best = seq if (sm_seq_best == sm and p2p_cap is None) else timed_run(
-        h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq_best, comm_priority=prio)
+    seq_best = seq if (sm_seq_best == sm and (p2p_cap is None or graph)) else timed_run(
+        h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq_best, comm_priority=prio, graph=graph)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
                                              time_kernels=False, sync_mode=sm, comm_priority=prio,
                                              graph=graph)
