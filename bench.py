@@ -415,7 +415,8 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     from paper_2103_07974_b200.scheduler import CrossoverScheduler
 
     if graph:
-        return timed_run_graph(h, base, policy, W, K, host_data, clocks, sync_mode, comm_priority)
+        return timed_run_graph(h, base, policy, W, K, host_data, clocks, sync_mode, comm_priority,
+                               p2p_ctas)
     mode = sync_mode if h.world > 1 else "auto"
     sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
                                comm_priority=comm_priority,
@@ -470,7 +471,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
 
 
 def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
-                    sync_mode: str = "bucket", comm_priority: int = -1):
+                    sync_mode: str = "bucket", comm_priority: int = -1, p2p_ctas: int | None = None):
     """timed_run in graph mode (paper_2103_07974_b200.graphs): W eager rotations, the graph-layout
     rotation + capture, two untimed replays, then K timed replays (one launch per rotation).
     With `host_data` every replay is preceded by the H2D copies of that rotation's batches into the
@@ -482,7 +483,8 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
 
     mode = "bucket" if h.world == 1 or sync_mode == "auto" else sync_mode
     sched = CrossoverScheduler(policy, comm=h.comm, sync_mode=mode, comm_priority=comm_priority,
-                               sync_ctas=SYNC_CTAS, p2p_ctas=P2P_CTAS, barrier=BARRIER)
+                               sync_ctas=SYNC_CTAS, barrier=BARRIER,
+                               p2p_ctas=P2P_CTAS if p2p_ctas is None else p2p_ctas)
     total = W + 1 + 2 + K
     static = {}
     regs = []
@@ -786,7 +788,7 @@ def run_ours(args):
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio,
                     p2p_ctas=p2p_cap, graph=graph)
     # and the fastest back-to-back configuration (full-grid P2P kernel at W > 1)
-    seq_best = seq if (sm_seq_best == sm and (p2p_cap is None or graph)) else timed_run(
+    seq_best = seq if (sm_seq_best == sm and p2p_cap is None) else timed_run(
         h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm_seq_best, comm_priority=prio, graph=graph)
     e2e = None if args.no_e2e else timed_run(h, base, Policy.CROSSOVER, W, K, host_data=host_data,
                                              time_kernels=False, sync_mode=sm, comm_priority=prio,
