@@ -843,8 +843,9 @@ def run_ours(args):
         e2e_line = None
         if e2e is not None:
             ev = samples_per_rot * K / (e2e["ms"] / 1e3)
-            e2e_line = {"value": round(ev, 2), "unit": unit, "h2d_bytes_per_step": h2d_bytes,
-                        "d2h_bytes_per_step": len(base) * 4}
+            e2e_line = {"value": round(ev, 2), "unit": unit, "h2d_bytes_per_step": h2d_bytes * world,
+                        "d2h_bytes_per_step": len(base) * 4 * world,
+                        "per_rank": {"h2d_bytes": h2d_bytes, "d2h_bytes": len(base) * 4}}
         impl = {"rotation_graph": graph,
                 "precision": ("fp32" if args.config == "mlp" else "bf16 autocast, fp32 params / grads / update"),
                 "sync_mode": (sync0.mode if sync0.mode == sync_seq.mode else
