@@ -399,6 +399,7 @@ class Harness:
 
 P2P_CTAS: int | None = None   # --p2p-ctas; None = the scheduler's per-policy default
 SYNC_CTAS: int | None = None  # --sync-ctas; None = the scheduler's default K1 / K2 grid
+PACK_ENGINE = "sm"            # --pack-engine: K1 by a kernel (sm) or by the copy engines (ce)
 BARRIER = "auto"              # --barrier: cross-rank barrier of the p2p / ce transports
 
 
@@ -421,7 +422,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     sched = CrossoverScheduler(policy, comm=h.comm, time_kernels=time_kernels, sync_mode=mode,
                                comm_priority=comm_priority,
                                p2p_ctas=P2P_CTAS if p2p_ctas is None else p2p_ctas,
-                               barrier=BARRIER, sync_ctas=SYNC_CTAS)
+                               barrier=BARRIER, sync_ctas=SYNC_CTAS, pack_engine=PACK_ENGINE)
     for j, a in enumerate(base):
         sched.register(dataclasses.replace(a, iterations=W + K,
                                            data=host_data[j] if host_data else a.data))

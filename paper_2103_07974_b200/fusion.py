@@ -116,7 +116,7 @@ class FusedGradientSync:
                  comm: NcclCommunicator | None = None, local_workers: int = 1,
                  align: int = 32, mode: str = "auto", snapshot_rows: int = 0,
                  flat_params: torch.Tensor | None = None, p2p_ctas: int = 0,
-                 barrier: str = "auto", sync_ctas: int = 0):
+                 barrier: str = "auto", sync_ctas: int = 0, pack_engine: str = "sm"):
         if not params:
             raise ConfigError("an app needs at least one trainable parameter")
         dev = params[0].device
@@ -128,6 +128,9 @@ class FusedGradientSync:
         self.params = list(params)
         self.settings = settings
         self.sync_ctas = int(sync_ctas)     # K1 / K2 persistent grid cap (0: one CTA per chunk)
+        if pack_engine not in ("sm", "ce"):
+            raise ConfigError(f"unknown pack engine {pack_engine!r}")
+        self.pack_engine = pack_engine      # K1 by the SMs (kernel) or by the copy engines
         self.comm = comm
         self.ranks = comm.world if comm is not None else 1
         self.local_workers = int(local_workers)
@@ -360,6 +363,14 @@ class FusedGradientSync:
             raise ValueError(f"expected gradients of {self.local_workers} worker(s)")
         for w, grads in enumerate(grads_per_worker):
             self._pack["src"][w * n:(w + 1) * n] = _grad_ptrs(grads, self.params)
+        if self.pack_engine == "ce":
+            # the copy engines gather the gradients (one DMA per tensor, no SM): for apps with few
+            # large tensors whose sync overlaps tensor-core compute that would lose the SMs
+            for d in self._pack:
+                if d["numel"]:
+                    _lib.check("cs_copy_async", _lib.lib.cs_copy_async(
+                        int(d["dst"]), int(d["src"]), int(d["numel"]) * 4, stream))
+            return
         _lib.pack(self._pack, stream, self.sync_ctas)
         self.kernel_launches += 1
 

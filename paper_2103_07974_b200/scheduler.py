@@ -213,7 +213,7 @@ class CrossoverScheduler:
                  time_kernels: bool = False, comm_priority: int = -1,
                  perturb: tuple[int, int] | None = None, watchdog_s: float | None = 600.0,
                  nvtx: bool = False, p2p_ctas: int | None = None, barrier: str = "auto",
-                 sync_ctas: int | str | None = None):
+                 sync_ctas: int | str | None = None, pack_engine: str = "sm"):
         if not torch.cuda.is_available():
             raise ConfigError("CrossoverScheduler needs a CUDA device (there is no CPU fallback)")
         if not isinstance(policy, Policy):
@@ -231,6 +231,7 @@ class CrossoverScheduler:
         self.nvtx = nvtx
         self.p2p_ctas = p2p_ctas
         self.sync_ctas = sync_ctas
+        self.pack_engine = pack_engine
         self.barrier = barrier
         with torch.cuda.device(self.device):
             self.compute_stream = torch.cuda.Stream(self.device)
@@ -275,7 +276,8 @@ class CrossoverScheduler:
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
                                  self._mode_for(app), app.iterations if self.record_weights else 0,
                                  flat_params=app.flat_params, p2p_ctas=p2p_ctas,
-                                 barrier=self.barrier, sync_ctas=self._sync_grid())
+                                 barrier=self.barrier, sync_ctas=self._sync_grid(),
+                                 pack_engine=self.pack_engine)
         st = JobRuntimeState(app.job_id, app=app, sync=sync)
         self.states.append(st)
         return st

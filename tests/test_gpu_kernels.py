@@ -260,3 +260,20 @@ def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum):
         assert torch.equal(dsts[0].cpu(), want)
     for r in range(1, world):
         assert torch.equal(dsts[r], dsts[0])              # the fused all-gather wrote every rank
+
+
+def test_pack_by_copy_engines_equals_kernel(cuda_device):
+    """K1 by the copy engines (one DMA per tensor, pack_engine='ce') == the pack kernel, bitwise,
+    including ragged / misaligned tensors (the bucket's padding stays zero either way)."""
+    from paper_2103_07974_b200.fusion import FusedGradientSync, SgdSettings
+
+    torch.manual_seed(5)
+    params = [torch.randn(n, device=cuda_device) for n in RAGGED if n]
+    grads = [torch.randn_like(p) for p in params]
+    out = {}
+    for eng in ("sm", "ce"):
+        s = FusedGradientSync(params, SgdSettings(0.1), mode="bucket", local_workers=1, pack_engine=eng)
+        s.pack([grads], _stream())
+        torch.cuda.synchronize()
+        out[eng] = s.bucket.clone()
+    assert torch.equal(out["sm"].view(torch.int32), out["ce"].view(torch.int32))

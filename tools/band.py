@@ -88,6 +88,8 @@ def main():
     ap.add_argument("--sync-ctas", default="-1",
                     help="K1/K2 grid cap (-1 = 2 CTAs per SM; auto = measured per rho point by "
                          "CrossoverScheduler.calibrate_grid in an untimed probe)")
+    ap.add_argument("--pack-engine", default="sm", choices=["sm", "ce"],
+                    help="K1 by a kernel (sm) or by the copy engines (ce, no SM)")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scenario-band", action="store_true")
@@ -100,6 +102,7 @@ def main():
     h = Harness()
     args.sync_ctas = args.sync_ctas if args.sync_ctas == "auto" else int(args.sync_ctas)
     bench.SYNC_CTAS = -1 if args.sync_ctas == "auto" else args.sync_ctas
+    bench.PACK_ENGINE = args.pack_engine
     if h.world == 1 and args.sync_mode in ("ce", "p2p", "auto"):
         args.sync_mode = "auto"          # W = 1: the sync is K2 alone (direct)
     comp_ns = args.comp_ms * 1e6
@@ -123,6 +126,7 @@ def main():
     per_byte = (t2 - t1) / (s2 - s1)
     alpha = t1 - s1 * per_byte
     res = {"world": h.world, "compute": args.compute, "comp_ms": args.comp_ms, "sync_mode": args.sync_mode,
+           "pack_engine": args.pack_engine,
            "sync_ctas": args.sync_ctas, "steps": args.steps,
            "calibration": {"alpha_ms": round(alpha, 5), "GB_per_s": round(1e-6 / per_byte, 1),
                            "points": [[s, round(t, 5)] for s, t in cal]},
