@@ -66,6 +66,15 @@ def measure(h, base, args, policy_runs=("crossover", "sequential")):
     roof = overlap_roofline(comp, comm)
     rx, rs = cross["ms"] / args.steps, seq["ms"] / args.steps
     pred = (1 + rho) / max(1.0, rho)
+    if args.spans:
+        # per-phase medians of the overlapped run next to the sequential ones: where the time goes
+        cc, cm = phase_medians(cross["timed_spans"], order)
+        out["crossover_phase_ms"] = {"comp": [round(c, 4) for c in cc], "comm": [round(c, 4) for c in cm]}
+        gaps = []
+        gpu = sorted((s.start, s.end) for s in cross["timed_spans"] if s.lane_id == "gpu0")
+        for (a0, a1), (b0, b1) in zip(gpu, gpu[1:]):
+            gaps.append(max(0, b0 - a1) / 1e6)
+        out["crossover_gpu_idle_ms_per_rotation"] = round(sum(gaps) / args.steps, 4)
     out.update({"rho_measured": round(rho, 4), "speedup": round(rs / rx, 4), "predicted": round(pred, 4),
                 "speedup_over_predicted": round(rs / rx / pred, 4),
                 "rotation_ms": {"crossover": round(rx, 4), "sequential": round(rs, 4)},
@@ -93,6 +102,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scenario-band", action="store_true")
+    ap.add_argument("--spans", action="store_true", help="report crossover phase medians and GPU idle")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     import torch
