@@ -30,7 +30,15 @@ def run(policy, comm, dev, specs, T):
     s = CrossoverScheduler(policy, comm=comm, sync_mode="ce", sync_ctas=-1)
     for k, (job, fwd, bwd, nbytes) in enumerate(specs):
         s.register(fixed_time_app(job, fwd, bwd, nbytes, T, dev, seed=k, flat="ipc"))
-    tr = s.run()
+    # start every rank's device timeline together: under crossover the computes never wait for a
+    # sync while there is slack, so a start skew between ranks would persist (absorbed by the early
+    # rank's barrier waits) and show up in its makespan
+    torch.cuda.synchronize()
+    dist.barrier()
+    while s.step():
+        pass
+    s.drain()
+    tr = s.recorder.resolve()
     s.close()
     t0 = min(sp.start for sp in tr.spans if sp.phase.value == "forward")
     return [(sp.lane_id, sp.job_id, sp.phase.value, sp.iteration, sp.start - t0, sp.end - t0)
