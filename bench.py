@@ -676,6 +676,12 @@ class _HostBatches:
         return self.b[(t, worker)]
 
 
+def _graphed_models(args) -> bool:
+    """Per-app CUDA graphs for the image models' forward / backward -- not when the whole rotation
+    is captured (that graph contains the eager forward / backward itself)."""
+    return not args.no_graphs and args.rotation_graph != "on"
+
+
 def build_apps(args, h):
     """(apps, host-data callables for e2e or None, h2d bytes per step, per-app kernel launches
     per iteration that replay inside CUDA graphs) for the selected workload."""
@@ -707,7 +713,7 @@ def build_apps(args, h):
         sc = load_config(args.scenario)
         base = list(sc.device_plan(dev, 1, batch={"resnet50": args.batch, "vgg16": args.batch},
                                    time_scale=args.scenario_time_scale, workers=world, flat=flat,
-                                   graphed=not args.no_graphs, fast_bn=not args.aten_bn,
+                                   graphed=_graphed_models(args), fast_bn=not args.aten_bn,
                                    seed=0, data_seed=1000 * rank).jobs)
         args.mix = f"scenario {sc.name}"
         args.no_e2e, args.no_cpu_baseline = True, True
@@ -721,13 +727,13 @@ def build_apps(args, h):
             else:
                 fn = apps.resnet50_app if name == "resnet50" else apps.vgg16_app
                 base.append(fn(f"{name}_{j}", int(b), 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
-                               graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
+                               graphed=_graphed_models(args), flat=flat, fast_bn=not args.aten_bn,
                                stem="cudnn" if args.cudnn_stem else "gemm"))
         args.no_e2e, args.no_cpu_baseline = True, True
     else:
         build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
         base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
-                      graphed=not args.no_graphs, flat=flat, fast_bn=not args.aten_bn,
+                      graphed=_graphed_models(args), flat=flat, fast_bn=not args.aten_bn,
                       stem="cudnn" if args.cudnn_stem else "gemm")
                 for j in range(args.jobs)]
     host = None if args.no_e2e else [

@@ -247,9 +247,32 @@ class _CycleData:
 
     def __init__(self, batches: list[tuple]):
         self.batches = batches
+        self._stacked = None
 
     def __call__(self, t: int, worker: int):
         return self.batches[(t - 1) % len(self.batches)]
+
+    def graph(self, t_dev: torch.Tensor, worker: int):
+        """The same cycle with the iteration read from a device tensor (CUDA-graph replays): the
+        batches are stacked once (4-D image tensors in their NHWC storage order, so the selected
+        batch comes back as the same channels_last view) and indexed by (t - 1) mod n."""
+        if self._stacked is None:
+            def store(x):
+                if x.dim() == 4 and x.is_contiguous(memory_format=torch.channels_last):
+                    return x.permute(0, 2, 3, 1), True
+                return x, False
+            fields = list(zip(*self.batches))
+            self._stacked = []
+            for f in fields:
+                parts = [store(x) for x in f]
+                self._stacked.append((torch.stack([p for p, _ in parts]), parts[0][1]))
+        n = len(self.batches)
+        sel = torch.remainder(t_dev - 1, n)
+        out = []
+        for st, nhwc in self._stacked:
+            x = st.index_select(0, sel)[0]
+            out.append(x.permute(0, 3, 1, 2) if nhwc else x)
+        return tuple(out)
 
 
 def synthetic_image_batches(batch: int, n_batches: int, seed: int, device: torch.device,
@@ -331,7 +354,8 @@ def _image_app(model: torch.nn.Module, job_id: str, batch: int, iterations: int,
         model = _GraphedImageModel(model, sample)
     return App(job_id, model, _image_loss, data, sgd, iterations, params=params,
                autocast_dtype=torch.bfloat16, samples_per_batch=batch,
-               autocast_cache=not graphed, flat_params=flat_params)
+               autocast_cache=not graphed, flat_params=flat_params,
+               data_graph=None if host_data else data.graph)
 
 
 DEFAULT_IMAGE_SGD = SgdSettings(lr=0.1, momentum=0.9, weight_decay=1e-4)
@@ -396,8 +420,10 @@ def bert_app(job_id: str, batch: int, seq_len: int, iterations: int, device: tor
         h = m.bert(input_ids=i).last_hidden_state
         return F.cross_entropy(m.head(h).float().view(-1, cfg.vocab_size), lab.view(-1))
 
-    return App(job_id, wrap, loss_fn, _CycleData([(ids, labels)]), sgd, iterations,
-               autocast_dtype=torch.bfloat16, samples_per_batch=batch, flat_params=flat_params)
+    data = _CycleData([(ids, labels)])
+    return App(job_id, wrap, loss_fn, data, sgd, iterations,
+               autocast_dtype=torch.bfloat16, samples_per_batch=batch, flat_params=flat_params,
+               data_graph=data.graph)
 
 
 # ---------------------------------------------------------------------------
