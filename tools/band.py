@@ -91,6 +91,9 @@ def measure(h, base, args, policy_runs=("crossover", "sequential")):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rho", default="0.1,0.15,0.2")
+    ap.add_argument("--sizes-mb", default="",
+                    help="sweep these bucket sizes (MB) against the fixed compute instead of target rhos "
+                         "(BASELINE config 4: 1 MB .. 1 GB)")
     ap.add_argument("--compute", default="spin", choices=["spin", "gemm"])
     ap.add_argument("--comp-ms", type=float, default=4.0, help="per-app compute per iteration")
     ap.add_argument("--sync-mode", default="ce")
@@ -143,9 +146,15 @@ def main():
            "rows": []}
     if h.rank == 0:
         print(json.dumps({"calibration": res["calibration"]}), flush=True)
-    for rho in [float(x) for x in args.rho.split(",")]:
-        target = rho * args.comp_ms
-        nbytes = max(MB, int((target - alpha) / per_byte))
+    points = ([("size", int(float(x) * MB)) for x in args.sizes_mb.split(",")] if args.sizes_mb
+              else [("rho", float(x)) for x in args.rho.split(",")])
+    for kind, val in points:
+        if kind == "rho":
+            rho = val
+            nbytes = max(MB, int((rho * args.comp_ms - alpha) / per_byte))
+        else:
+            nbytes = val
+            rho = (alpha + nbytes * per_byte) / args.comp_ms     # predicted by the fitted price
         nbytes -= nbytes % (128 * h.world)
         base = make_apps(h, args.compute, comp_ns, nbytes, gemm_ms=gemm_ms)
         row = {"rho_target": rho, "bucket_MB": round(nbytes / MB, 2), **measure(h, base, args)}
