@@ -253,6 +253,30 @@ def cpu_mlp(workers: int, steps: int, warmup: int):
     return len(specs) * workers * 64 * steps / wall, wall
 
 
+def reference_paths() -> dict:
+    """The reference's own CPU algorithms (restated in oracle/, the GPU box has no /root/reference)
+    timed on this host at the sizes BASELINE.md §3 quotes: the schedule recurrence of
+    scheduler.schedule_crossover / schedule_sequential (N = 2, T = 1000 -> 6,000 spans) and the
+    numeric run_crossover (2 linear jobs x W = 2 x T = 1000, dim 8, batch 16)."""
+    from oracle import schedule as osched
+    from oracle import sgd as osgd
+
+    jobs = [(f"j{k}", 1, 1, 1, 1000) for k in range(2)]
+    t0 = time.perf_counter()
+    spans, _ = osched.crossover(jobs)
+    spans2, _ = osched.sequential(jobs)
+    t_sched = time.perf_counter() - t0
+    lj = [osgd.LinearJob(0.05, 2, osgd.LEAST_SQUARES, 20, 0), osgd.LinearJob(0.05, 2, osgd.LOGISTIC, 21, 1)]
+    t0 = time.perf_counter()
+    osgd.run_crossover(lj, 1000)
+    t_num = time.perf_counter() - t0
+    return {"schedule_spans_per_s": round((len(spans) + len(spans2)) / t_sched),
+            "run_crossover_job_iterations_per_s": round(2 * 1000 / t_num),
+            "run_crossover_samples_per_s": round(2 * 2 * 16 * 1000 / t_num),
+            "note": "oracle restatements of scheduler.py:209-218 / equivalence.py:190-232 "
+                    "(BASELINE.md §3: 197 k spans/s, 6.4 k job-iterations/s on the survey host)"}
+
+
 def host_threads() -> dict:
     import torch
 
@@ -310,7 +334,8 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": workload_config(args, world),
             "cpu_baseline": {"value": round(val, 3), "unit": unit_of(args), "cores": host["cores"],
-                             "kind": "port", "sample": sample, "threads": host},
+                             "kind": "port", "sample": sample, "threads": host,
+                             "reference_paths": reference_paths()},
             "e2e": {"value": round(val, 3), "unit": unit_of(args), "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -846,7 +871,7 @@ def run_ours(args):
                           f"sample of batch {args.batch}), {rot} rotations after 1 warm-up, torch-CPU "
                           f"fwd/bwd + oracle rotation / fusion / average / SGD-momentum ({wall:.1f} s)")
             cpu = {"value": round(cv, 3), "unit": unit, "cores": host["cores"], "kind": "port",
-                   "sample": sample, "threads": host}
+                   "sample": sample, "threads": host, "reference_paths": reference_paths()}
         e2e_line = None
         if e2e is not None:
             ev = samples_per_rot * K / (e2e["ms"] / 1e3)
