@@ -125,6 +125,12 @@ def case_parity(rank, world, dev, comm, res):
         res["checks"].append({"name": f"mlp_momentum_{mode}_mode", "ok": modes == {mode}})
     res["checks"].append({"name": "mlp_momentum_ce_bitwise_eq_p2p",
                           "ok": all(torch.equal(a, b) for a, b in zip(mlp_w["ce"], mlp_w["p2p"]))})
+    # L4 at W ranks: the schedule adds no staleness -- sequential == crossover, bit for bit
+    apps = [mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T, dev,
+                    local_workers=1, worker_count=world, flat="ipc") for k, (ds, rs) in enumerate(specs)]
+    seq_w, _, _, _, _ = _run(apps, comm, "ce", policy=Policy.SEQUENTIAL)
+    res["checks"].append({"name": "mlp_momentum_ce_sequential_bitwise_eq_crossover",
+                          "ok": all(torch.equal(a, b) for a, b in zip(seq_w, mlp_w["ce"]))})
     res["checks"].append({"name": "mlp_momentum_ranks_identical",
                           "ok": _gather_equal(torch.cat([x.reshape(-1) for x in mlp_w["ce"]]), rank, world)})
     # adaptive: calibrate() measures both transports on real iterations, every rank keeps the same one
