@@ -283,7 +283,14 @@ class FusedGradientSync:
             if barrier == "flags" or not nccl:
                 raise ConfigError("stream memory operations are not supported on every rank")
             return
-        self._flags = FlagArray(self.rank, self.ranks)      # host shared memory, zeroed
+        try:
+            self._flags = FlagArray(self.rank, self.ranks)  # host shared memory, zeroed
+        except ConfigError:
+            # the segment failed on some rank (every rank raises together): the NCCL barrier
+            # still works where there is a communicator
+            if barrier == "flags" or not nccl:
+                raise
+            return
         self._flag_peers = self._flags.peer_rows               # per phase
         self._flag_local = self._flags.local_rows
         self._barrier_kind = "flags"
