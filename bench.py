@@ -168,6 +168,14 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
             out["sequential_arm"] = {k: seq_line[k] for k in ("kernel", "bound", "achieved", "peak",
                                                                "unit", "frac", "grid_cap_ctas")}
         return out
+    if "c1_allreduce" in kernels and "k2_update" not in kernels:
+        c1 = kernels["c1_allreduce"]
+        return {"kernel": "sync graph (NCCL all-reduce + K2) of the rotation graph", "bound": "nvlink",
+                "achieved": c1["busbw_GB/s"], "peak": NVLINK_P2P_GBS, "unit": "GB/s",
+                "frac": round(c1["busbw_GB/s"] / NVLINK_P2P_GBS, 4), "traffic": None,
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                "bytes_per_launch": c1["bus_bytes"],
+                "note": "a 0.8 MB bucket: latency-bound, the fraction says so"}
     return {"kernel": "k2_update (fused 1/W average + SGD-momentum)", "bound": "hbm",
             "achieved": k2["GB/s"], "peak": hbm_peak, "unit": "GB/s",
             "frac": round(k2["GB/s"] / hbm_peak, 4),
@@ -847,6 +855,11 @@ def run_ours(args):
                                                      "GB/s": round(sync0.k2_bytes() / (comm_t[0] / 1e3) / 1e9, 1)}}
         if world == 1:   # the sync graph is K2 alone (two simulated workers' rows)
             kernels["k2_update"] = kernels["sync_graph"]
+        else:            # C1 + K2: report the exchange against NVLink (latency-bound for small buckets)
+            nv = sync0.c1_bus_bytes()
+            kernels["c1_allreduce"] = {"ms": round(comm_t[0], 4), "bus_bytes": nv,
+                                       "busbw_GB/s": round(nv / (comm_t[0] / 1e3) / 1e9, 1),
+                                       "peak_GB/s": 900.0, "note": "whole sync graph (C1 + K2)"}
     else:
         comp, comm_t = phase_medians(seq["timed_spans"], order)
         kernels = kernel_summary(cross["kernels"], sync0)
