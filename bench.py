@@ -519,7 +519,7 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
     sched = CrossoverScheduler(policy, comm=h.comm, sync_mode=mode, comm_priority=comm_priority,
                                sync_ctas=SYNC_CTAS, barrier=BARRIER,
                                p2p_ctas=P2P_CTAS if p2p_ctas is None else p2p_ctas)
-    total = W + 1 + 2 + K
+    total = W + 1 + 2 * 8 + K
     static = {}
     regs = []
     for j, a in enumerate(base):
@@ -537,7 +537,10 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
     for _ in range(W):
         for _j in range(len(base)):
             sched.step()
-    rg = RotationGraph(sched)
+    # several rotations per graph launch (fewer launches; the e2e path feeds every rotation's
+    # batches from the host, so it replays one rotation per launch)
+    per = 1 if host_data else next(k for k in (8, 4, 2, 1) if K % k == 0)
+    rg = RotationGraph(sched, rotations=per)
 
     def feed(t):
         if host_data:
@@ -551,6 +554,7 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
     for _ in range(2):
         feed(rg.t + 1)
         rg.replay()
+    K_launches = K // per
     sched.drain()
     h.barrier()
     gc.collect()
@@ -558,7 +562,7 @@ def timed_run_graph(h: Harness, base, policy, W: int, K: int, host_data=None, cl
     clk = Clocks(h.local) if clocks else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(cs)
-    for _ in range(K):
+    for _ in range(K_launches):
         feed(rg.t + 1)
         rg.replay()
         if host_data:   # D2H of every app's loss of this rotation
@@ -729,7 +733,7 @@ def build_apps(args, h):
     if args.config == "mlp":
         w = max(2, world)
         local = w // world
-        iters = max(args.warmup + args.steps + 8, 9)   # >= calibration / graph-mode prologue
+        iters = max(args.warmup + args.steps + 24, 17)  # >= calibration / graph-mode prologue
         base = [apps.mlp_app(apps.MlpConfig(dataset_seed=11 + k, workers=w), f"mlp{k}", k, iters, dev,
                              local_workers=local, worker_count=w, flat=flat) for k in range(2)]
         host = None

@@ -52,7 +52,7 @@ class RotationGraph:
     initialises momentum; kernels and the allocator warm up), then ``begin()``, ``replay()`` once per
     rotation, ``end()`` -- after which ``sched.drain()`` / ``run``-style accounting applies."""
 
-    def __init__(self, sched: CrossoverScheduler):
+    def __init__(self, sched: CrossoverScheduler, rotations: int = 1):
         if not sched.states:
             raise ConfigError("no apps registered")
         for st in sched.states:
@@ -68,7 +68,10 @@ class RotationGraph:
         its = {st.next_iteration for st in sched.states}
         if len(its) != 1 or min(its) < 3:
             raise ConfigError("graph mode starts after >= 2 eager rotations of every app")
+        if rotations < 1:
+            raise ConfigError("rotations per graph must be >= 1")
         self.sched = sched
+        self.rotations = int(rotations)   # rotations unrolled into one graph (fewer launches)
         self.t_dev = torch.zeros(1, dtype=torch.int64, device=sched.device)
         self.graph: torch.cuda.CUDAGraph | None = None
         self.t = 0                # last iteration whose compute has been enqueued
@@ -137,50 +140,59 @@ class RotationGraph:
         n = len(states)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=cs):
-            self.t_dev.add_(1)
-            fork = torch.cuda.Event()
-            fork.record(cs)
-            ms.wait_event(fork)
-            if sched.policy is Policy.CROSSOVER:
-                with torch.cuda.stream(ms):
-                    self._sync(states[n - 1])        # sync(N-1, t-1): the deferred one
-                tail = torch.cuda.Event()
-                tail.record(ms)
-                for j, st in enumerate(states):
-                    if j == n - 1:
-                        cs.wait_event(tail)          # Alg. 1: compute(N-1, t) after sync(N-1, t-1)
-                    self._compute(st)
-                    if j < n - 1:
-                        e = torch.cuda.Event()
-                        e.record(cs)
-                        ms.wait_event(e)
-                        with torch.cuda.stream(ms):
-                            self._sync(st)
-            else:
-                for st in states:
-                    self._compute(st)
+            for _ in range(self.rotations):
+                self._capture_rotation(states, n)
+        self.graph = g
+
+    def _capture_rotation(self, states, n: int) -> None:
+        """One rotation's nodes; it ends with the compute stream joining the comm stream, so a
+        second copy in the same graph starts exactly where the next replay would."""
+        sched = self.sched
+        cs, ms = sched.compute_stream, sched.comm_stream
+        self.t_dev.add_(1)
+        fork = torch.cuda.Event()
+        fork.record(cs)
+        ms.wait_event(fork)
+        if sched.policy is Policy.CROSSOVER:
+            with torch.cuda.stream(ms):
+                self._sync(states[n - 1])        # sync(N-1, t-1): the deferred one
+            tail = torch.cuda.Event()
+            tail.record(ms)
+            for j, st in enumerate(states):
+                if j == n - 1:
+                    cs.wait_event(tail)          # Alg. 1: compute(N-1, t) after sync(N-1, t-1)
+                self._compute(st)
+                if j < n - 1:
                     e = torch.cuda.Event()
                     e.record(cs)
                     ms.wait_event(e)
                     with torch.cuda.stream(ms):
                         self._sync(st)
-                    back = torch.cuda.Event()
-                    back.record(ms)
-                    cs.wait_event(back)
-            join = torch.cuda.Event()
-            join.record(ms)
-            cs.wait_event(join)
-        self.graph = g
+        else:
+            for st in states:
+                self._compute(st)
+                e = torch.cuda.Event()
+                e.record(cs)
+                ms.wait_event(e)
+                with torch.cuda.stream(ms):
+                    self._sync(st)
+                back = torch.cuda.Event()
+                back.record(ms)
+                cs.wait_event(back)
+        join = torch.cuda.Event()
+        join.record(ms)
+        cs.wait_event(join)
 
     def replay(self) -> None:
-        """One rotation: every app computes iteration t+1 (and the syncs of the schedule above)."""
+        """`rotations` rotations: every app computes iterations t+1 .. t+rotations (and the syncs of
+        the schedule above)."""
         if self.graph is None:
             raise ConfigError("begin() first")
-        if self.t + 1 > min(st.app.iterations for st in self.sched.states):
+        if self.t + self.rotations > min(st.app.iterations for st in self.sched.states):
             raise ConfigError("iteration budget exhausted")
         with torch.cuda.stream(self.sched.compute_stream):
             self.graph.replay()
-        self.t += 1
+        self.t += self.rotations
         self.replays += 1
 
     def end(self) -> None:

@@ -21,7 +21,7 @@ def _flat(app):
     return torch.cat([p.detach().reshape(-1) for p in app.params]).cpu()
 
 
-def _run(make_apps, policy, T, graph, warm=2):
+def _run(make_apps, policy, T, graph, warm=2, per=1):
     from paper_2103_07974_b200.graphs import RotationGraph
     from paper_2103_07974_b200.scheduler import CrossoverScheduler
 
@@ -34,7 +34,7 @@ def _run(make_apps, policy, T, graph, warm=2):
         return [_flat(a) for a in apps], None
     for _ in range(warm * len(apps)):
         s.step()
-    rg = RotationGraph(s)
+    rg = RotationGraph(s, rotations=per)
     rg.begin()
     while rg.t < T:
         rg.replay()
@@ -59,6 +59,11 @@ def test_rotation_graph_bitwise_eq_eager_mlp(cuda_device, policy_name):
     eager, _ = _run(make, pol, 10, graph=False)
     graphed, rg = _run(make, pol, 10, graph=True)
     assert rg.replays == 10 - 3
+    unrolled, rg = _run(make, pol, 11, graph=True, per=4)      # 2 launches of 4 rotations
+    assert rg.replays == 2
+    eager11, _ = _run(make, pol, 11, graph=False)
+    for a, b in zip(eager11, unrolled):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
     for a, b in zip(eager, graphed):
         assert torch.equal(a.view(torch.int32), b.view(torch.int32))
 
