@@ -80,9 +80,10 @@ __device__ __forceinline__ int find_segment(const int* chunk_begin, int n, int c
 template <int CAP, int U>
 __device__ __forceinline__ void pack_chunk(const PackArgs<CAP>& a, int c);
 
-// grid = #chunks (one chunk per CTA) or capped (cs_tune "sync_ctas"): persistent over chunks
+// grid = #chunks (one chunk per CTA) or capped (cs_tune "sync_ctas"): persistent over chunks.
+// The min-blocks hint keeps ptxas from capping the kernel at 32 registers (which spilled 8 bytes).
 template <int CAP, int U>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 pack_kernel(const __grid_constant__ PackArgs<CAP> a) {
   for (int c = blockIdx.x; c < a.total_chunks; c += gridDim.x) pack_chunk<CAP, U>(a, c);
 }
