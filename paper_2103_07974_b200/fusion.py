@@ -322,11 +322,10 @@ class FusedGradientSync:
     def _init_p2p(self, bmap, fmap, off: int, p2p_ctas: int) -> None:
         self._p2p = _lib.P2PDesc()
         for r in range(self.ranks):
-            # sources in rank order (the sum order is the reference's); destinations rotated so
-            # every rank's stores start at its right neighbour instead of all hitting rank 0 first
-            d = (self.rank + r) % self.ranks if P2P_ROTATE_DESTINATIONS else r
+            # sources in rank order: the sum order is the reference's (rotating the destination
+            # order measured no difference, tools/c1bench.py: thousands of threads interleave)
             self._p2p.src[r] = bmap.addresses[r] + off
-            self._p2p.dst[r] = fmap.addresses[d] + off
+            self._p2p.dst[r] = fmap.addresses[r] + off
         self._p2p.param = self.flat.data_ptr() + off
         self._p2p.momentum_buf = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else None
         self._p2p.numel = self.shard
@@ -614,7 +613,6 @@ class FusedGradientSync:
 
 
 _zero_cache: dict[tuple, torch.Tensor] = {}
-P2P_ROTATE_DESTINATIONS = True   # tools/c1bench.py --no-rotate measures the rank-order variant
 
 
 def _dense(t: torch.Tensor) -> bool:

@@ -27,12 +27,8 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--out", default="")
     ap.add_argument("--p2p-caps", default="0", help="comma list of p2p_ctas values to time (0 = default)")
-    ap.add_argument("--no-rotate", action="store_true", help="P2P kernel stores in rank order")
     args = ap.parse_args()
-    from paper_2103_07974_b200 import fusion
     from paper_2103_07974_b200.fusion import FusedGradientSync, SgdSettings, flatten_parameters
-
-    fusion.P2P_ROTATE_DESTINATIONS = not args.no_rotate
 
     h = Harness()
     W = h.world
