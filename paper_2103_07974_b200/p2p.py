@@ -121,20 +121,21 @@ def exchange_peer_addresses(buf: DeviceBuffer, rank: int, world: int) -> PeerMap
                 break
             addrs.append(int(p.value))
             opened.append(int(p.value))
-    ok = torch.tensor([0 if error else 1], dtype=torch.int32)
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     mapping = PeerMapping(addrs, opened)
-    if int(ok.item()) == 0:
+    if not all_ranks_agree(not error):
         mapping.close()
         raise ConfigError("p2p peer mapping failed on some rank" + (f" ({error})" if error else ""))
     return mapping
 
 
 def all_ranks_agree(ok: bool) -> bool:
-    """True iff every rank passes True (collective over torch.distributed's CPU group)."""
+    """True iff every rank passes True (collective over the default torch.distributed group; a
+    CUDA tensor when that group is NCCL-backed, which takes no CPU tensors)."""
     import torch.distributed as dist
 
     t = torch.tensor([1 if ok else 0], dtype=torch.int32)
+    if dist.get_backend() == "nccl":
+        t = t.to(torch.cuda.current_device())
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     return bool(int(t.item()))
 
