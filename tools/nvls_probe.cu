@@ -27,7 +27,7 @@ FN(cuDeviceGetAttribute)
 
 template <class T> static void load(T& f, const char* name) {
   cudaDriverEntryPointQueryResult q;
-  cudaGetDriverEntryPointByVersion(name, (void**)&f, 12000, cudaEnableDefault, &q);
+  cudaGetDriverEntryPointByVersion(name, (void**)&f, 12090, cudaEnableDefault, &q);
   if (!f) { printf("no entry point %s\n", name); exit(2); }
 }
 
