@@ -86,7 +86,8 @@ def parse():
                          "(cs_bn_backward2) instead of an autograd add kernel")
     ap.add_argument("--bn-no-pdl", action="store_true",
                     help="launch the BN finalize / apply kernels without programmatic dependent launch")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused"],
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused",
+                                                            "nvls"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
                          "the fused NVLink P2P kernel; ce = copy-engine pulls + shard K2; auto = ce "
                          "under crossover and p2p for the sequential arm (bucket if peers cannot "
@@ -120,6 +121,15 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
     Under crossover the P2P kernel is launched on a deliberately small grid (it overlaps the
     other app's compute and only has to finish inside it), so its live fraction is low by
     design; ``isolated`` is the same kernel at the full grid in the sequential arm."""
+    if "k2_nvls_fused" in kernels:
+        k = kernels["k2_nvls_fused"]
+        ach = k["nvlink_GB/s"]
+        return {"kernel": "k2_nvls_fused (multimem.ld_reduce of every rank's bucket shard through the "
+                          "NVSwitch, /W, SGD-momentum, multimem.st of the new shard to every rank)",
+                "bound": "nvlink", "achieved": ach, "peak": NVLINK_P2P_GBS, "unit": "GB/s",
+                "frac": round(ach / NVLINK_P2P_GBS, 4), "traffic": None,
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                "bytes_per_launch": k["nvlink_bytes"], "grid_cap_ctas": int(sync._nvls.max_ctas) or "2 per SM"}
     if "k2_p2p_fused" in kernels:
         k = kernels["k2_p2p_fused"]
         per_dir = sync.c1_bus_bytes()          # 2(W-1)/W * S through each GPU's links per direction
@@ -693,6 +703,11 @@ def kernel_summary(kern: dict, sync) -> dict:
         out["k2_p2p_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes("p2p"),
                                "GB/s": round(sync.k2_bytes("p2p") / (t / 1e3) / 1e9, 1),
                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
+    if "k2_nvls_fused" in kern:
+        t = statistics.mean(kern["k2_nvls_fused"])
+        nv = sync.c1_bus_bytes()
+        out["k2_nvls_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes("nvls"),
+                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
     if "c1_allreduce" in kern:
         t = statistics.mean(kern["c1_allreduce"])
         out["c1_allreduce"] = {"ms": round(t, 4), "bus_bytes": sync.c1_bus_bytes(),
@@ -728,7 +743,7 @@ def build_apps(args, h):
 
     rank, world, dev = h.rank, h.world, h.dev
     # auto at W > 1: IPC flat parameters, and the scheduler picks the transport per policy
-    flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc"}.get(args.sync_mode, False)
+    flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc", "nvls": "nvls"}.get(args.sync_mode, False)
             if world > 1 else False)
     if args.config == "mlp":
         w = max(2, world)
@@ -828,7 +843,9 @@ def run_ours(args):
                       graph=graph)
     # the same transport with the same launch caps for the sequential arm: the speedup measures
     # the schedule alone (crossover vs back-to-back, same kernels)
-    p2p_cap = cross["sched"].states[0].sync._p2p.max_ctas if hasattr(cross["sched"].states[0].sync, "_p2p") else None
+    s0 = cross["sched"].states[0].sync
+    p2p_cap = (s0._p2p.max_ctas if hasattr(s0, "_p2p") else
+               s0._nvls.max_ctas if hasattr(s0, "_nvls") else None)
     seq = timed_run(h, base, Policy.SEQUENTIAL, W, K, sync_mode=sm, comm_priority=prio,
                     p2p_ctas=p2p_cap, graph=graph)
     # and the fastest back-to-back configuration (full-grid P2P kernel at W > 1)

@@ -172,6 +172,37 @@ typedef struct cs_p2p_desc {
 CS_API int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* desc, const cs_sgd_hyper* hyper,
                                    void* stream);
 
+/* Collective-fused update through NVSwitch multicast (NVLS): same contract as
+ * cs_p2p_reduce_sgd_bcast, but the W-rank sum is a multimem.ld_reduce on the multicast mapping of
+ * the buckets (the switch adds; its order is unspecified, so results match the rank-order
+ * transports within fp32 rounding, not bitwise) and the new shard is a multimem.st into the
+ * multicast mapping of the flat parameters (the switch writes every rank's copy).
+ * mc_bucket / mc_param: this rank's shard in the multicast mappings; param: the same shard in the
+ * local (unicast) mapping.  numel % 4 == 0.  The caller orders it between two barriers. */
+typedef struct cs_nvls_desc {
+  const float* mc_bucket;
+  float* mc_param;
+  float* param;
+  float* momentum_buf;   /* this rank's momentum shard, NULL when momentum == 0 */
+  int64_t numel;
+  int32_t nranks;
+  int32_t max_ctas;      /* persistent grid cap, 0 = 2 CTAs per SM */
+} cs_nvls_desc;
+CS_API int cs_nvls_reduce_sgd_bcast(const cs_nvls_desc* desc, const cs_sgd_hyper* hyper, void* stream);
+/* Multicast objects and the physical memory bound to them (driver entry points resolved at run
+ * time).  Rank 0 creates the object and exports it as a POSIX file descriptor; the other ranks
+ * import it; every rank adds its device, then (after all ranks added theirs) allocates, binds and
+ * maps its memory twice: unicast (uc_ptr, local accesses) and multicast (mc_ptr, multimem ops). */
+CS_API int cs_nvls_supported(int device);
+CS_API int cs_nvls_granularity(int nranks, size_t bytes, size_t* gran);
+CS_API int cs_nvls_create(int nranks, size_t bytes, uint64_t* mc, int* fd);
+CS_API int cs_nvls_import(int fd, uint64_t* mc);
+CS_API int cs_nvls_add_device(uint64_t mc, int device);
+CS_API int cs_nvls_alloc_bind(uint64_t mc, int device, size_t bytes, size_t gran, uint64_t* phys,
+                              void** uc_ptr, void** mc_ptr);
+CS_API int cs_nvls_free(uint64_t mc, int device, uint64_t phys, void* uc_ptr, void* mc_ptr, size_t bytes);
+CS_API int cs_nvls_release(uint64_t mc);
+
 /* IPC-capable device memory (cudaMalloc'd, zero-filled) and its peer mapping. */
 #define CS_IPC_HANDLE_BYTES 64
 CS_API int cs_device_alloc(size_t bytes, void** ptr);

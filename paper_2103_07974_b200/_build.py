@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO_DIR = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libcrossover.so"
-SOURCES = ["crossover_im2col.cu", "crossover_kernels.cu", "crossover_p2p.cu", "crossover_bn.cu",
+SOURCES = ["crossover_im2col.cu", "crossover_kernels.cu", "crossover_p2p.cu", "crossover_nvls.cu", "crossover_bn.cu",
            "crossover_pool.cu", "crossover_abi.cu", "crossover_nccl.cu"]
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -44,6 +44,12 @@ class P2PDesc(ctypes.Structure):
                 ("numel", ctypes.c_int64), ("nranks", ctypes.c_int32), ("max_ctas", ctypes.c_int32)]
 
 
+class NvlsDesc(ctypes.Structure):
+    _fields_ = [("mc_bucket", ctypes.c_void_p), ("mc_param", ctypes.c_void_p), ("param", ctypes.c_void_p),
+                ("momentum_buf", ctypes.c_void_p), ("numel", ctypes.c_int64), ("nranks", ctypes.c_int32),
+                ("max_ctas", ctypes.c_int32)]
+
+
 class CrossoverLibError(RuntimeError):
     """A libcrossover.so call returned a non-zero status."""
 
@@ -76,6 +82,20 @@ EXPORTS = {
                            ctypes.c_void_p], ctypes.c_int),
     "cs_p2p_reduce_sgd_bcast": ([ctypes.POINTER(P2PDesc), ctypes.POINTER(SgdHyper), ctypes.c_void_p],
                                 ctypes.c_int),
+    "cs_nvls_reduce_sgd_bcast": ([ctypes.POINTER(NvlsDesc), ctypes.POINTER(SgdHyper), ctypes.c_void_p],
+                                 ctypes.c_int),
+    "cs_nvls_supported": ([ctypes.c_int], ctypes.c_int),
+    "cs_nvls_granularity": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)], ctypes.c_int),
+    "cs_nvls_create": ([ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64),
+                        ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "cs_nvls_import": ([ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
+    "cs_nvls_add_device": ([ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
+    "cs_nvls_alloc_bind": ([ctypes.c_uint64, ctypes.c_int, ctypes.c_size_t, ctypes.c_size_t,
+                            ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_void_p),
+                            ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "cs_nvls_free": ([ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_size_t], ctypes.c_int),
+    "cs_nvls_release": ([ctypes.c_uint64], ctypes.c_int),
     "cs_device_alloc": ([ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "cs_device_free": ([ctypes.c_void_p], ctypes.c_int),
     "cs_ipc_get_handle": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),

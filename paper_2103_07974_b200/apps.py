@@ -38,11 +38,11 @@ def _world() -> int:
 def _flatten(params, flat):
     """flatten_parameters for the sharded / p2p sync (shards = world size); None when not asked.
 
-    ``flat`` is False, True (torch allocation, sharded NCCL sync) or "ipc" (cudaMalloc'd,
-    mappable by peers, p2p sync)."""
+    ``flat`` is False, True (torch allocation, sharded NCCL sync), "ipc" (cudaMalloc'd,
+    mappable by peers, p2p / ce sync) or "nvls" (bound to an NVSwitch multicast object)."""
     if not flat:
         return None
-    return flatten_parameters(params, 32, _world(), ipc=(flat == "ipc"))[0]
+    return flatten_parameters(params, 32, _world(), ipc="nvls" if flat == "nvls" else (flat == "ipc"))[0]
 
 __all__ = [
     "LossKind",

@@ -43,11 +43,18 @@ def flatten_parameters(params: Sequence[torch.Tensor], align: int = 32, shards: 
     to ``align * shards`` so the buffer splits into equal aligned shards.  This is what
     lets the sharded sync all-gather updated shards straight into the model's weights.
     Call it before anything captures parameter addresses (CUDA graphs).  ``ipc=True``
-    allocates the buffer with cs_device_alloc so peers can map it (p2p sync mode).
+    allocates the buffer with cs_device_alloc so peers can map it (p2p / ce sync modes);
+    ``ipc="nvls"`` binds it to an NVSwitch multicast object (nvls sync mode, collective).
     """
     lay = BucketLayout.build([p.numel() for p in params], align, multiple=align * shards)
     dev = params[0].device
-    if ipc:
+    if ipc == "nvls":
+        import torch.distributed as dist
+
+        from .nvls import NvlsBuffer
+
+        flat = NvlsBuffer(lay.total, dev, dist.get_rank(), dist.get_world_size()).tensor
+    elif ipc:
         from .p2p import DeviceBuffer
 
         flat = DeviceBuffer(lay.total, dev).tensor
@@ -146,13 +153,13 @@ class FusedGradientSync:
                 mode = "ce"
             else:
                 mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
-        if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "adaptive", "unfused"):
+        if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "adaptive", "unfused", "nvls"):
             raise ConfigError(f"unknown sync mode {mode!r}")
         if mode == "direct" and self.workers != 1:
             raise ConfigError("direct mode has no bucket and needs exactly one worker")
         if mode == "unfused" and self.local_workers != 1:
             raise ConfigError("unfused mode all-reduces each gradient tensor in place: one worker per rank")
-        if mode in ("sharded", "p2p", "ce", "adaptive") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
+        if mode in ("sharded", "p2p", "ce", "adaptive", "nvls") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
             raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
                               "and one worker per rank")
         if (self.ranks > 1 and mode in ("bucket", "sharded", "unfused")
@@ -160,7 +167,7 @@ class FusedGradientSync:
             raise ConfigError(f"{mode} sync needs an NCCL communicator at world > 1")
         self.mode = mode
         self.flat = flat_params
-        sharded = mode in ("sharded", "p2p", "ce", "adaptive")
+        sharded = mode in ("sharded", "p2p", "ce", "adaptive", "nvls")
         multiple = align * self.ranks if sharded else None
         self.layout = BucketLayout.build([p.numel() for p in self.params], align, multiple=multiple)
         if sharded:
@@ -179,7 +186,16 @@ class FusedGradientSync:
         self._flags = None
         self.failed = False
         self.transport = None
-        if mode in ("p2p", "ce", "adaptive"):
+        if mode == "nvls":
+            from .nvls import NvlsBuffer, nvls_buffer_of
+
+            self._flat_nvls = nvls_buffer_of(flat_params)
+            if self._flat_nvls is None:
+                raise ConfigError("nvls sync needs multicast-bound flat parameters "
+                                  "(flatten_parameters(ipc='nvls'))")
+            self._bucket_nvls = NvlsBuffer(lay.total, dev, comm.rank, self.ranks)
+            self.bucket = self._bucket_nvls.tensor
+        elif mode in ("p2p", "ce", "adaptive"):
             from .p2p import DeviceBuffer, buffer_of
 
             if self.ranks > _lib.CS_MAX_SOURCES:
@@ -214,6 +230,21 @@ class FusedGradientSync:
                 sl["dst"] = base + w * row_bytes + offs_bytes
                 sl["numel"] = numels
         # K2 descriptors: fixed except grad_offset in direct mode
+        if mode == "nvls":
+            off = self.rank * self.shard * 4
+            self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
+            self._init_barrier(barrier)
+            self._nvls = _lib.NvlsDesc()
+            self._nvls.mc_bucket = self._bucket_nvls.mc_ptr + off
+            self._nvls.mc_param = self._flat_nvls.mc_ptr + off
+            self._nvls.param = flat_params.data_ptr() + off
+            self._nvls.momentum_buf = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else None
+            self._nvls.numel = self.shard
+            self._nvls.nranks = self.ranks
+            self._nvls.max_ctas = int(p2p_ctas)
+            self.transport = "nvls"
+            self._finish_init(settings)
+            return
         if mode in ("p2p", "ce", "adaptive"):
             from .p2p import buffer_of, exchange_peer_addresses
 
@@ -307,7 +338,7 @@ class FusedGradientSync:
 
     @property
     def barrier_kind(self) -> str | None:
-        if self.mode not in ("p2p", "ce", "adaptive"):
+        if self.mode not in ("p2p", "ce", "adaptive", "nvls"):
             return None
         return self._barrier_kind
 
@@ -365,7 +396,7 @@ class FusedGradientSync:
     # -- per-iteration pieces (all asynchronous on `stream`) -----------------
     def pack(self, grads_per_worker: Sequence[Sequence[torch.Tensor]], stream: int) -> None:
         """K1: gather each worker's gradients into its bucket row."""
-        if self.mode not in ("bucket", "sharded", "p2p", "ce", "adaptive"):
+        if self.mode not in ("bucket", "sharded", "p2p", "ce", "adaptive", "nvls"):
             raise ConfigError("pack() needs bucket mode")
         n = len(self.params)
         if len(grads_per_worker) != self.local_workers:
@@ -441,6 +472,9 @@ class FusedGradientSync:
         if self.mode == "sharded":
             self._sharded_tail(stream, snapshot_row, timer)
             return
+        if self.transport == "nvls":
+            self._nvls_tail(stream, snapshot_row, timer)
+            return
         if self.transport == "p2p":
             self._p2p_tail(stream, snapshot_row, timer)
             return
@@ -467,6 +501,8 @@ class FusedGradientSync:
             self._sharded_tail(stream, None, None)
         elif self.transport == "p2p":
             self._p2p_tail(stream, None, None)
+        elif self.transport == "nvls":
+            self._nvls_tail(stream, None, None)
         elif self.transport == "ce":
             self._ce_tail(stream, None, None)
         elif self.mode == "bucket":
@@ -512,6 +548,26 @@ class FusedGradientSync:
         if timer is not None:
             timer.end("k2_p2p_fused")
         self._rank_barrier(stream, 1)                  # every rank's parameter writes landed
+        if snapshot_row is not None:
+            if self.snapshot is None:
+                raise ConfigError("no snapshot buffer (snapshot_rows=0)")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.snapshot[snapshot_row].copy_(self.flat)
+
+    def _nvls_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
+        """barrier -> one kernel: switch-reduced shard (multimem.ld_reduce), /W, SGD, switch-broadcast
+        new shard (multimem.st) -> barrier."""
+        self._rank_barrier(stream, 0)                  # every rank's K1 has landed
+        if timer is not None:
+            timer.begin("k2_nvls_fused")
+        self._hyper.first_step = int(self.first_step)
+        _lib.check("cs_nvls_reduce_sgd_bcast", _lib.lib.cs_nvls_reduce_sgd_bcast(
+            ctypes.byref(self._nvls), ctypes.byref(self._hyper), stream))
+        self.first_step = False
+        self.kernel_launches += 1
+        if timer is not None:
+            timer.end("k2_nvls_fused")
+        self._rank_barrier(stream, 1)                  # every rank's multicast stores landed
         if snapshot_row is not None:
             if self.snapshot is None:
                 raise ConfigError("no snapshot buffer (snapshot_rows=0)")
@@ -568,7 +624,7 @@ class FusedGradientSync:
         for m in self._peer_maps:
             m.close()
         self._peer_maps = []
-        bucket = getattr(self, "_bucket_buf", None)
+        bucket = getattr(self, "_bucket_buf", None) or getattr(self, "_bucket_nvls", None)
         if bucket is None and self._flags is None:
             return
         if self.ranks > 1 and not self.failed:
@@ -579,7 +635,7 @@ class FusedGradientSync:
         if bucket is not None:
             self.bucket = None
             bucket.close()
-            self._bucket_buf = None
+            self._bucket_buf = self._bucket_nvls = None
         if self._flags is not None:
             self._flags.close()
             self._flags = None
@@ -591,6 +647,10 @@ class FusedGradientSync:
 
     def k2_bytes(self, transport: str | None = None) -> int:
         transport = transport or self.transport
+        if transport == "nvls":
+            # local HBM: read p (+ momentum r/w); the reduced shard arrives from and the new shard
+            # leaves through the switch
+            return (1 + (2 if self.settings.momentum else 0)) * self.shard * 4
         if transport == "p2p":
             # W source shards + p read + W destination shards (+ momentum read/write)
             return (2 * self.ranks + 1 + (2 if self.settings.momentum else 0)) * self.shard * 4

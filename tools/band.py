@@ -31,6 +31,7 @@ import bench  # noqa: E402
 from bench import Harness, kernel_summary, phase_medians, timed_run  # noqa: E402
 
 MB = 2**20
+FLAT_KIND = "ipc"       # "nvls" when the apps' flat parameters must be multicast-bound
 
 
 def make_apps(h, compute, comp_ns, nbytes, split=None, fwd_frac=1 / 3, gemm_ms=None):
@@ -38,7 +39,7 @@ def make_apps(h, compute, comp_ns, nbytes, split=None, fwd_frac=1 / 3, gemm_ms=N
     4096^3 GEMMs that takes comp_ns -- either way independent of the bucket size."""
     from paper_2103_07974_b200.apps import fixed_time_app
 
-    flat = "ipc" if h.world > 1 else False
+    flat = FLAT_KIND if h.world > 1 else False
     if compute == "spin":
         fwd, total, n = int(comp_ns * fwd_frac), int(comp_ns), 0
     else:
@@ -113,6 +114,8 @@ def main():
     from paper_2103_07974_b200.scheduler import Policy
 
     h = Harness()
+    global FLAT_KIND
+    FLAT_KIND = "nvls" if args.sync_mode == "nvls" else "ipc"
     args.sync_ctas = args.sync_ctas if args.sync_ctas == "auto" else int(args.sync_ctas)
     bench.SYNC_CTAS = -1 if args.sync_ctas == "auto" else args.sync_ctas
     bench.PACK_ENGINE = args.pack_engine
