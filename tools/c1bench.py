@@ -78,6 +78,31 @@ def main():
                 "ms": round(t, 4), "busbw_equiv_GB/s": round(nv / (t / 1e3) / 1e9, 1), "hbm_bytes": sync.k2_bytes()}
         _lib.tune("p2p_ctas", 0)
         sync.close()
+        # the NVSwitch-multicast fused sync (multimem.ld_reduce / multimem.st), same bucket
+        from paper_2103_07974_b200.nvls import nvls_available
+
+        if all(x for x in [nvls_available(h.dev)]):
+            pn = [torch.nn.Parameter(torch.randn(n - 32 * W, device=h.dev))]
+            flatn, _ = flatten_parameters(pn, 32, W, ipc="nvls")
+            for cap in [int(c) for c in args.p2p_caps.split(",")]:
+                syn = FusedGradientSync(pn, SgdSettings(0.01, momentum=0.9), h.comm, mode="nvls",
+                                        flat_params=flatn, p2p_ctas=cap)
+                ts = []
+                for it in range(args.iters + 2):
+                    syn.pack([g], s.cuda_stream)
+                    h.barrier()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(s)
+                    syn._nvls_tail(s.cuda_stream, None, None)
+                    b.record(s); b.synchronize()
+                    if it >= 2:
+                        ts.append(h.max_over_ranks(a.elapsed_time(b)))
+                t = statistics.median(ts)
+                nv = 2.0 * (W - 1) / W * n * 4
+                row[f"nvls_fused_with_barriers[ctas={cap}]"] = {
+                    "ms": round(t, 4), "busbw_equiv_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
+                syn.close()
+            del flatn, pn
         rows.append(row)
         if h.rank == 0:
             print(json.dumps(row), flush=True)
