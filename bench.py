@@ -642,6 +642,10 @@ def calibrate_transport(h: Harness, base, sm: str, prio: int = -1):
         probe.close()
         h.barrier()
         SYNC_CTAS = grid["choice"] if grid else 0
+    from paper_2103_07974_b200.nvls import nvls_buffer_of
+
+    if sm == "auto" and base[0].flat_params is not None and nvls_buffer_of(base[0].flat_params) is not None:
+        sm = "nvls"
     if h.world < 2 or sm not in ("p2p", "ce", "auto"):
         return sm, sm, ({"grid": grid} if grid else None)
     try:
@@ -742,9 +746,18 @@ def build_apps(args, h):
     from paper_2103_07974_b200 import apps
 
     rank, world, dev = h.rank, h.world, h.dev
-    # auto at W > 1: IPC flat parameters, and the scheduler picks the transport per policy
+    # auto at W > 1: multicast-bound flat parameters (the nvls transport: measured ahead of the
+    # ce / p2p transports for config 2 at W = 2 and 4, profiles/r02_nvls/) when every rank's GPU
+    # supports NVSwitch multicast, else IPC flat parameters and the adaptive ce / p2p choice
     flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc", "nvls": "nvls"}.get(args.sync_mode, False)
             if world > 1 else False)
+    if (flat == "ipc" and args.sync_mode == "auto" and args.config != "mlp" and not args.mix
+            and not args.scenario and world > 1):
+        from paper_2103_07974_b200.nvls import nvls_available
+        from paper_2103_07974_b200.p2p import all_ranks_agree
+
+        if all_ranks_agree(nvls_available(dev)):
+            flat = "nvls"
     if args.config == "mlp":
         w = max(2, world)
         local = w // world
@@ -783,11 +796,23 @@ def build_apps(args, h):
                                stem="cudnn" if args.cudnn_stem else "gemm"))
         args.no_e2e, args.no_cpu_baseline = True, True
     else:
+        from paper_2103_07974_b200.errors import ConfigError
+
         build = apps.resnet50_app if args.model == "resnet50" else apps.vgg16_app
-        base = [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
-                      graphed=_graphed_models(args), flat=flat, fast_bn=not args.aten_bn,
-                      stem="cudnn" if args.cudnn_stem else "gemm")
-                for j in range(args.jobs)]
+
+        def make(fl):
+            return [build(f"{args.model}_{j}", args.batch, 1, dev, seed=1000 * j, data_seed=1000 * j + rank,
+                          graphed=_graphed_models(args), flat=fl, fast_bn=not args.aten_bn,
+                          stem="cudnn" if args.cudnn_stem else "gemm")
+                    for j in range(args.jobs)]
+        try:
+            base = make(flat)
+        except ConfigError as exc:            # multicast setup failed on some rank (all agree)
+            if flat != "nvls" or args.sync_mode != "auto":
+                raise
+            if rank == 0:
+                print(f"nvls unavailable ({exc}); using IPC flat parameters", file=sys.stderr)
+            base = make("ipc")
     host = None if args.no_e2e else [
         apps._CycleData(apps.synthetic_image_batches(args.batch, 2, 7 + 1000 * j + rank, dev,
                                                      host_uint8=True))

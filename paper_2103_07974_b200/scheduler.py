@@ -303,11 +303,16 @@ class CrossoverScheduler:
         second than the P2P kernel -- so the crossover run is "adaptive" (:class:`_TransportTuner`
         measures both and keeps the faster); the sequential baseline has the GPU to itself and
         takes the fastest isolated path, the fused P2P kernel on the full grid.  Every transport
-        sums in rank order, so the weights are bitwise identical whichever runs."""
+        sums in rank order, so the weights are bitwise identical whichever runs.  Flat parameters
+        bound to an NVSwitch multicast object (flatten_parameters(ipc="nvls")) select the nvls
+        transport for both policies."""
         if self.sync_mode != "auto" or self.comm is None or self.comm.world < 2:
             return self.sync_mode
+        from .nvls import nvls_buffer_of
         from .p2p import buffer_of
 
+        if app.flat_params is not None and app.local_workers == 1 and nvls_buffer_of(app.flat_params) is not None:
+            return "nvls"          # multicast-bound flat parameters: the switch reduces and broadcasts
         if app.flat_params is None or buffer_of(app.flat_params) is None or app.local_workers != 1:
             return self.sync_mode
         return "adaptive" if self.policy is Policy.CROSSOVER else "p2p"

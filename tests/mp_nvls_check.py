@@ -75,6 +75,14 @@ def main():
         wr = max(float(np.max(np.abs(lw[k][:, :8].numpy().astype(np.float64) - ref[k]) /
                               (1e-5 + 1e-4 * np.abs(ref[k])))) for k in range(2))
         res["checks"].append({"name": "linear_momentum_nvls_vs_fp64_oracle", "ok": wr <= 1.0, "worst_ratio": wr})
+        # sync_mode="auto" with multicast-bound flat parameters selects nvls (both policies)
+        apps = [linear_app(lcfg[0], "auto0", 40, 4, dev, local_workers=1, momentum=0.9, flat="nvls")]
+        for pol in (Policy.CROSSOVER, Policy.SEQUENTIAL):
+            s = CrossoverScheduler(pol, comm=comm, sync_mode="auto")
+            s.register(apps[0])
+            res["checks"].append({"name": f"auto_selects_nvls_{pol.value}", "ok": s.states[0].sync.mode == "nvls"})
+            s.run()
+            s.close()
         res["ok"] = all(c["ok"] for c in res["checks"])
     oks = [None] * world
     dist.all_gather_object(oks, res["ok"])
