@@ -58,7 +58,7 @@ class RotationGraph:
         for st in sched.states:
             if st.app.data_graph is None:
                 raise ConfigError(f"job {st.job_id!r}: graph mode needs App.data_graph")
-            if st.sync.mode not in ("bucket", "sharded", "p2p", "ce", "adaptive"):
+            if st.sync.mode not in ("bucket", "sharded", "p2p", "ce", "adaptive", "nvls"):
                 raise ConfigError(f"job {st.job_id!r}: graph mode needs a bucket transport "
                                   f"(got {st.sync.mode!r})")
             if st.sync.snapshot is not None:
