@@ -404,7 +404,8 @@ class Clocks:
 
 
 class Harness:
-    """Per-process plumbing shared by bench.py and tools/sweep.py: device, comm, barrier, max."""
+    """Per-process plumbing shared by bench.py and the tools (band, c1bench, cebench): device, comm,
+    barrier, max over ranks."""
 
     def __init__(self, nccl_max_ctas: int = 0):
         import torch
