@@ -1,9 +1,10 @@
 """B200-native CrossoverScheduler (arXiv 2103.07974).
 
 Several data-parallel training apps share every GPU in a fixed rotation; one
-app's fused-gradient synchronization (K1 pack -> NCCL all-reduce -> K2 fused
-average + SGD update) runs on the comm stream while the next app's
-forward/backward occupies the SMs.  The public API mirrors the reference
+app's fused-gradient synchronization (K1 pack -> bucket exchange over NVLink -- NCCL,
+the fused P2P kernel, copy-engine pulls or NVSwitch multicast -> K2 fused average +
+SGD update) runs on the comm stream while the next app's forward/backward occupies
+the SMs.  The public API mirrors the reference
 simulator (colosim, /root/reference/pkg/src/colosim/__init__.py:11-56): plans,
 policies, traces, metrics -- backed by the device pipeline instead of a
 discrete-event simulation.
@@ -57,8 +58,9 @@ _DEVICE_EXPORTS = {
     "schedule_sequential": "scheduler", "rotation_schedule": "scheduler",
     "steady_state_period": "scheduler", "predicted_speedup": "scheduler",
     "overlap_roofline": "scheduler",
-    "SgdSettings": "fusion", "FusedGradientSync": "fusion",
-    "NcclCommunicator": "comm",
+    "SgdSettings": "fusion", "FusedGradientSync": "fusion", "flatten_parameters": "fusion",
+    "NcclCommunicator": "comm", "PeerGroup": "comm",
+    "RotationGraph": "graphs", "NvlsBuffer": "nvls",
 }
 
 
