@@ -129,7 +129,10 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
                 "bound": "nvlink", "achieved": ach, "peak": NVLINK_P2P_GBS, "unit": "GB/s",
                 "frac": round(ach / NVLINK_P2P_GBS, 4), "traffic": None,
                 "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                "bytes_per_launch": k["nvlink_bytes"], "grid_cap_ctas": int(sync._nvls.max_ctas) or "2 per SM"}
+                "bytes_per_launch": k["nvlink_bytes"], "grid_cap_ctas": int(sync._nvls.max_ctas) or "2 per SM",
+                "bytes_convention": "all-reduce bus bytes 2(W-1)/W*S (NCCL busbw)",
+                "link_bytes_per_direction": k["link_bytes_per_direction"],
+                "link_frac": round(k["link_GB/s"] / NVLINK_P2P_GBS, 4)}
     if "k2_p2p_fused" in kernels:
         k = kernels["k2_p2p_fused"]
         per_dir = sync.c1_bus_bytes()          # 2(W-1)/W * S through each GPU's links per direction
@@ -711,8 +714,11 @@ def kernel_summary(kern: dict, sync) -> dict:
     if "k2_nvls_fused" in kern:
         t = statistics.mean(kern["k2_nvls_fused"])
         nv = sync.c1_bus_bytes()
+        link = sync.nvls_link_bytes()
         out["k2_nvls_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes("nvls"),
-                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
+                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1),
+                                "link_bytes_per_direction": link,
+                                "link_GB/s": round(link / (t / 1e3) / 1e9, 1)}
     if "c1_allreduce" in kern:
         t = statistics.mean(kern["c1_allreduce"])
         out["c1_allreduce"] = {"ms": round(t, 4), "bus_bytes": sync.c1_bus_bytes(),
@@ -747,13 +753,16 @@ def build_apps(args, h):
     from paper_2103_07974_b200 import apps
 
     rank, world, dev = h.rank, h.world, h.dev
-    # auto at W > 1: multicast-bound flat parameters (the nvls transport: measured ahead of the
-    # ce / p2p transports for config 2 at W = 2 and 4, profiles/r02_nvls/) when every rank's GPU
-    # supports NVSwitch multicast, else IPC flat parameters and the adaptive ce / p2p choice
+    # auto at W >= 4: multicast-bound flat parameters (the nvls transport) when every rank's GPU
+    # supports NVSwitch multicast, else IPC flat parameters and the adaptive ce / p2p choice.  Per
+    # rank and link direction nvls moves S(1 + 1/W) bytes (the switch reads every member's shard,
+    # the local one included, and fans the stores out to every member) against 2S(W-1)/W for the
+    # peer-to-peer transports, so it only pays from W = 4 up (W = 2: 1.5S vs S, and the fused sync
+    # measured 0.33 vs 0.20 ms, profiles/r02_nvls/c1_w2.json; W = 4: 1.25S vs 1.5S).
     flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc", "nvls": "nvls"}.get(args.sync_mode, False)
             if world > 1 else False)
     if (flat == "ipc" and args.sync_mode == "auto" and args.config != "mlp" and not args.mix
-            and not args.scenario and world > 1):
+            and not args.scenario and world >= 4):
         from paper_2103_07974_b200.nvls import nvls_available
         from paper_2103_07974_b200.p2p import all_ranks_agree
 

@@ -666,6 +666,13 @@ class FusedGradientSync:
             per += 2 * s                   # read + write the momentum buffer
         return per
 
+    def nvls_link_bytes(self) -> int:
+        """Bytes through each GPU's NVLink ports per direction for one nvls sync: the switch reads
+        every member's copy of every rank's shard (W shards out, the local copy included) and fans
+        each rank's new shard out to every member (W shards in), plus the reduced shard back to
+        the issuer and the issuer's own stores: (W + 1) shards each way."""
+        return (self.ranks + 1) * self.shard * 4
+
     def c1_bus_bytes(self) -> float:
         """All-reduce bus bytes 2(W-1)/W * S (== reduce-scatter + all-gather in sharded mode)."""
         w = self.ranks
