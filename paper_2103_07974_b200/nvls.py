@@ -38,8 +38,9 @@ def nvls_buffer_of(t: torch.Tensor) -> "NvlsBuffer | None":
     return _live.get(t.data_ptr())
 
 
-def _share_fd(fd: int, rank: int, world: int) -> int:
-    """Rank 0's file descriptor to every rank (returns this rank's own descriptor)."""
+def _share_fd(fd: int, rank: int, world: int, timeout: float = 60.0) -> int:
+    """Rank 0's file descriptor to every rank (returns this rank's own descriptor, -1 on failure;
+    a failure is agreed on by the caller, so no rank waits for a peer that gave up)."""
     import torch.distributed as dist
 
     path = [None]
@@ -50,6 +51,7 @@ def _share_fd(fd: int, rank: int, world: int) -> int:
         server = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
         server.bind(path[0])
         server.listen(world)
+        server.settimeout(timeout)
     dist.broadcast_object_list(path, src=0)
     if rank == 0:
         try:
@@ -57,21 +59,29 @@ def _share_fd(fd: int, rank: int, world: int) -> int:
                 conn, _ = server.accept()
                 with conn:
                     socket.send_fds(conn, [b"f"], [fd])
+        except OSError:
+            return -1
         finally:
             server.close()
             os.unlink(path[0])
             os.rmdir(os.path.dirname(path[0]))
         return fd
-    sock = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-    for _ in range(200):
+    deadline = time.monotonic() + timeout
+    with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as sock:
+        sock.settimeout(timeout)
+        while True:
+            try:
+                sock.connect(path[0])
+                break
+            except (FileNotFoundError, ConnectionRefusedError):
+                if time.monotonic() > deadline:
+                    return -1
+                time.sleep(0.01)
         try:
-            sock.connect(path[0])
-            break
-        except (FileNotFoundError, ConnectionRefusedError):
-            time.sleep(0.01)
-    with sock:
-        _, fds, _, _ = socket.recv_fds(sock, 1, 1)
-    return fds[0]
+            _, fds, _, _ = socket.recv_fds(sock, 1, 1)
+        except OSError:
+            return -1
+    return fds[0] if fds else -1
 
 
 class NvlsBuffer:
@@ -106,9 +116,14 @@ class NvlsBuffer:
             if not all_ranks_agree(not error):
                 raise ConfigError("nvls multicast object creation failed" + (f" ({error})" if error else ""))
             myfd = _share_fd(fd.value, rank, world)
-            if rank != 0 and _lib.lib.cs_nvls_import(myfd, ctypes.byref(mc)):
+            if myfd < 0:
+                error = f"rank {rank}: passing the multicast handle over a UNIX socket failed"
+            elif rank != 0 and _lib.lib.cs_nvls_import(myfd, ctypes.byref(mc)):
                 error = f"rank {rank}: {_lib.lib.cs_last_error().decode()}"
-            os.close(myfd)
+            if myfd >= 0:
+                os.close(myfd)
+            elif rank == 0:
+                os.close(fd.value)
             self.mc = int(mc.value)
             if not error and _lib.lib.cs_nvls_add_device(self.mc, self.dev_index):
                 error = f"rank {rank}: {_lib.lib.cs_last_error().decode()}"

@@ -8,7 +8,9 @@ Drives the product's own classes -- no GPU needed:
   peer transports require (a rank on ce and a rank on p2p would not exchange the same data);
 * FlagArray's shared-memory rendezvous and its collective failure agreement: rank 0 creates the
   segment, every rank attaches by name; where the page-locking step fails (no CUDA here) every
-  rank raises ConfigError together and the segment is unlinked -- no rank is left waiting.
+  rank raises ConfigError together and the segment is unlinked -- no rank is left waiting;
+* the nvls transport's multicast-handle passing (a POSIX file descriptor from rank 0 to every rank
+  over a UNIX-domain socket).
 """
 
 import os
@@ -49,6 +51,21 @@ def _worker(rank, world, port, q):
     out["periods"] = tuner.periods_ms
     out["agree_all"] = all_ranks_agree(True)
     out["agree_one_no"] = all_ranks_agree(rank != world - 1)
+    # the nvls transport's handle passing: rank 0's file descriptor reaches every rank (SCM_RIGHTS)
+    from paper_2103_07974_b200.nvls import _share_fd
+
+    import tempfile
+
+    fd = -1
+    if rank == 0:
+        tf = tempfile.TemporaryFile()
+        tf.write(b"multicast-handle")
+        tf.flush()
+        fd = os.dup(tf.fileno())
+    got = _share_fd(fd, rank, world)
+    out["fd_payload"] = os.pread(got, 64, 0) if got >= 0 else None
+    if got >= 0:
+        os.close(got)
     names_before = set(os.listdir("/dev/shm")) if os.path.isdir("/dev/shm") else set()
     try:
         FlagArray(rank, world)
@@ -86,6 +103,7 @@ def test_peer_group_tuner_and_flag_rendezvous(world):
     assert res[0]["choice"] == ("ce" if ce <= p2p else "p2p")
     assert all(abs(r["periods"]["ce"] - ce) < 1e-12 and abs(r["periods"]["p2p"] - p2p) < 1e-12 for r in res)
     assert all(r["agree_all"] for r in res) and not any(r["agree_one_no"] for r in res)
+    assert all(r["fd_payload"] == b"multicast-handle" for r in res)
     # without CUDA page-locking fails on every rank, and every rank refuses together
     import torch
 
