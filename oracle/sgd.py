@@ -13,8 +13,9 @@ Restates /root/reference/pkg/src/colosim/equivalence.py:
 Everything is float64 like the reference; `dtype=np.float32` runs the same
 sequence in fp32 (the device's arithmetic type) to bound the expected drift.
 
-Extensions with no reference counterpart (parity UNPINNED):
-  mlp_*               784-256-10 MLP, cross-entropy (config 1)
+Extensions with no reference counterpart (parity UNPINNED by reference vectors):
+  mlp_*               784-256-10 MLP, cross-entropy (config 1); cross-checked against torch
+                      autograd + torch.optim.SGD in fp64 (tests/test_oracle_golden.py)
   torch_sgd_step      torch.optim.SGD momentum/weight-decay/nesterov semantics
 """
 

@@ -160,3 +160,33 @@ def test_fixture_inventories_match_torchvision(fixtures_golden):
     vs = [p.numel() * 4 for p in v.parameters()]
     assert vs == fixtures_golden["vgg16"]["sizes"]
     assert sum(vs) == 553_430_176 and len(vs) == 32
+
+
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_mlp_trajectory_vs_torch_fp64(momentum):
+    """The config-1 MLP oracle has no reference counterpart (SURVEY §8 c), so cross-check the whole
+    trajectory against an independent implementation: torch autograd + torch.optim.SGD in fp64,
+    the W workers' gradients averaged in worker order (equivalence.py:150-160's structure)."""
+    import torch
+
+    T, W, B, size, lr = 4, 2, 16, 256, 0.05
+    specs = [(11, 0), (12, 1)]
+    traj = osgd.run_mlp_crossover(specs, T, W, batch=B, lr=lr, dataset_size=size, momentum=momentum)
+    for k, (ds, rs) in enumerate(specs):
+        x, y = osgd.mlp_dataset(ds, size)
+        ps = [torch.tensor(p, dtype=torch.float64, requires_grad=True) for p in osgd.mlp_init(rs)]
+        opt = torch.optim.SGD(ps, lr=lr, momentum=momentum, foreach=False)
+        for t in range(1, T + 1):
+            acc = [torch.zeros_like(p) for p in ps]
+            for w in range(W):
+                idx = osgd.batch_indices(rs, t, w, size, B)
+                xb, yb = torch.tensor(x[idx]), torch.tensor(y[idx])
+                h = torch.relu(xb @ ps[0].T + ps[1])
+                loss = torch.nn.functional.cross_entropy(h @ ps[2].T + ps[3], yb)
+                gs = torch.autograd.grad(loss, ps)
+                acc = [a + g for a, g in zip(acc, gs)]
+            for p, a in zip(ps, acc):
+                p.grad = a / W
+            opt.step()
+            for got, want in zip(traj[k][t - 1], ps):
+                np.testing.assert_allclose(got, want.detach().numpy(), rtol=1e-12, atol=1e-14)
