@@ -406,6 +406,29 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class Energy:
+    """The GPU's cumulative energy counter (NVML, mJ) around a timed region: average board power over
+    it, against the enforced power limit (tools/band.py's power accounting)."""
+
+    def __init__(self, device):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        self.nv = pynvml
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda._get_nvml_device_index(device))
+        self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+
+    def read(self) -> tuple[float, float]:
+        return time.perf_counter(), self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) / 1000.0
+
+    @staticmethod
+    def between(a, b) -> dict:
+        dt = b[0] - a[0]
+        return {"joules": round(b[1] - a[1], 4), "seconds": round(dt, 5),
+                "watts": round((b[1] - a[1]) / dt, 1) if dt > 0 else None}
+
+
 class Harness:
     """Per-process plumbing shared by bench.py and the tools (band, c1bench, cebench): device, comm,
     barrier, max over ranks."""
@@ -437,6 +460,13 @@ class Harness:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def mean_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64)
+        self.dist.all_reduce(t)
+        return float(t.item()) / self.world
+
     def close(self):
         if self.comm is not None:
             self.comm.close()
@@ -448,6 +478,7 @@ P2P_CTAS: int | None = None   # --p2p-ctas; None = the scheduler's per-policy de
 SYNC_CTAS: int | None = None  # --sync-ctas; None = the scheduler's default K1 / K2 grid
 PACK_ENGINE = "sm"            # --pack-engine: K1 by a kernel (sm) or by the copy engines (ce)
 BARRIER = "auto"              # --barrier: cross-rank barrier of the p2p / ce transports
+ENERGY: Energy | None = None  # set by tools/band.py: NVML energy counter around timed regions
 
 
 def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: bool = False,
@@ -496,6 +527,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     gc.collect()
     gc.disable()
     clk = Clocks(h.local) if clocks else None
+    e0 = ENERGY.read() if ENERGY is not None else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(cs)
     for _ in range(K):
@@ -505,6 +537,7 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     cs.wait_event(join)
     end.record(cs)
     end.synchronize()
+    energy = Energy.between(e0, ENERGY.read()) if e0 is not None else None
     gc.enable()
     clk_info = clk.stop() if clk else None
     ms_total = h.max_over_ranks(start.elapsed_time(end))
@@ -514,7 +547,8 @@ def timed_run(h: Harness, base, policy, W: int, K: int, host_data=None, clocks: 
     out = {"ms": ms_total, "trace": trace, "timed_spans": trace.spans[n_spans0:],
            "replicas_identical": replicas_identical(h, base),
            "kernels": sched.timer.summary() if sched.timer is not None else {},
-           "launches": sched.kernel_launches - launches0, "clocks": clk_info, "sched": sched}
+           "launches": sched.kernel_launches - launches0, "clocks": clk_info, "energy": energy,
+           "sched": sched}
     return out
 
 

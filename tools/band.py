@@ -13,7 +13,9 @@ the sync time of the chosen transport is fitted as t(S) = a + S / B from two cal
 Two co-located apps per run (fixed_time_app: compute = spin kernel of known duration on one SM,
 or --compute gemm: a bf16 GEMM chain of the same duration), crossover and sequential with the same
 transport and launch caps.  Per rho: measured rho (sequential medians), speedup T_seq / T_cross, the
-closed form (1 + rho) / max(1, rho) (pkg/README.md:69-70), and the overlap-roofline fractions.
+closed form (1 + rho) / max(1, rho) (pkg/README.md:69-70), the overlap-roofline fractions, and the
+split of any shortfall: comp_inflation (compute phases under crossover / alone) and
+gpu_lane_busy_frac (compute phases / crossover rotation; 1 = the schedule hid every sync).
 --scenario-band adds the reference's own speedup_band.json jobs (124.75 MB in 4 tensors, forward :
 backward = 30 : 70) with the compute dialed to the scenario's priced rho = 3/20.
 """
@@ -22,6 +24,7 @@ import dataclasses
 import json
 import statistics
 import sys
+import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -32,6 +35,7 @@ from bench import Harness, kernel_summary, phase_medians, timed_run  # noqa: E40
 
 MB = 2**20
 FLAT_KIND = "ipc"       # "nvls" when the apps' flat parameters must be multicast-bound
+IDLE_W = 0.0            # --energy: board power with the GPU idle, measured at start
 
 
 def make_apps(h, compute, comp_ns, nbytes, split=None, fwd_frac=1 / 3, gemm_ms=None):
@@ -62,20 +66,30 @@ def measure(h, base, args, policy_runs=("crossover", "sequential")):
     seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=args.sync_mode,
                     p2p_ctas=p2p_cap.max_ctas if p2p_cap is not None else None)
     order = [a.job_id for a in base]
+    rx, rs = cross["ms"] / args.steps, seq["ms"] / args.steps
     comp, comm = phase_medians(seq["timed_spans"], order)
     rho = sum(comm) / sum(comp)
     roof = overlap_roofline(comp, comm)
-    rx, rs = cross["ms"] / args.steps, seq["ms"] / args.steps
     pred = (1 + rho) / max(1.0, rho)
-    if args.spans:
-        # per-phase medians of the overlapped run next to the sequential ones: where the time goes
-        cc, cm = phase_medians(cross["timed_spans"], order)
-        out["crossover_phase_ms"] = {"comp": [round(c, 4) for c in cc], "comm": [round(c, 4) for c in cm]}
-        gaps = []
-        gpu = sorted((s.start, s.end) for s in cross["timed_spans"] if s.lane_id == "gpu0")
-        for (a0, a1), (b0, b1) in zip(gpu, gpu[1:]):
-            gaps.append(max(0, b0 - a1) / 1e6)
-        out["crossover_gpu_idle_ms_per_rotation"] = round(sum(gaps) / args.steps, 4)
+    # where the crossover time goes: the compute phases as measured while the syncs overlap them
+    # (slower than alone when the sync takes power / SM time from them) and the GPU
+    # lane's idle time between them (what the schedule failed to hide)
+    cc, cm = phase_medians(cross["timed_spans"], order)
+    out["crossover_phase_ms"] = {"comp": [round(c, 4) for c in cc], "comm": [round(c, 4) for c in cm]}
+    gpu = sorted((s.start, s.end) for s in cross["timed_spans"] if s.lane_id == "gpu0")
+    idle = sum(max(0, b0 - a1) for (_, a1), (b0, _) in zip(gpu, gpu[1:])) / 1e6
+    out["crossover_gpu_idle_ms_per_rotation"] = round(idle / args.steps, 4)
+    out["comp_inflation"] = round(sum(cc) / sum(comp), 4)
+    out["gpu_lane_busy_frac"] = round(sum(cc) / rx, 4)
+    out["nic_lane_busy_frac"] = round(sum(cm) / rx, 4)          # the bound lane when rho > 1
+    if cross.get("energy") and seq.get("energy"):
+        # board power over the timed regions (NVML energy counter, mean over ranks) against the
+        # enforced limit.  No energy bound is derived from it: under the cap the controller lowers
+        # clock and voltage, so the same work costs less energy in the crossover arm than in the
+        # sequential one (measured: a naive E_seq / P_limit "bound" is beaten by every GEMM point).
+        out["power"] = {"crossover_w": round(h.mean_over_ranks(cross["energy"]["watts"]), 1),
+                        "sequential_w": round(h.mean_over_ranks(seq["energy"]["watts"]), 1),
+                        "limit_w": bench.ENERGY.limit_w, "idle_w": round(IDLE_W, 1)}
     out.update({"rho_measured": round(rho, 4), "speedup": round(rs / rx, 4), "predicted": round(pred, 4),
                 "speedup_over_predicted": round(rs / rx / pred, 4),
                 "rotation_ms": {"crossover": round(rx, 4), "sequential": round(rs, 4)},
@@ -106,7 +120,9 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scenario-band", action="store_true")
-    ap.add_argument("--spans", action="store_true", help="report crossover phase medians and GPU idle")
+    ap.add_argument("--spans", action="store_true", help="(always on) crossover phase medians and GPU idle")
+    ap.add_argument("--energy", action="store_true",
+                    help="board power over every timed region (NVML energy counter) and the power bound")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     import torch
@@ -114,7 +130,13 @@ def main():
     from paper_2103_07974_b200.scheduler import Policy
 
     h = Harness()
-    global FLAT_KIND
+    global FLAT_KIND, IDLE_W
+    if args.energy:
+        bench.ENERGY = bench.Energy(h.dev)
+        torch.cuda.synchronize()
+        a = bench.ENERGY.read()
+        time.sleep(2.0)
+        IDLE_W = h.mean_over_ranks(bench.Energy.between(a, bench.ENERGY.read())["watts"])
     FLAT_KIND = "nvls" if args.sync_mode == "nvls" else "ipc"
     args.sync_ctas = args.sync_ctas if args.sync_ctas == "auto" else int(args.sync_ctas)
     bench.SYNC_CTAS = -1 if args.sync_ctas == "auto" else args.sync_ctas
