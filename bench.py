@@ -111,6 +111,10 @@ def peaks():
 
 
 NVLINK_P2P_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
+# NVLS ceiling: multimem.ld_reduce + multimem.st of every rank's 102 MB shard with nothing else in
+# the kernel (no update, no barriers), 64 CTAs, all ranks at once, as all-reduce bus GB/s
+# (tools/nvls_ceiling.cu, profiles/r02_nvls_ceiling/w{2,4}_102.json)
+NVLS_CEILING_BUSBW = {2: 391.8, 4: 672.6}
 
 
 def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: str,
@@ -132,7 +136,11 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
                 "bytes_per_launch": k["nvlink_bytes"], "grid_cap_ctas": int(sync._nvls.max_ctas) or "2 per SM",
                 "bytes_convention": "all-reduce bus bytes 2(W-1)/W*S (NCCL busbw)",
                 "link_bytes_per_direction": k["link_bytes_per_direction"],
-                "link_frac": round(k["link_GB/s"] / NVLINK_P2P_GBS, 4)}
+                "link_frac": round(k["link_GB/s"] / NVLINK_P2P_GBS, 4),
+                "nvls_ceiling": ({"busbw_GBps": NVLS_CEILING_BUSBW[sync.ranks],
+                                  "frac": round(ach / NVLS_CEILING_BUSBW[sync.ranks], 4),
+                                  "source": "tools/nvls_ceiling.cu, 102 MB, 64 CTAs"}
+                                 if sync.ranks in NVLS_CEILING_BUSBW else None)}
     if "k2_p2p_fused" in kernels:
         k = kernels["k2_p2p_fused"]
         per_dir = sync.c1_bus_bytes()          # 2(W-1)/W * S through each GPU's links per direction

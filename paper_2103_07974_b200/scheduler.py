@@ -268,13 +268,16 @@ class CrossoverScheduler:
         for p in app.params:
             if p.device != self.device:
                 raise ConfigError(f"job {app.job_id!r}: parameters must be on {self.device}")
-        # SM footprint of the fused P2P sync: under crossover it overlaps another app's compute
-        # and has that compute as slack, so it holds few SMs (32 CTAs, ~NCCL's channel count);
-        # the sequential baseline runs it alone and uses the whole GPU (2 CTAs per SM).
+        # SM footprint of the fused P2P / NVLS sync: under crossover it overlaps another app's
+        # compute and has that compute as slack, so it holds few SMs (32 CTAs, ~NCCL's channel
+        # count; 64 for nvls, whose multimem.ld_reduce round trips through the switch need more
+        # loads in flight: 32 CTAs reach 0.58 of the W = 2 ceiling, 64 reach it,
+        # tools/nvls_ceiling.cu); the sequential baseline runs it alone on the whole GPU.
+        mode = self._mode_for(app)
         p2p_ctas = self.p2p_ctas if self.p2p_ctas is not None else (
-            32 if self.policy is Policy.CROSSOVER else 0)
+            (64 if mode == "nvls" else 32) if self.policy is Policy.CROSSOVER else 0)
         sync = FusedGradientSync(app.params, app.sgd, self.comm, app.local_workers, self.align,
-                                 self._mode_for(app), app.iterations if self.record_weights else 0,
+                                 mode, app.iterations if self.record_weights else 0,
                                  flat_params=app.flat_params, p2p_ctas=p2p_ctas,
                                  barrier=self.barrier, sync_ctas=self._sync_grid(),
                                  pack_engine=self.pack_engine)
