@@ -962,6 +962,14 @@ def run_ours(args):
         comp, comm_t = phase_medians(seq["timed_spans"], order)
         kernels = kernel_summary(cross["kernels"], sync0)
         kernels_isolated = kernel_summary(seq_best["kernels"], sync_seq)
+    split = None
+    if cross.get("timed_spans"):
+        # where the crossover rotation goes (tools/band.py): compute phases measured while the syncs
+        # overlap them vs alone, and the GPU lane's busy fraction
+        cc, cm = phase_medians(cross["timed_spans"], order)
+        split = {"crossover_comp_ms": [round(c, 4) for c in cc], "crossover_comm_ms": [round(c, 4) for c in cm],
+                 "comp_inflation": round(sum(cc) / sum(comp), 4) if sum(comp) else None,
+                 "gpu_lane_busy_frac": round(sum(cc) / (cross["ms"] / K), 4)}
     roof = overlap_roofline(comp, comm_t)
     rot_cross, rot_seq, rot_best = cross["ms"] / K, seq["ms"] / K, seq_best["ms"] / K
     value = samples_per_rot * K / (cross["ms"] / 1e3)
@@ -1026,7 +1034,8 @@ def run_ours(args):
                                  "frac": round(roof["north_star"] / rot_cross, 4),
                                  "frac_tight": round(roof["tight"] / rot_cross, 4),
                                  "comp_ms": [round(c, 4) for c in comp],
-                                 "comm_ms": [round(c, 4) for c in comm_t]},
+                                 "comm_ms": [round(c, 4) for c in comm_t],
+                                 "crossover_split": split},
             "roofline": roofline_line(kernels, sync0, hbm_peak, peak_kind,
                                       "mlp" if args.config == "mlp" else args.model,
                                       kernels_isolated, sync_seq),
