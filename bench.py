@@ -86,8 +86,8 @@ def parse():
                          "(cs_bn_backward2) instead of an autograd add kernel")
     ap.add_argument("--bn-no-pdl", action="store_true",
                     help="launch the BN finalize / apply kernels without programmatic dependent launch")
-    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "ce", "unfused",
-                                                            "nvls"],
+    ap.add_argument("--sync-mode", default="auto", choices=["auto", "bucket", "sharded", "p2p", "p2p_gather",
+                                                            "ce", "unfused", "nvls"],
                     help="W>1 sync: all-reduce bucket, reduce-scatter/all-gather (sharded) or "
                          "the fused NVLink P2P kernel; ce = copy-engine pulls + shard K2; auto = ce "
                          "under crossover and p2p for the sequential arm (bucket if peers cannot "
@@ -141,6 +141,16 @@ def roofline_line(kernels: dict, sync, hbm_peak: float, peak_kind: str, model: s
                                   "frac": round(ach / NVLS_CEILING_BUSBW[sync.ranks], 4),
                                   "source": "tools/nvls_ceiling.cu, 102 MB, 64 CTAs"}
                                  if sync.ranks in NVLS_CEILING_BUSBW else None)}
+    if "k2_p2p_gather" in kernels:
+        k = kernels["k2_p2p_gather"]
+        per_dir = sync.c1_bus_bytes()
+        ach = per_dir / (k["ms"] / 1e3) / 1e9
+        return {"kernel": "k2_p2p_gather (no K1: NVLink reads of every rank's gradient tensors in place, "
+                          "rank-order sum, /W, SGD-momentum, NVLink writes of the new shard to every rank)",
+                "bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_P2P_GBS, "unit": "GB/s",
+                "frac": round(ach / NVLINK_P2P_GBS, 4), "traffic": None,
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                "bytes_per_launch": per_dir, "grid_cap_ctas": int(sync._gather_ctas) or "2 per SM"}
     if "k2_p2p_fused" in kernels:
         k = kernels["k2_p2p_fused"]
         per_dir = sync.c1_bus_bytes()          # 2(W-1)/W * S through each GPU's links per direction
@@ -753,6 +763,12 @@ def kernel_summary(kern: dict, sync) -> dict:
         out["k2_p2p_fused"] = {"ms": round(t, 4), "bytes": sync.k2_bytes("p2p"),
                                "GB/s": round(sync.k2_bytes("p2p") / (t / 1e3) / 1e9, 1),
                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
+    if "k2_p2p_gather" in kern:
+        t = statistics.mean(kern["k2_p2p_gather"])
+        nv = sync.c1_bus_bytes()
+        out["k2_p2p_gather"] = {"ms": round(t, 4), "bytes": sync.k2_bytes("p2p_gather"),
+                                "GB/s": round(sync.k2_bytes("p2p_gather") / (t / 1e3) / 1e9, 1),
+                                "nvlink_bytes": nv, "nvlink_GB/s": round(nv / (t / 1e3) / 1e9, 1)}
     if "k2_nvls_fused" in kern:
         t = statistics.mean(kern["k2_nvls_fused"])
         nv = sync.c1_bus_bytes()
@@ -801,7 +817,8 @@ def build_apps(args, h):
     # the local one included, and fans the stores out to every member) against 2S(W-1)/W for the
     # peer-to-peer transports, so it only pays from W = 4 up (W = 2: 1.5S vs S, and the fused sync
     # measured 0.33 vs 0.20 ms, profiles/r02_nvls/c1_w2.json; W = 4: 1.25S vs 1.5S).
-    flat = ({"sharded": True, "p2p": "ipc", "ce": "ipc", "auto": "ipc", "nvls": "nvls"}.get(args.sync_mode, False)
+    flat = ({"sharded": True, "p2p": "ipc", "p2p_gather": "ipc", "ce": "ipc", "auto": "ipc",
+             "nvls": "nvls"}.get(args.sync_mode, False)
             if world > 1 else False)
     if (flat == "ipc" and args.sync_mode == "auto" and args.config != "mlp" and not args.mix
             and not args.scenario and world >= 4):

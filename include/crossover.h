@@ -48,7 +48,7 @@ extern "C" {
 #define CS_API
 #endif
 
-#define CS_ABI_VERSION 2
+#define CS_ABI_VERSION 3
 #define CS_ERR_ARG (-1)
 #define CS_ERR_NCCL_BASE 10000
 #define CS_NCCL_UNIQUE_ID_BYTES 128
@@ -172,6 +172,27 @@ typedef struct cs_p2p_desc {
 CS_API int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* desc, const cs_sgd_hyper* hyper,
                                    void* stream);
 
+/* The same update without K1 ("p2p_gather"): every rank's GRADIENT TENSORS are read in place over
+ * NVLink (no bucket, no pack).  This rank's shard of the bucket layout is cut into pieces, one per
+ * gradient tensor it overlaps; piece i is a cs_p2p_desc whose src[r] points into rank r's gradient
+ * tensor (mapped in this process), dst[r] / param / momentum_buf at the piece's offset of the flat
+ * parameters / momentum shard, numel its length.  Work items are chunks (piece, e0) with e0 a
+ * multiple of cs_p2p_gather_chunk_elems(nranks), one per chunk of every piece.  Arithmetic and
+ * sum order are cs_p2p_reduce_sgd_bcast's, so the result is bit-identical to it (and to K1 + p2p).
+ * Gradients must stay at these addresses while syncs run (CUDA-graphed backward passes).
+ * cs_p2p_gather_check validates a host copy of the tables; the launch takes device copies. */
+typedef struct cs_gather_chunk {
+  int32_t piece;
+  int32_t pad_;
+  int64_t e0;
+} cs_gather_chunk;
+CS_API int64_t cs_p2p_gather_chunk_elems(int nranks);
+CS_API int cs_p2p_gather_check(const cs_p2p_desc* pieces, int64_t npieces, const cs_gather_chunk* chunks,
+                               int64_t nchunks, int nranks, int momentum);
+CS_API int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* pieces_dev, const cs_gather_chunk* chunks_dev,
+                                          int64_t nchunks, int nranks, int max_ctas,
+                                          const cs_sgd_hyper* hyper, void* stream);
+
 /* Collective-fused update through NVSwitch multicast (NVLS): same contract as
  * cs_p2p_reduce_sgd_bcast, but the W-rank sum is a multimem.ld_reduce on the multicast mapping of
  * the buckets (the switch adds; its order is unspecified, so results match the rank-order
@@ -210,6 +231,10 @@ CS_API int cs_device_free(void* ptr);
 CS_API int cs_ipc_get_handle(void* ptr, uint8_t* out /* CS_IPC_HANDLE_BYTES */);
 CS_API int cs_ipc_open_handle(const uint8_t* handle, void** ptr);
 CS_API int cs_ipc_close_handle(void* ptr);
+/* Base address and size of the device allocation that contains ptr (cuMemGetAddressRange): the
+ * IPC handle of a tensor inside a caching allocator's segment is its segment's handle plus the
+ * offset ptr - base. */
+CS_API int cs_ipc_base_of(const void* ptr, void** base, size_t* size);
 /* Stream-ordered copy by the copy engines (cudaMemcpyAsync, cudaMemcpyDefault): src / dst may be
  * local or peer-mapped (IPC) device memory, so a pull from a peer crosses NVLink without
  * occupying any SM -- the transport of the "ce" sync mode. */

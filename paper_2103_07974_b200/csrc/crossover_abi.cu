@@ -340,6 +340,77 @@ int cs_ipc_close_handle(void* ptr) {
   return cuda_status(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
 }
 
+int cs_ipc_base_of(const void* ptr, void** base, size_t* size) {
+  if (ptr == nullptr || base == nullptr || size == nullptr)
+    return set_error(CS_ERR_ARG, "cs_ipc_base_of: NULL argument");
+  typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN_range range = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", (void**)&range, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      range = nullptr;
+    cudaGetLastError();
+  });
+  if (range == nullptr) return set_error((int)cudaErrorNotSupported, "cs_ipc_base_of: no cuMemGetAddressRange");
+  CUdeviceptr b = 0;
+  size_t n = 0;
+  const CUresult r = range(&b, &n, (CUdeviceptr)ptr);
+  if (r != CUDA_SUCCESS) return set_error((int)r, "cs_ipc_base_of(%p): cuMemGetAddressRange failed (%d)", ptr, (int)r);
+  *base = (void*)b;
+  *size = n;
+  return 0;
+}
+
+int64_t cs_p2p_gather_chunk_elems(int nranks) {
+  if (nranks < 1 || nranks > CS_MAX_SOURCES) return 0;
+  return p2p_gather_chunk_elems(nranks);
+}
+
+int cs_p2p_gather_check(const cs_p2p_desc* pieces, int64_t npieces, const cs_gather_chunk* chunks,
+                        int64_t nchunks, int nranks, int momentum) {
+  if ((npieces > 0 && pieces == nullptr) || (nchunks > 0 && chunks == nullptr) || npieces < 0 || nchunks < 0)
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_check: bad table");
+  if (nranks < 1 || nranks > CS_MAX_SOURCES)
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_check: nranks=%d outside [1, %d]", nranks, CS_MAX_SOURCES);
+  const int64_t ch = p2p_gather_chunk_elems(nranks);
+  for (int64_t i = 0; i < npieces; ++i) {
+    const cs_p2p_desc& d = pieces[i];
+    if (d.nranks != nranks || d.numel <= 0 || d.param == nullptr || (momentum && d.momentum_buf == nullptr))
+      return set_error(CS_ERR_ARG, "cs_p2p_gather_check: piece %lld malformed", (long long)i);
+    uintptr_t al = (uintptr_t)d.param | (uintptr_t)d.momentum_buf;
+    for (int r = 0; r < nranks; ++r) {
+      if (d.src[r] == 0 || d.dst[r] == 0)
+        return set_error(CS_ERR_ARG, "cs_p2p_gather_check: piece %lld: NULL address of rank %d", (long long)i, r);
+      al |= (uintptr_t)d.src[r] | (uintptr_t)d.dst[r];
+    }
+    if (al & 15u) return set_error(CS_ERR_ARG, "cs_p2p_gather_check: piece %lld not 16-byte aligned", (long long)i);
+  }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const cs_gather_chunk& k = chunks[c];
+    if (k.piece < 0 || k.piece >= npieces || k.e0 < 0 || k.e0 >= pieces[k.piece].numel || k.e0 % ch)
+      return set_error(CS_ERR_ARG, "cs_p2p_gather_check: chunk %lld out of range", (long long)c);
+  }
+  return 0;
+}
+
+int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* pieces_dev, const cs_gather_chunk* chunks_dev,
+                                   int64_t nchunks, int nranks, int max_ctas, const cs_sgd_hyper* h,
+                                   void* stream) {
+  if (h == nullptr || (nchunks > 0 && (pieces_dev == nullptr || chunks_dev == nullptr)) || nchunks < 0)
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: NULL argument");
+  if (nranks < 1 || nranks > CS_MAX_SOURCES || max_ctas < 0)
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: bad nranks / max_ctas");
+  if (h->divisor != nranks)
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: divisor %d != nranks %d", h->divisor, nranks);
+  if (!(h->lr > 0.0f)) return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: learning rate must be > 0");
+  if (h->rounding == CS_ROUND_REFERENCE && (h->momentum != 0.0f || h->weight_decay != 0.0f))
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: reference rounding has no momentum / weight decay");
+  return cuda_status(launch_p2p_gather(pieces_dev, chunks_dev, nchunks, nranks, max_ctas, *h, (cudaStream_t)stream),
+                     "cs_p2p_gather_reduce_sgd_bcast launch");
+}
+
 size_t cs_bn_workspace_bytes(int64_t M, int C) {
   if (M <= 0 || C <= 0 || C % 8) return 0;
   return bn_workspace_bytes(M, C);

@@ -146,6 +146,62 @@ static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream
   else p2p_reduce_sgd_bcast_kernel<false, U, MAXW><<<(unsigned)grid, kThreads, 0, s>>>(d, h);
 }
 
+// ---------------------------------------------------------------------------------------------
+// K1-free variant: the pieces of this rank's shard read every rank's gradient tensors in place.
+// Each work item is one chunk of one piece; its descriptor is staged in shared memory once per
+// chunk (the per-element code is p2p_chunk's, so the arithmetic is bit-identical).
+// ---------------------------------------------------------------------------------------------
+template <bool kMom, int U, int MAXW>
+__global__ void __launch_bounds__(kThreads)
+p2p_gather_kernel(const cs_p2p_desc* __restrict__ pieces, const cs_gather_chunk* __restrict__ chunks,
+                  int64_t nchunks, const __grid_constant__ cs_sgd_hyper h) {
+  __shared__ cs_p2p_desc sd;
+  const Rule r = make_rule(h, kMom);
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const cs_gather_chunk ch = chunks[c];
+    if (threadIdx.x == 0) sd = pieces[ch.piece];
+    __syncthreads();
+    p2p_chunk<kMom, U, MAXW>(sd, r, ch.e0);
+    __syncthreads();          // sd is rewritten for the next chunk
+  }
+  __threadfence_system();
+}
+
+template <int U>
+static int64_t gather_grid(int64_t nchunks, int max_ctas) {
+  int cap = max_ctas > 0 ? max_ctas : g_tune_p2p_ctas;
+  if (cap <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = 2 * sms;
+  }
+  return nchunks < cap ? nchunks : cap;
+}
+
+template <int U, int MAXW>
+static void launch_gather_u(const cs_p2p_desc* pieces, const cs_gather_chunk* chunks, int64_t nchunks,
+                            int max_ctas, const cs_sgd_hyper& h, cudaStream_t s) {
+  const unsigned grid = (unsigned)gather_grid<U>(nchunks, max_ctas);
+  if (h.momentum != 0.0f) p2p_gather_kernel<true, U, MAXW><<<grid, kThreads, 0, s>>>(pieces, chunks, nchunks, h);
+  else p2p_gather_kernel<false, U, MAXW><<<grid, kThreads, 0, s>>>(pieces, chunks, nchunks, h);
+}
+
+int64_t p2p_gather_chunk_elems(int nranks) {
+  if (nranks <= 2) return p2p_chunk_elems<4>();
+  if (nranks <= 4) return p2p_chunk_elems<2>();
+  return p2p_chunk_elems<1>();
+}
+
+cudaError_t launch_p2p_gather(const cs_p2p_desc* pieces, const cs_gather_chunk* chunks, int64_t nchunks,
+                              int nranks, int max_ctas, const cs_sgd_hyper& h, cudaStream_t s) {
+  if (nchunks == 0) return cudaSuccess;
+  if (nranks <= 2) launch_gather_u<4, 2>(pieces, chunks, nchunks, max_ctas, h, s);
+  else if (nranks <= 4) launch_gather_u<2, 4>(pieces, chunks, nchunks, max_ctas, h, s);
+  else launch_gather_u<1, CS_MAX_SOURCES>(pieces, chunks, nchunks, max_ctas, h, s);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
   if (d.nranks <= 2) launch_p2p_u<4, 2>(d, h, s);

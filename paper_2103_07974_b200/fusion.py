@@ -114,6 +114,8 @@ class FusedGradientSync:
       bucket    K1 -> NCCL all-reduce of the bucket -> K2 (also W simulated workers on one GPU)
       sharded   K1 -> reduce-scatter -> K2 on this rank's shard -> all-gather into flat params
       p2p       K1 -> barrier -> one NVLink kernel (rank-order reduce, /W, SGD, broadcast writes)
+      p2p_gather  no K1: barrier -> the same kernel reading every rank's gradient tensors in place
+                (static gradient addresses: CUDA-graphed backward passes) -> barrier
       ce        K1 -> barrier -> copy-engine pulls -> shard K2 -> barrier -> copy-engine pulls
       adaptive  p2p and ce over the same buffers; the scheduler picks one per sync
       unfused   one all-reduce per gradient tensor (the per-message counterfactual), then K2
@@ -153,13 +155,14 @@ class FusedGradientSync:
                 mode = "ce"
             else:
                 mode = "sharded" if (flat_params is not None and self.local_workers == 1) else "bucket"
-        if mode not in ("bucket", "direct", "sharded", "p2p", "ce", "adaptive", "unfused", "nvls"):
+        if mode not in ("bucket", "direct", "sharded", "p2p", "p2p_gather", "ce", "adaptive", "unfused", "nvls"):
             raise ConfigError(f"unknown sync mode {mode!r}")
         if mode == "direct" and self.workers != 1:
             raise ConfigError("direct mode has no bucket and needs exactly one worker")
         if mode == "unfused" and self.local_workers != 1:
             raise ConfigError("unfused mode all-reduces each gradient tensor in place: one worker per rank")
-        if mode in ("sharded", "p2p", "ce", "adaptive", "nvls") and (flat_params is None or self.local_workers != 1 or self.ranks < 2):
+        if mode in ("sharded", "p2p", "p2p_gather", "ce", "adaptive", "nvls") and (
+                flat_params is None or self.local_workers != 1 or self.ranks < 2):
             raise ConfigError("sharded mode needs flat parameters (flatten_parameters), world > 1 "
                               "and one worker per rank")
         if (self.ranks > 1 and mode in ("bucket", "sharded", "unfused")
@@ -167,7 +170,7 @@ class FusedGradientSync:
             raise ConfigError(f"{mode} sync needs an NCCL communicator at world > 1")
         self.mode = mode
         self.flat = flat_params
-        sharded = mode in ("sharded", "p2p", "ce", "adaptive", "nvls")
+        sharded = mode in ("sharded", "p2p", "p2p_gather", "ce", "adaptive", "nvls")
         multiple = align * self.ranks if sharded else None
         self.layout = BucketLayout.build([p.numel() for p in self.params], align, multiple=multiple)
         if sharded:
@@ -195,15 +198,16 @@ class FusedGradientSync:
                                   "(flatten_parameters(ipc='nvls'))")
             self._bucket_nvls = NvlsBuffer(lay.total, dev, comm.rank, self.ranks)
             self.bucket = self._bucket_nvls.tensor
-        elif mode in ("p2p", "ce", "adaptive"):
+        elif mode in ("p2p", "p2p_gather", "ce", "adaptive"):
             from .p2p import DeviceBuffer, buffer_of
 
             if self.ranks > _lib.CS_MAX_SOURCES:
                 raise ConfigError(f"{mode} sync supports up to {_lib.CS_MAX_SOURCES} ranks")
             if buffer_of(flat_params) is None:
                 raise ConfigError(f"{mode} sync needs IPC-capable flat parameters (flatten_parameters(ipc=True))")
-            self._bucket_buf = DeviceBuffer(lay.total, dev)
-            self.bucket = self._bucket_buf.tensor
+            if mode != "p2p_gather":           # p2p_gather reads the gradients: no bucket
+                self._bucket_buf = DeviceBuffer(lay.total, dev)
+                self.bucket = self._bucket_buf.tensor
         elif mode in ("bucket", "sharded"):
             self.bucket = torch.zeros(self.local_workers * lay.total, dtype=torch.float32, device=dev)
         self.momentum_bufs = None
@@ -243,6 +247,19 @@ class FusedGradientSync:
             self._nvls.nranks = self.ranks
             self._nvls.max_ctas = int(p2p_ctas)
             self.transport = "nvls"
+            self._finish_init(settings)
+            return
+        if mode == "p2p_gather":
+            from .p2p import buffer_of, exchange_peer_addresses
+
+            self._flat_map = exchange_peer_addresses(buffer_of(flat_params), self.rank, self.ranks)
+            self._peer_maps = [self._flat_map]
+            self._barrier = torch.zeros(32, dtype=torch.float32, device=dev)
+            self._init_barrier(barrier)
+            self._gather_ctas = int(p2p_ctas)
+            self._gather = None               # built at the first sync, from its gradient tensors
+            self._gather_keys = []
+            self.transport = "p2p_gather"
             self._finish_init(settings)
             return
         if mode in ("p2p", "ce", "adaptive"):
@@ -338,7 +355,7 @@ class FusedGradientSync:
 
     @property
     def barrier_kind(self) -> str | None:
-        if self.mode not in ("p2p", "ce", "adaptive", "nvls"):
+        if self.mode not in ("p2p", "p2p_gather", "ce", "adaptive", "nvls"):
             return None
         return self._barrier_kind
 
@@ -464,6 +481,9 @@ class FusedGradientSync:
             if timer is not None:
                 timer.end("k2_update")
             return
+        if self.transport == "p2p_gather":
+            self._gather_tail(grads_per_worker[0], stream, snapshot_row, timer)
+            return
         if timer is not None:
             timer.begin("k1_pack")
         self.pack(grads_per_worker, stream)
@@ -554,6 +574,77 @@ class FusedGradientSync:
             with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
                 self.snapshot[snapshot_row].copy_(self.flat)
 
+    def _gather_plan(self, grads: Sequence[torch.Tensor]) -> None:
+        """Pieces of this rank's shard, one per gradient tensor it overlaps, with every rank's
+        gradient addresses (collective: map_peer_tensors), uploaded once; the gradients must keep
+        these addresses for every later sync."""
+        from .p2p import map_peer_tensors
+
+        if len(grads) != len(self.params):
+            raise ValueError(f"expected {len(self.params)} gradients")
+        for i, (g, p) in enumerate(zip(grads, self.params)):
+            if (g is None or g.dtype != torch.float32 or g.shape != p.shape or g.stride() != p.stride()
+                    or not _dense(g) or g.data_ptr() % 16):
+                raise ConfigError(f"p2p_gather: gradient {i} must be a dense fp32 tensor laid out like its "
+                                  "parameter, 16-byte aligned")
+        addrs, self._gather_keys = map_peer_tensors(grads, self.rank, self.ranks, self.flat.device)
+        lay = self.layout
+        s0, s1 = self.rank * self.shard, (self.rank + 1) * self.shard
+        ch = int(_lib.lib.cs_p2p_gather_chunk_elems(self.ranks))
+        flat = self._flat_map.addresses
+        mom = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else 0
+        pieces, chunks = [], []
+        for i, (o, n) in enumerate(zip(lay.offsets, lay.numels)):
+            a, b = max(o, s0), min(o + n, s1)
+            if a >= b:
+                continue
+            row = np.zeros((), dtype=_lib.P2P_DESC)
+            row["src"][:self.ranks] = [addrs[r][i] + 4 * (a - o) for r in range(self.ranks)]
+            row["dst"][:self.ranks] = [flat[r] + 4 * a for r in range(self.ranks)]
+            row["param"] = self.flat.data_ptr() + 4 * a
+            row["momentum_buf"] = mom + 4 * (a - s0) if mom else 0
+            row["numel"] = b - a
+            row["nranks"] = self.ranks
+            chunks.extend((len(pieces), e0) for e0 in range(0, b - a, ch))
+            pieces.append(row)
+        pt = np.array(pieces, dtype=_lib.P2P_DESC)
+        ct = np.zeros(len(chunks), dtype=_lib.GATHER_CHUNK)
+        if chunks:
+            ct["piece"], ct["e0"] = zip(*chunks)
+        _lib.check("cs_p2p_gather_check", _lib.lib.cs_p2p_gather_check(
+            pt.ctypes.data, len(pt), ct.ctypes.data, len(ct), self.ranks, int(bool(mom))))
+        dev = self.flat.device
+        self._gather = (torch.from_numpy(pt.view(np.uint8).copy()).to(dev),
+                        torch.from_numpy(ct.view(np.uint8).copy()).to(dev), len(ct))
+        self._gather_ptrs = [g.data_ptr() for g in grads]
+
+    def _gather_tail(self, grads: Sequence[torch.Tensor], stream: int, snapshot_row: int | None, timer) -> None:
+        """barrier -> one NVLink kernel over every rank's gradient tensors (rank-order reduce, /W,
+        SGD, broadcast writes of the new shard) -> barrier.  No K1, no bucket."""
+        if self._gather is None:
+            self._gather_plan(grads)
+        elif [g.data_ptr() for g in grads] != self._gather_ptrs:
+            raise ConfigError("p2p_gather: the gradients moved since the first sync (the transport "
+                              "needs a CUDA-graphed backward with static gradient buffers)")
+        self._rank_barrier(stream, 0)                  # every rank's gradients are complete
+        if timer is not None:
+            timer.begin("k2_p2p_gather")
+        self._hyper.first_step = int(self.first_step)
+        pieces, chunks, n = self._gather
+        _lib.check("cs_p2p_gather_reduce_sgd_bcast", _lib.lib.cs_p2p_gather_reduce_sgd_bcast(
+            pieces.data_ptr(), chunks.data_ptr(), n, self.ranks, self._gather_ctas,
+            ctypes.byref(self._hyper), stream))
+        self.first_step = False
+        self.kernel_launches += 1
+        if timer is not None:
+            timer.end("k2_p2p_gather")
+        self._rank_barrier(stream, 1)                  # every peer read my gradients, wrote my shard
+        if snapshot_row is not None:
+            if self.snapshot is None:
+                raise ConfigError("no snapshot buffer (snapshot_rows=0)")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.snapshot[snapshot_row].copy_(self.flat)
+
     def _nvls_tail(self, stream: int, snapshot_row: int | None, timer) -> None:
         """barrier -> one kernel: switch-reduced shard (multimem.ld_reduce), /W, SGD, switch-broadcast
         new shard (multimem.st) -> barrier."""
@@ -624,6 +715,11 @@ class FusedGradientSync:
         for m in self._peer_maps:
             m.close()
         self._peer_maps = []
+        if getattr(self, "_gather_keys", None):
+            from .p2p import unmap_peer_tensors
+
+            unmap_peer_tensors(self._gather_keys)
+            self._gather_keys = []
         bucket = getattr(self, "_bucket_buf", None) or getattr(self, "_bucket_nvls", None)
         if bucket is None and self._flags is None:
             return
@@ -643,6 +739,8 @@ class FusedGradientSync:
 
     # -- algorithmic bytes per launch ---------------------------
     def k1_bytes(self) -> int:
+        if self.mode == "p2p_gather":
+            return 0                       # no pack: the kernel reads the gradients in place
         return 2 * self.local_workers * self.layout.payload_bytes
 
     def k2_bytes(self, transport: str | None = None) -> int:
@@ -651,7 +749,7 @@ class FusedGradientSync:
             # local HBM: read p (+ momentum r/w); the reduced shard arrives from and the new shard
             # leaves through the switch
             return (1 + (2 if self.settings.momentum else 0)) * self.shard * 4
-        if transport == "p2p":
+        if transport in ("p2p", "p2p_gather"):
             # W source shards + p read + W destination shards (+ momentum read/write)
             return (2 * self.ranks + 1 + (2 if self.settings.momentum else 0)) * self.shard * 4
         if self.mode == "sharded":

@@ -17,7 +17,8 @@ import torch
 
 from . import _lib
 
-__all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping", "all_ranks_agree", "FlagArray"]
+__all__ = ["DeviceBuffer", "exchange_peer_addresses", "PeerMapping", "all_ranks_agree", "FlagArray",
+           "map_peer_tensors", "unmap_peer_tensors"]
 
 # ptr -> DeviceBuffer, weakly: a buffer lives exactly as long as a tensor viewing it (torch keeps
 # the __cuda_array_interface__ provider alive as the storage's owner), then cudaFree runs
@@ -126,6 +127,86 @@ def exchange_peer_addresses(buf: DeviceBuffer, rank: int, world: int) -> PeerMap
         mapping.close()
         raise ConfigError("p2p peer mapping failed on some rank" + (f" ({error})" if error else ""))
     return mapping
+
+
+# (peer rank, peer allocation base) -> [address here, users]: one mapping per peer allocation and
+# process however many syncs read tensors inside it (CUDA maps an allocation once per context)
+_peer_allocs: dict[tuple[int, int], list] = {}
+
+
+def map_peer_tensors(tensors, rank: int, world: int, device) -> tuple[list[list[int]], list[tuple[int, int]]]:
+    """Addresses of every rank's `tensors` (same count and order on every rank) as seen from this
+    process -- the p2p_gather transport reads the gradient tensors of the peers in place.
+
+    Each tensor's IPC handle is its allocation's (cs_ipc_base_of: a caching-allocator segment) plus
+    its offset in it.  Collective over torch.distributed; a failure anywhere is agreed on, every rank
+    releases what it mapped and raises ConfigError.  Returns (addresses[rank][i], keys to release
+    with unmap_peer_tensors)."""
+    import torch.distributed as dist
+
+    from .errors import ConfigError
+
+    bases: dict[int, int] = {}
+    mine, error = [], ""
+    for t in tensors:
+        base, size = ctypes.c_void_p(), ctypes.c_size_t()
+        if _lib.lib.cs_ipc_base_of(t.data_ptr(), ctypes.byref(base), ctypes.byref(size)):
+            error = f"rank {rank}: {_lib.lib.cs_last_error().decode()}"
+            break
+        b = int(base.value)
+        if b not in bases:
+            bases[b] = len(bases)
+        mine.append((bases[b], t.data_ptr() - b))
+    handles = []
+    for b in bases:
+        out = (ctypes.c_uint8 * _lib.CS_IPC_HANDLE_BYTES)()
+        if not error and _lib.lib.cs_ipc_get_handle(b, out):
+            error = f"rank {rank}: {_lib.lib.cs_last_error().decode()}"
+        handles.append((b, bytes(out)))
+    if not all_ranks_agree(not error):
+        raise ConfigError("gradient IPC export failed on some rank" + (f" ({error})" if error else ""))
+    everyone: list = [None] * world
+    dist.all_gather_object(everyone, (handles, mine))
+    keys, addrs = [], []
+    with torch.cuda.device(device):
+        for r, (hs, items) in enumerate(everyone):
+            if r == rank:
+                addrs.append([int(t.data_ptr()) for t in tensors])
+                continue
+            mapped = []
+            for b, h in hs:
+                key = (r, b)
+                ent = _peer_allocs.get(key)
+                if ent is None and not error:
+                    hb = (ctypes.c_uint8 * _lib.CS_IPC_HANDLE_BYTES).from_buffer_copy(h)
+                    p = ctypes.c_void_p()
+                    if _lib.lib.cs_ipc_open_handle(hb, ctypes.byref(p)):
+                        error = f"rank {rank}: cannot map rank {r}: {_lib.lib.cs_last_error().decode()}"
+                        mapped.append(0)
+                        continue
+                    ent = _peer_allocs[key] = [int(p.value), 0]
+                if ent is None:
+                    mapped.append(0)
+                    continue
+                ent[1] += 1
+                keys.append(key)
+                mapped.append(ent[0])
+            addrs.append([mapped[i] + off for i, off in items])
+    if not all_ranks_agree(not error):
+        unmap_peer_tensors(keys)
+        raise ConfigError("gradient peer mapping failed on some rank" + (f" ({error})" if error else ""))
+    return addrs, keys
+
+
+def unmap_peer_tensors(keys) -> None:
+    for key in keys:
+        ent = _peer_allocs.get(key)
+        if ent is None:
+            continue
+        ent[1] -= 1
+        if ent[1] == 0:
+            del _peer_allocs[key]
+            _lib.check("cs_ipc_close_handle", _lib.lib.cs_ipc_close_handle(ent[0]))
 
 
 def all_ranks_agree(ok: bool) -> bool:

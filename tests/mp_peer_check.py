@@ -24,6 +24,9 @@ CASE resnet   two ResNet-50 apps (bf16 autocast, CUDA graphs, momentum 0.9, weig
               through ce for 3 iterations: every rank's update equals torch.optim.SGD
               (foreach=False) on the CPU applied to the rank-order average of the W ranks'
               captured gradients, bit for bit.
+CASE gather   the same with the K1-free p2p_gather transport (the kernel reads every rank's
+              graph-static gradient tensors in place): bitwise vs torch.optim.SGD, one kernel
+              launch per sync.
 """
 
 import json
@@ -246,13 +249,23 @@ def case_graph(rank, world, dev, comm, res):
 def case_resnet(rank, world, dev, comm, res):
     """Config-2 update path at W ranks: 161 tensors, channels_last conv weights, CUDA-graph static
     gradients, IPC flat parameters, copy-engine transport; bitwise vs torch.optim.SGD."""
+    _resnet_update_check(rank, world, dev, comm, res, "ce")
+
+
+def case_gather(rank, world, dev, comm, res):
+    """The K1-free p2p_gather transport (every rank's graph-static gradient tensors read in place
+    over NVLink / IPC) on the same check: bitwise vs torch.optim.SGD, one kernel per sync."""
+    _resnet_update_check(rank, world, dev, comm, res, "p2p_gather")
+
+
+def _resnet_update_check(rank, world, dev, comm, res, mode):
     from paper_2103_07974_b200.apps import DEFAULT_IMAGE_SGD, resnet50_app
 
     steps, batch = 3, 32
     apps = [resnet50_app(f"r{j}", batch, steps, dev, seed=1000 * j, data_seed=1000 * j + rank,
                          graphed=True, flat="ipc",
                          fast_bn=True) for j in range(2)]
-    s = CrossoverScheduler(Policy.CROSSOVER, comm=comm, sync_mode="ce")
+    s = CrossoverScheduler(Policy.CROSSOVER, comm=comm, sync_mode=mode)
     for a in apps:
         s.register(a)
     before = {a.job_id: [p.detach().cpu().clone() for p in a.params] for a in apps}
@@ -290,9 +303,14 @@ def case_resnet(rank, world, dev, comm, res):
         ok = ok and mism == 0
         before[st.job_id] = after
     s.drain()
+    launches = [st.sync.kernel_launches for st in s.states]
+    modes = {st.sync.mode for st in s.states}
     s.close()
-    res["checks"].append({"name": f"resnet50_ce_w{world}_bitwise_eq_torch_sgd", "ok": ok,
+    res["checks"].append({"name": f"resnet50_{mode}_w{world}_bitwise_eq_torch_sgd", "ok": ok and modes == {mode},
                           "mismatched_elements": worst, "tensors": len(apps[0].params)})
+    if mode == "p2p_gather":   # one kernel per sync: no K1 pack
+        res["checks"].append({"name": "p2p_gather_one_kernel_per_sync", "ok": launches == [steps, steps],
+                              "launches": launches})
 
 
 def main():
@@ -307,7 +325,7 @@ def main():
     comm = PeerGroup(rank, world)
     res = {"world": world, "case": case, "ok": True, "checks": []}
     {"parity": case_parity, "fail": case_fail, "resnet": case_resnet,
-     "graph": case_graph}[case](rank, world, dev, comm, res)
+     "graph": case_graph, "gather": case_gather}[case](rank, world, dev, comm, res)
     res["ok"] = all(c["ok"] for c in res["checks"])
     oks = [None] * world
     dist.all_gather_object(oks, res["ok"])

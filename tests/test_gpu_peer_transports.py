@@ -62,3 +62,11 @@ def test_rotation_graph_over_peer_transports(tmp_path, world):
     """graphs.RotationGraph with ce / p2p: barriers, CE pulls and the P2P kernel captured into one
     graph per rotation -- bitwise equal to eager, ranks identical."""
     _launch(tmp_path, world, "graph", 29750 + world)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_gather_resnet50_update_parity(tmp_path, world):
+    """The K1-free p2p_gather transport: one kernel per sync reads every rank's CUDA-graph static
+    gradient tensors in place (161 ResNet-50 tensors cut at the W shard boundaries); bitwise
+    torch.optim.SGD(foreach=False) on the rank-order average, 3 iterations x 2 apps."""
+    _launch(tmp_path, world, "gather", 29760 + world)

@@ -62,9 +62,11 @@ def measure(h, base, args, policy_runs=("crossover", "sequential")):
         bench.calibrate_transport(h, base, args.sync_mode if h.world > 1 else "auto")
         out["grid_cap"] = bench.SYNC_CTAS
     cross = timed_run(h, base, Policy.CROSSOVER, args.warmup, args.steps, sync_mode=args.sync_mode)
-    p2p_cap = getattr(cross["sched"].states[0].sync, "_p2p", None)
+    sync0 = cross["sched"].states[0].sync
+    cap = (sync0._p2p.max_ctas if getattr(sync0, "_p2p", None) is not None
+           else getattr(sync0, "_gather_ctas", None))
     seq = timed_run(h, base, Policy.SEQUENTIAL, args.warmup, args.steps, sync_mode=args.sync_mode,
-                    p2p_ctas=p2p_cap.max_ctas if p2p_cap is not None else None)
+                    p2p_ctas=cap)
     order = [a.job_id for a in base]
     rx, rs = cross["ms"] / args.steps, seq["ms"] / args.steps
     comp, comm = phase_medians(seq["timed_spans"], order)
