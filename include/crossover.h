@@ -173,25 +173,18 @@ CS_API int cs_p2p_reduce_sgd_bcast(const cs_p2p_desc* desc, const cs_sgd_hyper* 
                                    void* stream);
 
 /* The same update without K1 ("p2p_gather"): every rank's GRADIENT TENSORS are read in place over
- * NVLink (no bucket, no pack).  This rank's shard of the bucket layout is cut into pieces, one per
- * gradient tensor it overlaps; piece i is a cs_p2p_desc whose src[r] points into rank r's gradient
- * tensor (mapped in this process), dst[r] / param / momentum_buf at the piece's offset of the flat
- * parameters / momentum shard, numel its length.  Work items are chunks (piece, e0) with e0 a
- * multiple of cs_p2p_gather_chunk_elems(nranks), one per chunk of every piece.  Arithmetic and
- * sum order are cs_p2p_reduce_sgd_bcast's, so the result is bit-identical to it (and to K1 + p2p).
- * Gradients must stay at these addresses while syncs run (CUDA-graphed backward passes).
- * cs_p2p_gather_check validates a host copy of the tables; the launch takes device copies. */
-typedef struct cs_gather_chunk {
-  int32_t piece;
-  int32_t pad_;
-  int64_t e0;
-} cs_gather_chunk;
+ * NVLink (no bucket, no pack).  This rank's shard of the bucket layout is cut into chunks that
+ * never cross a gradient tensor, at most cs_p2p_gather_chunk_elems(nranks) elements each; chunk i
+ * is a cs_p2p_desc whose src[r] points at the chunk inside rank r's gradient tensor (mapped in
+ * this process), dst[r] / param / momentum_buf at the chunk's place in the flat parameters /
+ * momentum shard, numel its length.  Arithmetic and sum order are cs_p2p_reduce_sgd_bcast's, so
+ * the result is bit-identical to it (and to K1 + p2p).  Gradients must stay at these addresses
+ * while syncs run (CUDA-graphed backward passes).  cs_p2p_gather_check validates a host copy of
+ * the table; the launch takes a device copy (16-byte aligned). */
 CS_API int64_t cs_p2p_gather_chunk_elems(int nranks);
-CS_API int cs_p2p_gather_check(const cs_p2p_desc* pieces, int64_t npieces, const cs_gather_chunk* chunks,
-                               int64_t nchunks, int nranks, int momentum);
-CS_API int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* pieces_dev, const cs_gather_chunk* chunks_dev,
-                                          int64_t nchunks, int nranks, int max_ctas,
-                                          const cs_sgd_hyper* hyper, void* stream);
+CS_API int cs_p2p_gather_check(const cs_p2p_desc* chunks, int64_t nchunks, int nranks, int momentum);
+CS_API int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* chunks_dev, int64_t nchunks, int nranks,
+                                          int max_ctas, const cs_sgd_hyper* hyper, void* stream);
 
 /* Collective-fused update through NVSwitch multicast (NVLS): same contract as
  * cs_p2p_reduce_sgd_bcast, but the W-rank sum is a multimem.ld_reduce on the multicast mapping of

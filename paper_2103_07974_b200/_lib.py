@@ -26,11 +26,10 @@ CS_ROUND_TORCH = 1
 PACK_DESC = np.dtype([("src", "<u8"), ("dst", "<u8"), ("numel", "<i8")])
 UPDATE_DESC = np.dtype([("param", "<u8"), ("momentum_buf", "<u8"), ("grad_offset", "<u8"),
                         ("snap_offset", "<u8"), ("numel", "<i8")])
-# cs_p2p_desc as a table row (the p2p_gather pieces) and cs_gather_chunk
+# cs_p2p_desc as a table row (the p2p_gather chunk table)
 P2P_DESC = np.dtype([("src", "<u8", (CS_MAX_SOURCES,)), ("dst", "<u8", (CS_MAX_SOURCES,)),
                      ("param", "<u8"), ("momentum_buf", "<u8"), ("numel", "<i8"),
                      ("nranks", "<i4"), ("max_ctas", "<i4")])
-GATHER_CHUNK = np.dtype([("piece", "<i4"), ("pad_", "<i4"), ("e0", "<i8")])
 
 
 class SgdHyper(ctypes.Structure):
@@ -88,10 +87,9 @@ EXPORTS = {
     "cs_p2p_reduce_sgd_bcast": ([ctypes.POINTER(P2PDesc), ctypes.POINTER(SgdHyper), ctypes.c_void_p],
                                 ctypes.c_int),
     "cs_p2p_gather_chunk_elems": ([ctypes.c_int], ctypes.c_int64),
-    "cs_p2p_gather_check": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
-                             ctypes.c_int], ctypes.c_int),
-    "cs_p2p_gather_reduce_sgd_bcast": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
-                                        ctypes.c_int, ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),
+    "cs_p2p_gather_check": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "cs_p2p_gather_reduce_sgd_bcast": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(SgdHyper), ctypes.c_void_p], ctypes.c_int),
     "cs_nvls_reduce_sgd_bcast": ([ctypes.POINTER(NvlsDesc), ctypes.POINTER(SgdHyper), ctypes.c_void_p],
                                  ctypes.c_int),
     "cs_nvls_supported": ([ctypes.c_int], ctypes.c_int),

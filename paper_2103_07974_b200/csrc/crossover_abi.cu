@@ -368,38 +368,33 @@ int64_t cs_p2p_gather_chunk_elems(int nranks) {
   return p2p_gather_chunk_elems(nranks);
 }
 
-int cs_p2p_gather_check(const cs_p2p_desc* pieces, int64_t npieces, const cs_gather_chunk* chunks,
-                        int64_t nchunks, int nranks, int momentum) {
-  if ((npieces > 0 && pieces == nullptr) || (nchunks > 0 && chunks == nullptr) || npieces < 0 || nchunks < 0)
-    return set_error(CS_ERR_ARG, "cs_p2p_gather_check: bad table");
+int cs_p2p_gather_check(const cs_p2p_desc* chunks, int64_t nchunks, int nranks, int momentum) {
+  if ((nchunks > 0 && chunks == nullptr) || nchunks < 0) return set_error(CS_ERR_ARG, "cs_p2p_gather_check: bad table");
   if (nranks < 1 || nranks > CS_MAX_SOURCES)
     return set_error(CS_ERR_ARG, "cs_p2p_gather_check: nranks=%d outside [1, %d]", nranks, CS_MAX_SOURCES);
   const int64_t ch = p2p_gather_chunk_elems(nranks);
-  for (int64_t i = 0; i < npieces; ++i) {
-    const cs_p2p_desc& d = pieces[i];
-    if (d.nranks != nranks || d.numel <= 0 || d.param == nullptr || (momentum && d.momentum_buf == nullptr))
-      return set_error(CS_ERR_ARG, "cs_p2p_gather_check: piece %lld malformed", (long long)i);
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const cs_p2p_desc& d = chunks[i];
+    if (d.nranks != nranks || d.numel <= 0 || d.numel > ch || d.param == nullptr ||
+        (momentum && d.momentum_buf == nullptr))
+      return set_error(CS_ERR_ARG, "cs_p2p_gather_check: chunk %lld malformed", (long long)i);
     uintptr_t al = (uintptr_t)d.param | (uintptr_t)d.momentum_buf;
     for (int r = 0; r < nranks; ++r) {
       if (d.src[r] == 0 || d.dst[r] == 0)
-        return set_error(CS_ERR_ARG, "cs_p2p_gather_check: piece %lld: NULL address of rank %d", (long long)i, r);
+        return set_error(CS_ERR_ARG, "cs_p2p_gather_check: chunk %lld: NULL address of rank %d", (long long)i, r);
       al |= (uintptr_t)d.src[r] | (uintptr_t)d.dst[r];
     }
-    if (al & 15u) return set_error(CS_ERR_ARG, "cs_p2p_gather_check: piece %lld not 16-byte aligned", (long long)i);
-  }
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const cs_gather_chunk& k = chunks[c];
-    if (k.piece < 0 || k.piece >= npieces || k.e0 < 0 || k.e0 >= pieces[k.piece].numel || k.e0 % ch)
-      return set_error(CS_ERR_ARG, "cs_p2p_gather_check: chunk %lld out of range", (long long)c);
+    if (al & 15u) return set_error(CS_ERR_ARG, "cs_p2p_gather_check: chunk %lld not 16-byte aligned", (long long)i);
   }
   return 0;
 }
 
-int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* pieces_dev, const cs_gather_chunk* chunks_dev,
-                                   int64_t nchunks, int nranks, int max_ctas, const cs_sgd_hyper* h,
-                                   void* stream) {
-  if (h == nullptr || (nchunks > 0 && (pieces_dev == nullptr || chunks_dev == nullptr)) || nchunks < 0)
+int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* chunks_dev, int64_t nchunks, int nranks, int max_ctas,
+                                   const cs_sgd_hyper* h, void* stream) {
+  if (h == nullptr || (nchunks > 0 && chunks_dev == nullptr) || nchunks < 0)
     return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: NULL argument");
+  if (((uintptr_t)chunks_dev & 15u) != 0)
+    return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: chunk table not 16-byte aligned");
   if (nranks < 1 || nranks > CS_MAX_SOURCES || max_ctas < 0)
     return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: bad nranks / max_ctas");
   if (h->divisor != nranks)
@@ -407,7 +402,7 @@ int cs_p2p_gather_reduce_sgd_bcast(const cs_p2p_desc* pieces_dev, const cs_gathe
   if (!(h->lr > 0.0f)) return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: learning rate must be > 0");
   if (h->rounding == CS_ROUND_REFERENCE && (h->momentum != 0.0f || h->weight_decay != 0.0f))
     return set_error(CS_ERR_ARG, "cs_p2p_gather_reduce_sgd_bcast: reference rounding has no momentum / weight decay");
-  return cuda_status(launch_p2p_gather(pieces_dev, chunks_dev, nchunks, nranks, max_ctas, *h, (cudaStream_t)stream),
+  return cuda_status(launch_p2p_gather(chunks_dev, nchunks, nranks, max_ctas, *h, (cudaStream_t)stream),
                      "cs_p2p_gather_reduce_sgd_bcast launch");
 }
 

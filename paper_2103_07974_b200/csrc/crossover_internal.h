@@ -58,8 +58,8 @@ extern int g_tune_bn_no_pdl;
 extern int g_tune_bn_ctas_per_sm;
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s);
 int64_t p2p_gather_chunk_elems(int nranks);
-cudaError_t launch_p2p_gather(const cs_p2p_desc* pieces, const cs_gather_chunk* chunks, int64_t nchunks,
-                              int nranks, int max_ctas, const cs_sgd_hyper& h, cudaStream_t s);
+cudaError_t launch_p2p_gather(const cs_p2p_desc* chunks, int64_t nchunks, int nranks, int max_ctas,
+                              const cs_sgd_hyper& h, cudaStream_t s);
 int bn_row_blocks(int64_t M, int C);
 cudaError_t launch_im2col_nhwc(const void* x, void* p, const int* shape, cudaStream_t stream);
 size_t bn_workspace_bytes(int64_t M, int C);

@@ -147,28 +147,48 @@ static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream
 }
 
 // ---------------------------------------------------------------------------------------------
-// K1-free variant: the pieces of this rank's shard read every rank's gradient tensors in place.
-// Each work item is one chunk of one piece; its descriptor is staged in shared memory once per
-// chunk (the per-element code is p2p_chunk's, so the arithmetic is bit-identical).
+// K1-free variant: the chunks of this rank's shard read every rank's gradient tensors in place.
+// One self-contained descriptor per chunk (pointers already at the chunk, numel <= one chunk);
+// the next chunk's descriptor is fetched into shared memory with cp.async while the current one
+// is processed, so the table lookup adds no latency to the peer loads.  The per-element code is
+// p2p_chunk's, so the arithmetic is bit-identical to the bucket kernel.
 // ---------------------------------------------------------------------------------------------
+constexpr int kDescVecs = (int)(sizeof(cs_p2p_desc) / 16);
+static_assert(sizeof(cs_p2p_desc) % 16 == 0, "cs_p2p_desc must be a whole number of 16-byte vectors");
+
+__device__ __forceinline__ void desc_prefetch(cs_p2p_desc* dst, const cs_p2p_desc* src) {
+  if (threadIdx.x < kDescVecs) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char*>(dst) + 16 * threadIdx.x);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s),
+                 "l"(reinterpret_cast<const char*>(src) + 16 * threadIdx.x)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <bool kMom, int U, int MAXW>
 __global__ void __launch_bounds__(kThreads)
-p2p_gather_kernel(const cs_p2p_desc* __restrict__ pieces, const cs_gather_chunk* __restrict__ chunks,
-                  int64_t nchunks, const __grid_constant__ cs_sgd_hyper h) {
-  __shared__ cs_p2p_desc sd;
+p2p_gather_kernel(const cs_p2p_desc* __restrict__ chunks, int64_t nchunks, const __grid_constant__ cs_sgd_hyper h) {
+  __shared__ __align__(16) cs_p2p_desc sd[2];
   const Rule r = make_rule(h, kMom);
-  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const cs_gather_chunk ch = chunks[c];
-    if (threadIdx.x == 0) sd = pieces[ch.piece];
+  int64_t c = blockIdx.x;
+  if (c < nchunks) desc_prefetch(&sd[0], chunks + c);
+  for (int buf = 0; c < nchunks; c += gridDim.x, buf ^= 1) {
+    const int64_t next = c + gridDim.x;
+    if (next < nchunks) desc_prefetch(&sd[buf ^ 1], chunks + next);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // this chunk's descriptor landed
     __syncthreads();
-    p2p_chunk<kMom, U, MAXW>(sd, r, ch.e0);
-    __syncthreads();          // sd is rewritten for the next chunk
+    p2p_chunk<kMom, U, MAXW>(sd[buf], r, 0);
+    __syncthreads();          // sd[buf] is the prefetch target of the next iteration but one
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __threadfence_system();
 }
 
-template <int U>
-static int64_t gather_grid(int64_t nchunks, int max_ctas) {
+template <int U, int MAXW>
+static void launch_gather_u(const cs_p2p_desc* chunks, int64_t nchunks, int max_ctas, const cs_sgd_hyper& h,
+                            cudaStream_t s) {
   int cap = max_ctas > 0 ? max_ctas : g_tune_p2p_ctas;
   if (cap <= 0) {
     int dev = 0, sms = 148;
@@ -176,15 +196,9 @@ static int64_t gather_grid(int64_t nchunks, int max_ctas) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cap = 2 * sms;
   }
-  return nchunks < cap ? nchunks : cap;
-}
-
-template <int U, int MAXW>
-static void launch_gather_u(const cs_p2p_desc* pieces, const cs_gather_chunk* chunks, int64_t nchunks,
-                            int max_ctas, const cs_sgd_hyper& h, cudaStream_t s) {
-  const unsigned grid = (unsigned)gather_grid<U>(nchunks, max_ctas);
-  if (h.momentum != 0.0f) p2p_gather_kernel<true, U, MAXW><<<grid, kThreads, 0, s>>>(pieces, chunks, nchunks, h);
-  else p2p_gather_kernel<false, U, MAXW><<<grid, kThreads, 0, s>>>(pieces, chunks, nchunks, h);
+  const unsigned grid = (unsigned)(nchunks < cap ? nchunks : cap);
+  if (h.momentum != 0.0f) p2p_gather_kernel<true, U, MAXW><<<grid, kThreads, 0, s>>>(chunks, nchunks, h);
+  else p2p_gather_kernel<false, U, MAXW><<<grid, kThreads, 0, s>>>(chunks, nchunks, h);
 }
 
 int64_t p2p_gather_chunk_elems(int nranks) {
@@ -193,12 +207,12 @@ int64_t p2p_gather_chunk_elems(int nranks) {
   return p2p_chunk_elems<1>();
 }
 
-cudaError_t launch_p2p_gather(const cs_p2p_desc* pieces, const cs_gather_chunk* chunks, int64_t nchunks,
-                              int nranks, int max_ctas, const cs_sgd_hyper& h, cudaStream_t s) {
+cudaError_t launch_p2p_gather(const cs_p2p_desc* chunks, int64_t nchunks, int nranks, int max_ctas,
+                              const cs_sgd_hyper& h, cudaStream_t s) {
   if (nchunks == 0) return cudaSuccess;
-  if (nranks <= 2) launch_gather_u<4, 2>(pieces, chunks, nchunks, max_ctas, h, s);
-  else if (nranks <= 4) launch_gather_u<2, 4>(pieces, chunks, nchunks, max_ctas, h, s);
-  else launch_gather_u<1, CS_MAX_SOURCES>(pieces, chunks, nchunks, max_ctas, h, s);
+  if (nranks <= 2) launch_gather_u<4, 2>(chunks, nchunks, max_ctas, h, s);
+  else if (nranks <= 4) launch_gather_u<2, 4>(chunks, nchunks, max_ctas, h, s);
+  else launch_gather_u<1, CS_MAX_SOURCES>(chunks, nchunks, max_ctas, h, s);
   return cudaGetLastError();
 }
 

@@ -575,7 +575,7 @@ class FusedGradientSync:
                 self.snapshot[snapshot_row].copy_(self.flat)
 
     def _gather_plan(self, grads: Sequence[torch.Tensor]) -> None:
-        """Pieces of this rank's shard, one per gradient tensor it overlaps, with every rank's
+        """Chunks of this rank's shard -- none crossing a gradient tensor -- with every rank's
         gradient addresses (collective: map_peer_tensors), uploaded once; the gradients must keep
         these addresses for every later sync."""
         from .p2p import map_peer_tensors
@@ -593,29 +593,22 @@ class FusedGradientSync:
         ch = int(_lib.lib.cs_p2p_gather_chunk_elems(self.ranks))
         flat = self._flat_map.addresses
         mom = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else 0
-        pieces, chunks = [], []
+        rows = []
         for i, (o, n) in enumerate(zip(lay.offsets, lay.numels)):
-            a, b = max(o, s0), min(o + n, s1)
-            if a >= b:
-                continue
-            row = np.zeros((), dtype=_lib.P2P_DESC)
-            row["src"][:self.ranks] = [addrs[r][i] + 4 * (a - o) for r in range(self.ranks)]
-            row["dst"][:self.ranks] = [flat[r] + 4 * a for r in range(self.ranks)]
-            row["param"] = self.flat.data_ptr() + 4 * a
-            row["momentum_buf"] = mom + 4 * (a - s0) if mom else 0
-            row["numel"] = b - a
-            row["nranks"] = self.ranks
-            chunks.extend((len(pieces), e0) for e0 in range(0, b - a, ch))
-            pieces.append(row)
-        pt = np.array(pieces, dtype=_lib.P2P_DESC)
-        ct = np.zeros(len(chunks), dtype=_lib.GATHER_CHUNK)
-        if chunks:
-            ct["piece"], ct["e0"] = zip(*chunks)
+            for a in range(max(o, s0), min(o + n, s1), ch):
+                b = min(a + ch, o + n, s1)
+                row = np.zeros((), dtype=_lib.P2P_DESC)
+                row["src"][:self.ranks] = [addrs[r][i] + 4 * (a - o) for r in range(self.ranks)]
+                row["dst"][:self.ranks] = [flat[r] + 4 * a for r in range(self.ranks)]
+                row["param"] = self.flat.data_ptr() + 4 * a
+                row["momentum_buf"] = mom + 4 * (a - s0) if mom else 0
+                row["numel"] = b - a
+                row["nranks"] = self.ranks
+                rows.append(row)
+        table = np.array(rows, dtype=_lib.P2P_DESC)
         _lib.check("cs_p2p_gather_check", _lib.lib.cs_p2p_gather_check(
-            pt.ctypes.data, len(pt), ct.ctypes.data, len(ct), self.ranks, int(bool(mom))))
-        dev = self.flat.device
-        self._gather = (torch.from_numpy(pt.view(np.uint8).copy()).to(dev),
-                        torch.from_numpy(ct.view(np.uint8).copy()).to(dev), len(ct))
+            table.ctypes.data, len(table), self.ranks, int(bool(mom))))
+        self._gather = (torch.from_numpy(table.view(np.uint8).copy()).to(self.flat.device), len(table))
         self._gather_ptrs = [g.data_ptr() for g in grads]
 
     def _gather_tail(self, grads: Sequence[torch.Tensor], stream: int, snapshot_row: int | None, timer) -> None:
@@ -630,10 +623,9 @@ class FusedGradientSync:
         if timer is not None:
             timer.begin("k2_p2p_gather")
         self._hyper.first_step = int(self.first_step)
-        pieces, chunks, n = self._gather
+        table, n = self._gather
         _lib.check("cs_p2p_gather_reduce_sgd_bcast", _lib.lib.cs_p2p_gather_reduce_sgd_bcast(
-            pieces.data_ptr(), chunks.data_ptr(), n, self.ranks, self._gather_ctas,
-            ctypes.byref(self._hyper), stream))
+            table.data_ptr(), n, self.ranks, self._gather_ctas, ctypes.byref(self._hyper), stream))
         self.first_step = False
         self.kernel_launches += 1
         if timer is not None:

@@ -50,41 +50,37 @@ def test_struct_layouts():
     assert _lib.UPDATE_DESC.itemsize == 40
     assert ctypes.sizeof(_lib.SgdHyper) == 32
     assert _lib.P2P_DESC.itemsize == ctypes.sizeof(_lib.P2PDesc)
-    assert _lib.GATHER_CHUNK.itemsize == 16
     assert _lib.lib.cs_abi_version() == 3
 
 
 def test_gather_table_validation_without_gpu():
-    """cs_p2p_gather_check validates the p2p_gather piece / chunk tables on the host."""
+    """cs_p2p_gather_check validates the p2p_gather chunk table on the host."""
     from paper_2103_07974_b200 import _lib
 
     assert [_lib.lib.cs_p2p_gather_chunk_elems(w) for w in (2, 4, 8)] == [4096, 2048, 1024]
     assert _lib.lib.cs_p2p_gather_chunk_elems(9) == 0
-    pieces = np.zeros(2, dtype=_lib.P2P_DESC)
-    for i in range(2):
-        pieces[i]["src"][:2] = [0x10000 + 0x10000 * i, 0x20000 + 0x10000 * i]
-        pieces[i]["dst"][:2] = [0x30000 + 0x10000 * i, 0x40000 + 0x10000 * i]
-        pieces[i]["param"] = 0x30000 + 0x10000 * i
-        pieces[i]["numel"] = 5000
-        pieces[i]["nranks"] = 2
-    chunks = np.zeros(4, dtype=_lib.GATHER_CHUNK)
-    chunks["piece"] = [0, 0, 1, 1]
-    chunks["e0"] = [0, 4096, 0, 4096]
+    t = np.zeros(3, dtype=_lib.P2P_DESC)
+    for i in range(3):
+        t[i]["src"][:2] = [0x100000 + 0x10000 * i, 0x200000 + 0x10000 * i]
+        t[i]["dst"][:2] = [0x300000 + 0x10000 * i, 0x400000 + 0x10000 * i]
+        t[i]["param"] = 0x300000 + 0x10000 * i
+        t[i]["numel"] = 4096 if i < 2 else 17
+        t[i]["nranks"] = 2
 
-    def check(p, c, momentum=0):
-        return _lib.lib.cs_p2p_gather_check(p.ctypes.data, len(p), c.ctypes.data, len(c), 2, momentum)
+    def check(tab, momentum=0):
+        return _lib.lib.cs_p2p_gather_check(tab.ctypes.data, len(tab), 2, momentum)
 
-    assert check(pieces, chunks) == 0
-    assert check(pieces, chunks, momentum=1) == _lib.CS_ERR_ARG          # no momentum buffer
-    bad = pieces.copy()
+    assert check(t) == 0
+    assert check(t, momentum=1) == _lib.CS_ERR_ARG                        # no momentum buffer
+    bad = t.copy()
     bad[1]["src"][1] += 4
-    assert check(bad, chunks) == _lib.CS_ERR_ARG and b"aligned" in _lib.lib.cs_last_error()
-    c2 = chunks.copy()
-    c2["e0"][1] = 2048                                                     # not on a chunk boundary
-    assert check(pieces, c2) == _lib.CS_ERR_ARG and b"chunk 1" in _lib.lib.cs_last_error()
-    c3 = chunks.copy()
-    c3["piece"][3] = 2
-    assert check(pieces, c3) == _lib.CS_ERR_ARG
+    assert check(bad) == _lib.CS_ERR_ARG and b"aligned" in _lib.lib.cs_last_error()
+    big = t.copy()
+    big[0]["numel"] = 4097                                                # longer than one chunk
+    assert check(big) == _lib.CS_ERR_ARG and b"chunk 0" in _lib.lib.cs_last_error()
+    w = t.copy()
+    w[2]["nranks"] = 4
+    assert check(w) == _lib.CS_ERR_ARG
 
 
 def test_argument_errors_without_gpu():

@@ -1,0 +1,14 @@
+# p2p_gather (K1-free) vs p2p in the config-2 bench at N = 2 / 4 and in the GEMM band at N = 4.
+# Run under gpurun --gpus 4.
+python -c "import sys; sys.path.insert(0,'.'); from paper_2103_07974_b200 import _build; _build.build(force=True)" || exit 1
+O=gpurun_out/gather2; mkdir -p $O
+for n in 2 4; do
+  R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1"
+  for m in p2p_gather p2p; do
+    timeout 600 $R --master-port 297${n}$([ $m = p2p ] && echo 1 || echo 2) bench.py --gpus $n --sync-mode $m --steps 20 --warmup 5 --no-cpu-baseline > $O/bench_n${n}_$m.json 2> $O/bench_n${n}_$m.err; echo bench n$n $m rc=$?
+  done
+done
+R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
+for m in p2p_gather p2p; do
+  timeout 600 $R --master-port 2978$([ $m = p2p ] && echo 1 || echo 2) tools/band.py --rho 0.2,0.5,1 --compute gemm --sync-mode $m --steps 60 --energy --out $O/band_gemm_${m}_n4.json > $O/band_gemm_${m}_n4.log 2>&1; echo band $m rc=$?
+done
