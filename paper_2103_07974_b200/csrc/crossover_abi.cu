@@ -100,6 +100,7 @@ int cs_tune(const char* key, int value) {
   const std::string k(key);
   if (k == "reg_shape" && value <= 4) g_tune_reg_shape = value;
   else if (k == "p2p_ctas" && value <= 65536) g_tune_p2p_ctas = value;
+  else if (k == "p2p_bulk" && value <= 1) g_tune_p2p_bulk = value;
   else if (k == "sync_ctas" && value <= 65536) g_tune_sync_ctas = value;
   else if (k == "bn_no_pdl" && value <= 1) g_tune_bn_no_pdl = value;
   else if (k == "bn_ctas_per_sm" && value <= 8) g_tune_bn_ctas_per_sm = value;

@@ -54,6 +54,7 @@ int reg_update_chunk();
 extern int g_tune_reg_shape;
 extern int g_tune_sync_ctas;
 extern int g_tune_p2p_ctas;
+extern int g_tune_p2p_bulk;
 extern int g_tune_bn_no_pdl;
 extern int g_tune_bn_ctas_per_sm;
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s);

@@ -147,6 +147,118 @@ static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream
 }
 
 // ---------------------------------------------------------------------------------------------
+// Bulk-copy (TMA) variant for a capped grid.  At the crossover cap (a few dozen CTAs) the register
+// kernel is latency-bound: each thread keeps only W x U 16-byte peer loads in flight.  Here one
+// thread per CTA streams whole tiles -- every source rank's 8 KB slice, the parameter slice and the
+// momentum slice -- into a ring of shared-memory stages with cp.async.bulk (the TMA engine, no
+// registers), completion counted by one mbarrier per stage; all threads reduce a landed stage in
+// rank order, apply the update and store the new slice to every rank while the next stages are in
+// flight.  The arithmetic is p2p_chunk's (same order, same sgd_elem), so the result is bitwise
+// identical.  Selected with cs_tune("p2p_bulk", 1) for launches whose grid cap is set.
+// ---------------------------------------------------------------------------------------------
+int g_tune_p2p_bulk = 0;
+constexpr int kBulkTile = 2048;                 // floats per buffer per stage (8 KB)
+
+template <int MAXW>
+__host__ __device__ constexpr int bulk_stages() { return MAXW <= 2 ? 4 : (MAXW <= 4 ? 3 : 2); }
+template <bool kMom, int MAXW>
+__host__ __device__ constexpr int bulk_buffers() { return MAXW + (kMom ? 2 : 1); }
+template <bool kMom, int MAXW>
+constexpr size_t bulk_smem_bytes() { return (size_t)bulk_stages<MAXW>() * bulk_buffers<kMom, MAXW>() * kBulkTile * 4; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity)
+      : "memory");
+}
+
+template <bool kMom, int MAXW>
+__global__ void __launch_bounds__(kThreads, 1)
+p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
+  constexpr int S = bulk_stages<MAXW>();
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full[S];
+  const Rule r = make_rule(h, kMom);
+  const int W = d.nranks;
+  const int nb = W + (kMom ? 2 : 1);             // buffers of a stage: W sources, p (, m)
+  const int64_t tiles = (d.numel + kBulkTile - 1) / kBulkTile;
+  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t k, int s) {           // thread 0: tile k of this CTA into stage s
+    const int64_t e0 = (blockIdx.x + k * gridDim.x) * kBulkTile;
+    const int64_t rem = d.numel - e0;
+    const uint32_t bytes = (uint32_t)((rem < kBulkTile ? rem : kBulkTile) * 4);
+    const uint32_t bar = smem_u32(&full[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * nb) : "memory");
+    float* st = ring + (size_t)s * nb * kBulkTile;
+    for (int b = 0; b < nb; ++b) {
+      const float* src = b < W ? (const float*)d.src[b] : (b == W ? d.param : d.momentum_buf);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(st + (size_t)b * kBulkTile)), "l"(src + e0), "r"(bytes), "r"(bar)
+                   : "memory");
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < S && k < mine; ++k) issue(k, k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % S);
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((k / S) & 1));
+    const int64_t e0 = (blockIdx.x + k * gridDim.x) * kBulkTile;
+    const int64_t rem = d.numel - e0;
+    const int nvec = (int)((rem < kBulkTile ? rem : kBulkTile) >> 2);
+    const float4* st = reinterpret_cast<const float4*>(ring + (size_t)s * nb * kBulkTile);
+    constexpr int V = kBulkTile / 4;               // float4 per buffer
+    for (int v = threadIdx.x; v < nvec; v += kThreads) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int src = 0; src < MAXW; ++src) {
+        if (src < W) {
+          const float4 g = st[src * V + v];
+          acc.x = __fadd_rn(acc.x, g.x);
+          acc.y = __fadd_rn(acc.y, g.y);
+          acc.z = __fadd_rn(acc.z, g.z);
+          acc.w = __fadd_rn(acc.w, g.w);
+        }
+      }
+      const float4 pv = st[W * V + v];
+      float4 mv = kMom ? st[(W + 1) * V + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 o;
+      o.x = sgd_elem(r, acc.x, pv.x, &mv.x);
+      o.y = sgd_elem(r, acc.y, pv.y, &mv.y);
+      o.z = sgd_elem(r, acc.z, pv.z, &mv.z);
+      o.w = sgd_elem(r, acc.w, pv.w, &mv.w);
+      if (kMom) st4(d.momentum_buf + e0 + 4 * v, mv);
+      for (int dst = 0; dst < W; ++dst) st4((float*)d.dst[dst] + e0 + 4 * v, o);   // fused all-gather
+    }
+    __syncthreads();                               // every thread is done with stage s
+    if (threadIdx.x == 0 && k + S < mine) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+      issue(k + S, s);
+    }
+  }
+  __threadfence_system();
+}
+
+template <int MAXW>
+static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_sgd_hyper& h, int grid, cudaStream_t s) {
+  const bool mom = h.momentum != 0.0f;
+  const size_t smem = mom ? bulk_smem_bytes<true, MAXW>() : bulk_smem_bytes<false, MAXW>();
+  auto* k = mom ? p2p_bulk_kernel<true, MAXW> : p2p_bulk_kernel<false, MAXW>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)grid, kThreads, smem, s>>>(d, h);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 // K1-free variant: the chunks of this rank's shard read every rank's gradient tensors in place.
 // One self-contained descriptor per chunk (pointers already at the chunk, numel <= one chunk);
 // the next chunk's descriptor is fetched into shared memory with cp.async while the current one
@@ -218,6 +330,13 @@ cudaError_t launch_p2p_gather(const cs_p2p_desc* chunks, int64_t nchunks, int nr
 
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
+  if (g_tune_p2p_bulk && d.max_ctas > 0 && d.numel % 4 == 0) {
+    const int64_t tiles = (d.numel + kBulkTile - 1) / kBulkTile;
+    const int grid = (int)(tiles < d.max_ctas ? tiles : d.max_ctas);
+    if (d.nranks <= 2) return launch_bulk<2>(d, h, grid, s);
+    if (d.nranks <= 4) return launch_bulk<4>(d, h, grid, s);
+    return launch_bulk<CS_MAX_SOURCES>(d, h, grid, s);
+  }
   if (d.nranks <= 2) launch_p2p_u<4, 2>(d, h, s);
   else if (d.nranks <= 4) launch_p2p_u<2, 4>(d, h, s);
   else launch_p2p_u<1, CS_MAX_SOURCES>(d, h, s);

@@ -215,12 +215,14 @@ def test_guard_bands_untouched(cuda_device):
     assert torch.isfinite(torch.cat([v for v in views["p"] if v.numel()])).all()
 
 
+@pytest.mark.parametrize("variant", ["registers", "bulk"])
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("momentum", [0.0, 0.9])
-def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum):
+def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum, variant):
     """The fused P2P kernel with every 'peer' address pointing at local memory (one GPU emulates
     W ranks): rank-order sum, /W, SGD, and the broadcast into all W destinations, bit-exact
-    against the same arithmetic (reference rounding) / torch-SGD rounding on the CPU."""
+    against the same arithmetic (reference rounding) / torch-SGD rounding on the CPU.  "bulk" is
+    the capped-grid variant that streams tiles through shared memory with cp.async.bulk (TMA)."""
     import ctypes
 
     from paper_2103_07974_b200 import _lib
@@ -240,8 +242,14 @@ def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum):
     h = _lib.SgdHyper(lr=0.05, momentum=momentum, dampening_complement=1.0, divisor=world,
                       first_step=0, rounding=_lib.CS_ROUND_TORCH if momentum else _lib.CS_ROUND_REFERENCE)
     p0, m0 = p.cpu().clone(), (mom.cpu().clone() if mom is not None else None)
-    _lib.check("p2p", _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(d), ctypes.byref(h), _stream()))
-    torch.cuda.synchronize()
+    if variant == "bulk":
+        d.max_ctas = 3                                    # fewer CTAs than tiles: the stage ring wraps
+        _lib.tune("p2p_bulk", 1)
+    try:
+        _lib.check("p2p", _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(d), ctypes.byref(h), _stream()))
+        torch.cuda.synchronize()
+    finally:
+        _lib.tune("p2p_bulk", 0)
     acc = torch.zeros(shard)
     for sr in srcs:
         acc = acc + sr.cpu()                              # rank order, fp32, one rounding per add
