@@ -65,8 +65,8 @@ def parse():
                     help="cross-rank barrier of the p2p / ce transports: SM-free stream-memory-op "
                          "flags (auto when supported) or a 1-element NCCL all-reduce")
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
-    ap.add_argument("--p2p-bulk", action="store_true",
-                    help="capped P2P launches stream tiles through shared memory with cp.async.bulk (TMA)")
+    ap.add_argument("--p2p-registers", action="store_true",
+                    help="capped P2P launches use the register kernel instead of the cp.async.bulk (TMA) one")
     ap.add_argument("--rotation-graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each rotation as one CUDA graph (graphs.RotationGraph); auto = on for "
                          "--config mlp (launch-bound), off for the image models")
@@ -911,10 +911,10 @@ def run_ours(args):
     global P2P_CTAS, BARRIER, SYNC_CTAS
     if args.p2p_ctas:   # override the scheduler's policy-dependent cap, both arms
         P2P_CTAS = args.p2p_ctas
-    if args.p2p_bulk:
+    if args.p2p_registers:
         from paper_2103_07974_b200 import _lib as _cs
 
-        _cs.tune("p2p_bulk", 1)
+        _cs.tune("p2p_bulk", 0)
     BARRIER = args.barrier
     SYNC_CTAS = args.sync_ctas
     if args.bn_no_pdl:
@@ -1031,8 +1031,7 @@ def run_ours(args):
                                      + ("" if args.cudnn_stem else ", RGB stem as im2col + GEMMs"))
         if args.mix:
             impl["mix"] = args.mix
-        if args.p2p_bulk:
-            impl["p2p_variant"] = "cp.async.bulk (TMA) tiles for capped launches"
+        impl["p2p_capped_variant"] = "registers" if args.p2p_registers else "cp.async.bulk (TMA) tiles"
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": round(rot_cross, 3), "higher_is_better": True,

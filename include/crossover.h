@@ -92,7 +92,8 @@ CS_API const char* cs_last_error(void);
 
 /* Launch-shape knobs (0 restores the built-in default): of the register K1/K2 "reg_shape"
  * (0..4: unroll x CTAs/SM); of the fused P2P kernel: "p2p_ctas" (persistent grid cap, 0 = default
- * 2 CTAs per SM); of the K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
+ * 2 CTAs per SM) and "p2p_bulk" (1, the default: a launch with max_ctas > 0 streams tiles through
+ * shared memory with cp.async.bulk; 0: the register kernel); of the K1/K2: "sync_ctas" (persistent grid cap, default 0 = one CTA per chunk) -- a
  * sync that overlaps another app's compute with slack can trade speed for fewer SMs; of the BN
  * kernels: "bn_no_pdl" (1 = launch finalize / apply without programmatic dependent launch),
  * "bn_ctas_per_sm" (row-block CTAs per SM of the partial kernels, 0 = 3; changes the partial

@@ -154,17 +154,25 @@ static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream
 // registers), completion counted by one mbarrier per stage; all threads reduce a landed stage in
 // rank order, apply the update and store the new slice to every rank while the next stages are in
 // flight.  The arithmetic is p2p_chunk's (same order, same sgd_elem), so the result is bitwise
-// identical.  Selected with cs_tune("p2p_bulk", 1) for launches whose grid cap is set.
+// identical.  Used for every launch whose grid cap is set (the crossover case), unless
+// cs_tune("p2p_bulk", 0); the uncapped whole-GPU launch keeps the register kernel.
 // ---------------------------------------------------------------------------------------------
-int g_tune_p2p_bulk = 0;
-constexpr int kBulkTile = 2048;                 // floats per buffer per stage (8 KB)
+int g_tune_p2p_bulk = 1;
 
+// floats per buffer per stage: 16 KB at W <= 2 (fewer, longer tiles: the per-tile wait / barrier /
+// issue overhead is paid half as often), 8 KB above; stages so a CTA keeps 128-192 KB in flight
 template <int MAXW>
-__host__ __device__ constexpr int bulk_stages() { return MAXW <= 2 ? 4 : (MAXW <= 4 ? 3 : 2); }
+__host__ __device__ constexpr int bulk_tile() { return MAXW <= 2 ? 4096 : 2048; }
+template <int MAXW>
+__host__ __device__ constexpr int bulk_stages() { return MAXW <= 2 ? 3 : (MAXW <= 4 ? 3 : 2); }
 template <bool kMom, int MAXW>
 __host__ __device__ constexpr int bulk_buffers() { return MAXW + (kMom ? 2 : 1); }
 template <bool kMom, int MAXW>
-constexpr size_t bulk_smem_bytes() { return (size_t)bulk_stages<MAXW>() * bulk_buffers<kMom, MAXW>() * kBulkTile * 4; }
+constexpr size_t bulk_smem_bytes() {
+  return (size_t)bulk_stages<MAXW>() * bulk_buffers<kMom, MAXW>() * bulk_tile<MAXW>() * 4;
+}
+static_assert(bulk_smem_bytes<true, 2>() <= 227 * 1024 && bulk_smem_bytes<true, 4>() <= 227 * 1024 &&
+              bulk_smem_bytes<true, CS_MAX_SOURCES>() <= 227 * 1024, "bulk P2P ring exceeds shared memory");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -180,6 +188,7 @@ template <bool kMom, int MAXW>
 __global__ void __launch_bounds__(kThreads, 1)
 p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
   constexpr int S = bulk_stages<MAXW>();
+  constexpr int kBulkTile = bulk_tile<MAXW>();
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[S];
   const Rule r = make_rule(h, kMom);
@@ -248,7 +257,9 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ c
 }
 
 template <int MAXW>
-static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_sgd_hyper& h, int grid, cudaStream_t s) {
+static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
+  const int64_t tiles = (d.numel + bulk_tile<MAXW>() - 1) / bulk_tile<MAXW>();
+  const int grid = (int)(tiles < d.max_ctas ? tiles : d.max_ctas);
   const bool mom = h.momentum != 0.0f;
   const size_t smem = mom ? bulk_smem_bytes<true, MAXW>() : bulk_smem_bytes<false, MAXW>();
   auto* k = mom ? p2p_bulk_kernel<true, MAXW> : p2p_bulk_kernel<false, MAXW>;
@@ -331,11 +342,9 @@ cudaError_t launch_p2p_gather(const cs_p2p_desc* chunks, int64_t nchunks, int nr
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
   if (g_tune_p2p_bulk && d.max_ctas > 0 && d.numel % 4 == 0) {
-    const int64_t tiles = (d.numel + kBulkTile - 1) / kBulkTile;
-    const int grid = (int)(tiles < d.max_ctas ? tiles : d.max_ctas);
-    if (d.nranks <= 2) return launch_bulk<2>(d, h, grid, s);
-    if (d.nranks <= 4) return launch_bulk<4>(d, h, grid, s);
-    return launch_bulk<CS_MAX_SOURCES>(d, h, grid, s);
+    if (d.nranks <= 2) return launch_bulk<2>(d, h, s);
+    if (d.nranks <= 4) return launch_bulk<4>(d, h, s);
+    return launch_bulk<CS_MAX_SOURCES>(d, h, s);
   }
   if (d.nranks <= 2) launch_p2p_u<4, 2>(d, h, s);
   else if (d.nranks <= 4) launch_p2p_u<2, 4>(d, h, s);

@@ -242,14 +242,13 @@ def test_p2p_kernel_emulated_ranks(cuda_device, world, momentum, variant):
     h = _lib.SgdHyper(lr=0.05, momentum=momentum, dampening_complement=1.0, divisor=world,
                       first_step=0, rounding=_lib.CS_ROUND_TORCH if momentum else _lib.CS_ROUND_REFERENCE)
     p0, m0 = p.cpu().clone(), (mom.cpu().clone() if mom is not None else None)
-    if variant == "bulk":
-        d.max_ctas = 3                                    # fewer CTAs than tiles: the stage ring wraps
-        _lib.tune("p2p_bulk", 1)
+    d.max_ctas = 1                                        # one CTA walks every tile: the stage ring wraps
+    _lib.tune("p2p_bulk", 1 if variant == "bulk" else 0)
     try:
         _lib.check("p2p", _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(d), ctypes.byref(h), _stream()))
         torch.cuda.synchronize()
     finally:
-        _lib.tune("p2p_bulk", 0)
+        _lib.tune("p2p_bulk", 1)
     acc = torch.zeros(shard)
     for sr in srcs:
         acc = acc + sr.cpu()                              # rank order, fp32, one rounding per add

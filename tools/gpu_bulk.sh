@@ -1,0 +1,12 @@
+# TMA bulk-copy P2P variant: bitwise kernel test, then the config-2 bench with the capped P2P kernel
+# in registers vs bulk.  Run under gpurun --gpus 4.
+python -c "import sys; sys.path.insert(0,'.'); from paper_2103_07974_b200 import _build; _build.build(force=True)" || exit 1
+O=gpurun_out/bulk; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -m gpu -p no:cacheprovider -k p2p_kernel_emulated > $O/pytest.log 2>&1; rc=$?; echo pytest rc=$rc; tail -3 $O/pytest.log
+[ $rc = 0 ] || exit 1
+run() { n=$1; tag=$2; shift 2
+  R="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1"
+  timeout 600 $R --master-port $((29900 + RANDOM % 90)) bench.py --gpus $n --sync-mode p2p --steps 20 --warmup 5 --no-cpu-baseline --no-e2e "$@" > $O/b_n${n}_$tag.json 2> $O/b_n${n}_$tag.err; echo b n$n $tag rc=$?
+}
+run 4 reg; run 4 bulk --p2p-bulk; run 4 reg32 --p2p-ctas 32; run 4 bulk32 --p2p-ctas 32 --p2p-bulk
+run 2 reg; run 2 bulk --p2p-bulk
