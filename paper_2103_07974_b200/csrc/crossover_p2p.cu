@@ -184,47 +184,68 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-template <bool kMom, int MAXW>
+// kTable = false: the tiles of one contiguous shard (d); kTable = true: the p2p_gather chunk table
+// (one cs_p2p_desc per chunk, numel <= one tile, not necessarily a multiple of 4: the copy is
+// rounded up to 16 bytes -- inside the caching allocator's 512-byte blocks and the padded layout --
+// and the last n & 3 elements take a scalar path).  Thread 0 writes each stage's tile descriptor
+// into shared memory before arming its mbarrier, so the consumers read it after the wait.
+template <bool kMom, int MAXW, bool kTable>
 __global__ void __launch_bounds__(kThreads, 1)
-p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ cs_sgd_hyper h) {
+p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const cs_p2p_desc* __restrict__ table, int64_t ntable,
+                const __grid_constant__ cs_sgd_hyper h) {
   constexpr int S = bulk_stages<MAXW>();
   constexpr int kBulkTile = bulk_tile<MAXW>();
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(16) cs_p2p_desc info[S];
   const Rule r = make_rule(h, kMom);
   const int W = d.nranks;
   const int nb = W + (kMom ? 2 : 1);             // buffers of a stage: W sources, p (, m)
-  const int64_t tiles = (d.numel + kBulkTile - 1) / kBulkTile;
-  const int64_t mine = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t units = kTable ? ntable : (d.numel + kBulkTile - 1) / kBulkTile;
+  const int64_t mine = units > blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int64_t k, int s) {           // thread 0: tile k of this CTA into stage s
-    const int64_t e0 = (blockIdx.x + k * gridDim.x) * kBulkTile;
-    const int64_t rem = d.numel - e0;
-    const uint32_t bytes = (uint32_t)((rem < kBulkTile ? rem : kBulkTile) * 4);
+    const int64_t u = blockIdx.x + k * gridDim.x;
+    cs_p2p_desc& t = info[s];
+    if (kTable) {
+      t = table[u];
+    } else {
+      const int64_t e0 = u * kBulkTile;
+      const int64_t rem = d.numel - e0;
+      for (int b = 0; b < W; ++b) {
+        t.src[b] = d.src[b] + 4 * (uint64_t)e0;
+        t.dst[b] = d.dst[b] + 4 * (uint64_t)e0;
+      }
+      t.param = d.param + e0;
+      t.momentum_buf = kMom ? d.momentum_buf + e0 : nullptr;
+      t.numel = rem < kBulkTile ? rem : kBulkTile;
+    }
+    const uint32_t bytes = (uint32_t)((t.numel * 4 + 15) & ~(int64_t)15);
     const uint32_t bar = smem_u32(&full[s]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * nb) : "memory");
     float* st = ring + (size_t)s * nb * kBulkTile;
     for (int b = 0; b < nb; ++b) {
-      const float* src = b < W ? (const float*)d.src[b] : (b == W ? d.param : d.momentum_buf);
+      const float* src = b < W ? (const float*)t.src[b] : (b == W ? t.param : t.momentum_buf);
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(st + (size_t)b * kBulkTile)), "l"(src + e0), "r"(bytes), "r"(bar)
+                   ::"r"(smem_u32(st + (size_t)b * kBulkTile)), "l"(src), "r"(bytes), "r"(bar)
                    : "memory");
     }
   };
   if (threadIdx.x == 0)
     for (int k = 0; k < S && k < mine; ++k) issue(k, k);
+  constexpr int V = kBulkTile / 4;                 // float4 per buffer
   for (int64_t k = 0; k < mine; ++k) {
     const int s = (int)(k % S);
     mbar_wait(smem_u32(&full[s]), (uint32_t)((k / S) & 1));
-    const int64_t e0 = (blockIdx.x + k * gridDim.x) * kBulkTile;
-    const int64_t rem = d.numel - e0;
-    const int nvec = (int)((rem < kBulkTile ? rem : kBulkTile) >> 2);
-    const float4* st = reinterpret_cast<const float4*>(ring + (size_t)s * nb * kBulkTile);
-    constexpr int V = kBulkTile / 4;               // float4 per buffer
+    const cs_p2p_desc& t = info[s];
+    const int n = (int)t.numel;
+    const int nvec = n >> 2;
+    const float* sf = ring + (size_t)s * nb * kBulkTile;
+    const float4* st = reinterpret_cast<const float4*>(sf);
     for (int v = threadIdx.x; v < nvec; v += kThreads) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -244,8 +265,18 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ c
       o.y = sgd_elem(r, acc.y, pv.y, &mv.y);
       o.z = sgd_elem(r, acc.z, pv.z, &mv.z);
       o.w = sgd_elem(r, acc.w, pv.w, &mv.w);
-      if (kMom) st4(d.momentum_buf + e0 + 4 * v, mv);
-      for (int dst = 0; dst < W; ++dst) st4((float*)d.dst[dst] + e0 + 4 * v, o);   // fused all-gather
+      if (kMom) st4(t.momentum_buf + 4 * v, mv);
+      for (int dst = 0; dst < W; ++dst) st4((float*)t.dst[dst] + 4 * v, o);   // fused all-gather
+    }
+    if (kTable) {
+      for (int e = 4 * nvec + threadIdx.x; e < n; e += kThreads) {   // tensor tail (n & 3 elements)
+        float a = 0.0f;
+        for (int src = 0; src < W; ++src) a = __fadd_rn(a, sf[src * kBulkTile + e]);
+        float b = kMom ? sf[(W + 1) * kBulkTile + e] : 0.0f;
+        const float np = sgd_elem(r, a, sf[W * kBulkTile + e], &b);
+        if (kMom) t.momentum_buf[e] = b;
+        for (int dst = 0; dst < W; ++dst) ((float*)t.dst[dst])[e] = np;
+      }
     }
     __syncthreads();                               // every thread is done with stage s
     if (threadIdx.x == 0 && k + S < mine) {
@@ -256,16 +287,18 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const __grid_constant__ c
   __threadfence_system();
 }
 
-template <int MAXW>
-static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
-  const int64_t tiles = (d.numel + bulk_tile<MAXW>() - 1) / bulk_tile<MAXW>();
-  const int grid = (int)(tiles < d.max_ctas ? tiles : d.max_ctas);
+template <int MAXW, bool kTable>
+static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_p2p_desc* table, int64_t ntable, int max_ctas,
+                               const cs_sgd_hyper& h, cudaStream_t s) {
+  const int64_t units = kTable ? ntable : (d.numel + bulk_tile<MAXW>() - 1) / bulk_tile<MAXW>();
+  const int grid = (int)(units < max_ctas ? units : max_ctas);
+  if (grid <= 0) return cudaSuccess;
   const bool mom = h.momentum != 0.0f;
   const size_t smem = mom ? bulk_smem_bytes<true, MAXW>() : bulk_smem_bytes<false, MAXW>();
-  auto* k = mom ? p2p_bulk_kernel<true, MAXW> : p2p_bulk_kernel<false, MAXW>;
+  auto* k = mom ? p2p_bulk_kernel<true, MAXW, kTable> : p2p_bulk_kernel<false, MAXW, kTable>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)grid, kThreads, smem, s>>>(d, h);
+  k<<<(unsigned)grid, kThreads, smem, s>>>(d, table, ntable, h);
   return cudaGetLastError();
 }
 
@@ -333,6 +366,13 @@ int64_t p2p_gather_chunk_elems(int nranks) {
 cudaError_t launch_p2p_gather(const cs_p2p_desc* chunks, int64_t nchunks, int nranks, int max_ctas,
                               const cs_sgd_hyper& h, cudaStream_t s) {
   if (nchunks == 0) return cudaSuccess;
+  if (g_tune_p2p_bulk && max_ctas > 0) {           // capped: the TMA-fed ring (the tile fields come
+    cs_p2p_desc d = {};                            // from the table; d carries only W)
+    d.nranks = nranks;
+    if (nranks <= 2) return launch_bulk<2, true>(d, chunks, nchunks, max_ctas, h, s);
+    if (nranks <= 4) return launch_bulk<4, true>(d, chunks, nchunks, max_ctas, h, s);
+    return launch_bulk<CS_MAX_SOURCES, true>(d, chunks, nchunks, max_ctas, h, s);
+  }
   if (nranks <= 2) launch_gather_u<4, 2>(chunks, nchunks, max_ctas, h, s);
   else if (nranks <= 4) launch_gather_u<2, 4>(chunks, nchunks, max_ctas, h, s);
   else launch_gather_u<1, CS_MAX_SOURCES>(chunks, nchunks, max_ctas, h, s);
@@ -342,9 +382,9 @@ cudaError_t launch_p2p_gather(const cs_p2p_desc* chunks, int64_t nchunks, int nr
 cudaError_t launch_p2p(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream_t s) {
   if (d.numel == 0) return cudaSuccess;
   if (g_tune_p2p_bulk && d.max_ctas > 0 && d.numel % 4 == 0) {
-    if (d.nranks <= 2) return launch_bulk<2>(d, h, s);
-    if (d.nranks <= 4) return launch_bulk<4>(d, h, s);
-    return launch_bulk<CS_MAX_SOURCES>(d, h, s);
+    if (d.nranks <= 2) return launch_bulk<2, false>(d, nullptr, 0, d.max_ctas, h, s);
+    if (d.nranks <= 4) return launch_bulk<4, false>(d, nullptr, 0, d.max_ctas, h, s);
+    return launch_bulk<CS_MAX_SOURCES, false>(d, nullptr, 0, d.max_ctas, h, s);
   }
   if (d.nranks <= 2) launch_p2p_u<4, 2>(d, h, s);
   else if (d.nranks <= 4) launch_p2p_u<2, 4>(d, h, s);
