@@ -123,6 +123,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--scenario-band", action="store_true")
     ap.add_argument("--spans", action="store_true", help="(always on) crossover phase medians and GPU idle")
+    ap.add_argument("--p2p-registers", action="store_true",
+                    help="capped P2P launches use the register kernel instead of the cp.async.bulk ring")
     ap.add_argument("--energy", action="store_true",
                     help="board power over every timed region (NVML energy counter) and the power bound")
     ap.add_argument("--out", default="")
@@ -133,6 +135,10 @@ def main():
 
     h = Harness()
     global FLAT_KIND, IDLE_W
+    if args.p2p_registers:
+        from paper_2103_07974_b200 import _lib
+
+        _lib.tune("p2p_bulk", 0)
     if args.energy:
         bench.ENERGY = bench.Energy(h.dev)
         torch.cuda.synchronize()
@@ -166,6 +172,7 @@ def main():
     per_byte = (t2 - t1) / (s2 - s1)
     alpha = t1 - s1 * per_byte
     res = {"world": h.world, "compute": args.compute, "comp_ms": args.comp_ms, "sync_mode": args.sync_mode,
+           "p2p_capped_variant": "registers" if args.p2p_registers else "cp.async.bulk ring",
            "pack_engine": args.pack_engine,
            "sync_ctas": args.sync_ctas, "steps": args.steps,
            "calibration": {"alpha_ms": round(alpha, 5), "GB_per_s": round(1e-6 / per_byte, 1),
