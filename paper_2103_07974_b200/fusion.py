@@ -594,17 +594,15 @@ class FusedGradientSync:
         flat = self._flat_map.addresses
         mom = self.momentum_bufs[0].data_ptr() if self.momentum_bufs else 0
         rows = []
-        for i, (o, n) in enumerate(zip(lay.offsets, lay.numels)):
-            for a in range(max(o, s0), min(o + n, s1), ch):
-                b = min(a + ch, o + n, s1)
-                row = np.zeros((), dtype=_lib.P2P_DESC)
-                row["src"][:self.ranks] = [addrs[r][i] + 4 * (a - o) for r in range(self.ranks)]
-                row["dst"][:self.ranks] = [flat[r] + 4 * a for r in range(self.ranks)]
-                row["param"] = self.flat.data_ptr() + 4 * a
-                row["momentum_buf"] = mom + 4 * (a - s0) if mom else 0
-                row["numel"] = b - a
-                row["nranks"] = self.ranks
-                rows.append(row)
+        for i, o, a, b in gather_chunks(lay.offsets, lay.numels, s0, s1, ch):
+            row = np.zeros((), dtype=_lib.P2P_DESC)
+            row["src"][:self.ranks] = [addrs[r][i] + 4 * (a - o) for r in range(self.ranks)]
+            row["dst"][:self.ranks] = [flat[r] + 4 * a for r in range(self.ranks)]
+            row["param"] = self.flat.data_ptr() + 4 * a
+            row["momentum_buf"] = mom + 4 * (a - s0) if mom else 0
+            row["numel"] = b - a
+            row["nranks"] = self.ranks
+            rows.append(row)
         table = np.array(rows, dtype=_lib.P2P_DESC)
         _lib.check("cs_p2p_gather_check", _lib.lib.cs_p2p_gather_check(
             table.ctypes.data, len(table), self.ranks, int(bool(mom))))
@@ -767,6 +765,15 @@ class FusedGradientSync:
         """All-reduce bus bytes 2(W-1)/W * S (== reduce-scatter + all-gather in sharded mode)."""
         w = self.ranks
         return 0.0 if w <= 1 else 2.0 * (w - 1) / w * self.layout.bucket_bytes
+
+
+def gather_chunks(offsets: Sequence[int], numels: Sequence[int], s0: int, s1: int, ch: int):
+    """The p2p_gather work list of the shard [s0, s1) of a bucket layout: (tensor index, tensor
+    offset, a, b) for every chunk [a, b) -- inside one tensor and the shard, at most `ch` elements,
+    in bucket order; the padding between tensors is not covered (it holds no gradient)."""
+    for i, (o, n) in enumerate(zip(offsets, numels)):
+        for a in range(max(o, s0), min(o + n, s1), ch):
+            yield i, o, a, min(a + ch, o + n, s1)
 
 
 _zero_cache: dict[tuple, torch.Tensor] = {}
