@@ -158,6 +158,8 @@ static void launch_p2p_u(const cs_p2p_desc& d, const cs_sgd_hyper& h, cudaStream
 // cs_tune("p2p_bulk", 0); the uncapped whole-GPU launch keeps the register kernel.
 // ---------------------------------------------------------------------------------------------
 int g_tune_p2p_bulk = 1;
+constexpr int kDescVecs = (int)(sizeof(cs_p2p_desc) / 16);
+static_assert(sizeof(cs_p2p_desc) % 16 == 0, "cs_p2p_desc must be a whole number of 16-byte vectors");
 
 // floats per buffer per stage: 16 KB at W <= 2 (fewer, longer tiles: the per-tile wait / barrier /
 // issue overhead is paid half as often), 8 KB above; stages so a CTA keeps 128-192 KB in flight
@@ -198,11 +200,22 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const cs_p2p_desc* __rest
   extern __shared__ __align__(128) float ring[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(16) cs_p2p_desc info[S];
+  __shared__ __align__(16) cs_p2p_desc pf[kTable ? S : 1];   // table entries prefetched S tiles ahead
   const Rule r = make_rule(h, kMom);
   const int W = d.nranks;
   const int nb = W + (kMom ? 2 : 1);             // buffers of a stage: W sources, p (, m)
   const int64_t units = kTable ? ntable : (d.numel + kBulkTile - 1) / kBulkTile;
   const int64_t mine = units > blockIdx.x ? (units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto prefetch = [&](int64_t k, int s) {        // thread 0: table entry of tile k -> pf[s], one group
+    if (k < mine) {
+      const char* g = reinterpret_cast<const char*>(table + blockIdx.x + k * gridDim.x);
+      for (int v = 0; v < kDescVecs; ++v)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(reinterpret_cast<char*>(&pf[s]) + 16 * v)),
+                     "l"(g + 16 * v)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -212,7 +225,11 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const cs_p2p_desc* __rest
     const int64_t u = blockIdx.x + k * gridDim.x;
     cs_p2p_desc& t = info[s];
     if (kTable) {
-      t = table[u];
+      // entry k landed: groups are committed one per tile in order (S in the prologue, then one
+      // per issue), so at most S - 1 younger ones may still be pending
+      asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+      t = pf[s];
+      prefetch(k + S, s);
     } else {
       const int64_t e0 = u * kBulkTile;
       const int64_t rem = d.numel - e0;
@@ -235,8 +252,11 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const cs_p2p_desc* __rest
                    : "memory");
     }
   };
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    if (kTable)
+      for (int k = 0; k < S; ++k) prefetch(k, k);
     for (int k = 0; k < S && k < mine; ++k) issue(k, k);
+  }
   constexpr int V = kBulkTile / 4;                 // float4 per buffer
   for (int64_t k = 0; k < mine; ++k) {
     const int s = (int)(k % S);
@@ -284,6 +304,7 @@ p2p_bulk_kernel(const __grid_constant__ cs_p2p_desc d, const cs_p2p_desc* __rest
       issue(k + S, s);
     }
   }
+  if (kTable && threadIdx.x == 0) asm volatile("cp.async.wait_all;" ::: "memory");
   __threadfence_system();
 }
 
@@ -309,8 +330,6 @@ static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_p2p_desc* table, i
 // is processed, so the table lookup adds no latency to the peer loads.  The per-element code is
 // p2p_chunk's, so the arithmetic is bit-identical to the bucket kernel.
 // ---------------------------------------------------------------------------------------------
-constexpr int kDescVecs = (int)(sizeof(cs_p2p_desc) / 16);
-static_assert(sizeof(cs_p2p_desc) % 16 == 0, "cs_p2p_desc must be a whole number of 16-byte vectors");
 
 __device__ __forceinline__ void desc_prefetch(cs_p2p_desc* dst, const cs_p2p_desc* src) {
   if (threadIdx.x < kDescVecs) {
