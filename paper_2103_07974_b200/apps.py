@@ -16,6 +16,7 @@ every gather, forward, backward and update runs on the device.
 
 from __future__ import annotations
 
+import contextlib
 import math
 from dataclasses import dataclass
 from typing import Sequence
@@ -223,13 +224,17 @@ def _ce_loss(model, batch):
 
 def mlp_app(config: MlpConfig, job_id: str, rng_seed: int, iterations: int,
             device: torch.device, local_workers: int | None = None,
-            worker_count: int | None = None, flat: bool = False) -> App:
-    """Config 1 app: two of these co-located, W = 2, batch 64 per worker."""
+            worker_count: int | None = None, flat: bool = False, graphed: bool = False) -> App:
+    """Config 1 app: two of these co-located, W = 2, batch 64 per worker.  ``graphed``: forward and
+    backward as CUDA graphs (fp32), so the gradients come back in static buffers (p2p_gather)."""
     x, y = make_mlp_dataset(config)
     workers = config.workers if worker_count is None else worker_count
     idx = _index_table(rng_seed, iterations, workers, config.dataset_size, config.batch_size)
     model = _mlp_module(config, mlp_initial_parameters(config, rng_seed)).to(device)
-    flat_params = _flatten(list(model.parameters()), flat)
+    flat_params = _flatten(list(model.parameters()), flat)   # before any graph captures the addresses
+    if graphed:
+        model = _GraphedImageModel(model, torch.zeros(config.batch_size, config.in_dim, device=device),
+                                   autocast=False)
     data = _GatherData(torch.as_tensor(x, dtype=torch.float32, device=device),
                        torch.as_tensor(y, dtype=torch.int64, device=device),
                        torch.as_tensor(idx, device=device))
@@ -317,13 +322,15 @@ class _GraphedImageModel(torch.nn.Module):
     scheduler keeps alive until the app's K2 has consumed them.
     """
 
-    def __init__(self, model: torch.nn.Module, sample: torch.Tensor):
+    def __init__(self, model: torch.nn.Module, sample: torch.Tensor, autocast: bool = True):
         super().__init__()
         self.inner = model
         quiet = getattr(torch.autograd.graph, "set_warn_on_accumulate_grad_stream_mismatch", None)
         if quiet is not None:  # capture runs on a side stream by design
             quiet(False)
-        with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+        amp = (torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False) if autocast
+               else contextlib.nullcontext())
+        with amp:
             self.graphed = torch.cuda.make_graphed_callables(model, (sample,), num_warmup_iters=3)
 
     def forward(self, x):

@@ -24,6 +24,7 @@ CASE resnet   two ResNet-50 apps (bf16 autocast, CUDA graphs, momentum 0.9, weig
               through ce for 3 iterations: every rank's update equals torch.optim.SGD
               (foreach=False) on the CPU applied to the rank-order average of the W ranks'
               captured gradients, bit for bit.
+CASE gather_mlp  p2p_gather at W = 2 / 4 / 8 on two CUDA-graphed MLPs: bitwise equal to p2p.
 CASE gather   the same with the K1-free p2p_gather transport (the kernel reads every rank's
               graph-static gradient tensors in place): bitwise vs torch.optim.SGD, one kernel
               launch per sync.
@@ -258,6 +259,36 @@ def case_gather(rank, world, dev, comm, res):
     _resnet_update_check(rank, world, dev, comm, res, "p2p_gather")
 
 
+def case_gather_mlp(rank, world, dev, comm, res):
+    """p2p_gather at any W on a cheap model: two CUDA-graphed MLP 784-256-10 apps (momentum),
+    per-iteration weights bitwise equal to the p2p transport on the same graphed apps and to p2p on
+    the eager apps, ranks identical, one kernel per sync."""
+    T = 6
+    specs = [(11, 0), (12, 1)]
+    out = {}
+    for mode, graphed in (("p2p_gather", True), ("p2p", True), ("p2p", False)):
+        apps = [mlp_app(MlpConfig(dataset_seed=ds, workers=world, momentum=0.9), f"m{k}", rs, T, dev,
+                        local_workers=1, worker_count=world, flat="ipc", graphed=graphed)
+                for k, (ds, rs) in enumerate(specs)]
+        s = CrossoverScheduler(Policy.CROSSOVER, comm=comm, record_weights=True, sync_mode=mode)
+        for a in apps:
+            s.register(a)
+        s.run()
+        out[(mode, graphed)] = [s.weights(a.job_id).cpu().clone() for a in apps]
+        if mode == "p2p_gather":
+            launches = [st.sync.kernel_launches for st in s.states]
+            res["checks"].append({"name": "gather_mlp_one_kernel_per_sync", "ok": launches == [T, T],
+                                  "launches": launches})
+        s.close()
+    g, p, e = out[("p2p_gather", True)], out[("p2p", True)], out[("p2p", False)]
+    res["checks"].append({"name": f"gather_mlp_w{world}_bitwise_eq_p2p_graphed",
+                          "ok": all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for a, b in zip(g, p))})
+    res["checks"].append({"name": f"gather_mlp_w{world}_bitwise_eq_p2p_eager",
+                          "ok": all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for a, b in zip(g, e))})
+    res["checks"].append({"name": "gather_mlp_ranks_identical",
+                          "ok": _gather_equal(torch.cat([x.reshape(-1) for x in g]), rank, world)})
+
+
 def _resnet_update_check(rank, world, dev, comm, res, mode):
     from paper_2103_07974_b200.apps import DEFAULT_IMAGE_SGD, resnet50_app
 
@@ -325,7 +356,7 @@ def main():
     comm = PeerGroup(rank, world)
     res = {"world": world, "case": case, "ok": True, "checks": []}
     {"parity": case_parity, "fail": case_fail, "resnet": case_resnet,
-     "graph": case_graph, "gather": case_gather}[case](rank, world, dev, comm, res)
+     "graph": case_graph, "gather": case_gather, "gather_mlp": case_gather_mlp}[case](rank, world, dev, comm, res)
     res["ok"] = all(c["ok"] for c in res["checks"])
     oks = [None] * world
     dist.all_gather_object(oks, res["ok"])

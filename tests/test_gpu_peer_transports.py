@@ -70,3 +70,11 @@ def test_p2p_gather_resnet50_update_parity(tmp_path, world):
     gradient tensors in place (161 ResNet-50 tensors cut at the W shard boundaries); bitwise
     torch.optim.SGD(foreach=False) on the rank-order average, 3 iterations x 2 apps."""
     _launch(tmp_path, world, "gather", 29760 + world)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_p2p_gather_graphed_mlp(tmp_path, world):
+    """p2p_gather at W = 2 / 4 / 8 (every chunk-table width of the kernel) on two CUDA-graphed MLP
+    apps: per-iteration weights bitwise equal to the p2p transport (graphed and eager), ranks
+    identical, one kernel launch per sync."""
+    _launch(tmp_path, world, "gather_mlp", 29770 + world)
