@@ -577,7 +577,9 @@ class FusedGradientSync:
     def _gather_plan(self, grads: Sequence[torch.Tensor]) -> None:
         """Chunks of this rank's shard -- none crossing a gradient tensor -- with every rank's
         gradient addresses (collective: map_peer_tensors), uploaded once; the gradients must keep
-        these addresses for every later sync."""
+        these addresses for every later sync.  Runs inside the app's first sync (the addresses
+        exist only after the first backward), so that one step pays a host round trip for the
+        handle exchange and the table upload; every later step is asynchronous."""
         from .p2p import map_peer_tensors
 
         if len(grads) != len(self.params):
