@@ -317,8 +317,16 @@ static cudaError_t launch_bulk(const cs_p2p_desc& d, const cs_p2p_desc* table, i
   const bool mom = h.momentum != 0.0f;
   const size_t smem = mom ? bulk_smem_bytes<true, MAXW>() : bulk_smem_bytes<false, MAXW>();
   auto* k = mom ? p2p_bulk_kernel<true, MAXW, kTable> : p2p_bulk_kernel<false, MAXW, kTable>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // the dynamic shared-memory opt-in, once per instantiation and device (a racing second call
+  // only repeats the same idempotent setting)
+  static bool opted[2][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !opted[mom][dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) opted[mom][dev] = true;
+  }
   k<<<(unsigned)grid, kThreads, smem, s>>>(d, table, ntable, h);
   return cudaGetLastError();
 }
