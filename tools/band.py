@@ -20,7 +20,6 @@ gpu_lane_busy_frac (compute phases / crossover rotation; 1 = the schedule hid ev
 backward = 30 : 70) with the compute dialed to the scenario's priced rho = 3/20.
 """
 import argparse
-import dataclasses
 import json
 import statistics
 import sys
