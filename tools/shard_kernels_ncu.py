@@ -1,6 +1,7 @@
 """Single-GPU stand-ins of the W-rank shard kernels, for ncu --set full (DRAM traffic per launch).
 
-    ncu --set full -k regex:"unpack_sgd|p2p_reduce" -c 4 -o prof python tools/shard_kernels_ncu.py [--world 4]
+    ncu --set full -k regex:"unpack_sgd|p2p_reduce|p2p_bulk" -c 4 -o prof python tools/shard_kernels_ncu.py
+        [--world 4] [--p2p-ctas 32 [--registers]]
 
 ncu cannot replay a multi-rank command, so the kernels of the `ce` and `p2p` transports are run
 here on one GPU with the W ranks' buffers all local (same kernels, same launch shapes, same
@@ -26,6 +27,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--world", type=int, default=4)
     ap.add_argument("--bucket-bytes", type=int, default=102_228_128)   # ResNet-50
+    ap.add_argument("--p2p-ctas", type=int, default=0,
+                    help="grid cap of the P2P launches (> 0: the crossover shape, TMA ring by default)")
+    ap.add_argument("--registers", action="store_true", help="capped P2P launches on the register kernel")
     args = ap.parse_args()
     from paper_2103_07974_b200 import _lib
 
@@ -52,6 +56,8 @@ def main():
     for r in range(W):
         d.src[r], d.dst[r] = srcs[r].data_ptr(), dsts[r].data_ptr()
     d.param, d.momentum_buf, d.numel, d.nranks = p.data_ptr(), mom.data_ptr(), shard, W
+    d.max_ctas = args.p2p_ctas
+    _lib.tune("p2p_bulk", 0 if args.registers else 1)
     for _ in range(2):
         _lib.check("p2p", _lib.lib.cs_p2p_reduce_sgd_bcast(ctypes.byref(d), ctypes.byref(h), s))
     torch.cuda.synchronize()
