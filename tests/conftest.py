@@ -20,6 +20,15 @@ except ImportError:  # pragma: no cover
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    # the C-ABI tests load libcrossover.so: build it (nvcc cross-compiles, no GPU needed) when a
+    # fresh checkout has none or its sources changed -- the product itself never builds on import
+    try:
+        from paper_2103_07974_b200 import _build
+
+        if _build.needs_rebuild():
+            _build.build()
+    except Exception as exc:  # noqa: BLE001 - no nvcc: the tests that need the library will say so
+        print(f"conftest: libcrossover.so not built ({exc})", file=sys.stderr)
 
 
 @pytest.fixture(scope="session")
