@@ -65,6 +65,8 @@ def parse():
                     help="cross-rank barrier of the p2p / ce transports: SM-free stream-memory-op "
                          "flags (auto when supported) or a 1-element NCCL all-reduce")
     ap.add_argument("--p2p-ctas", type=int, default=0, help="persistent grid cap of the fused P2P kernel")
+    ap.add_argument("--reg-shape", type=int, default=None,
+                    help="K1/K2 launch shape (cs_tune reg_shape: 0..4 = unroll x CTAs/SM)")
     ap.add_argument("--p2p-registers", action="store_true",
                     help="capped P2P launches use the register kernel instead of the cp.async.bulk (TMA) one")
     ap.add_argument("--rotation-graph", default="auto", choices=["auto", "on", "off"],
@@ -911,10 +913,13 @@ def run_ours(args):
     global P2P_CTAS, BARRIER, SYNC_CTAS
     if args.p2p_ctas:   # override the scheduler's policy-dependent cap, both arms
         P2P_CTAS = args.p2p_ctas
-    if args.p2p_registers:
+    if args.p2p_registers or args.reg_shape is not None:
         from paper_2103_07974_b200 import _lib as _cs
 
-        _cs.tune("p2p_bulk", 0)
+        if args.p2p_registers:
+            _cs.tune("p2p_bulk", 0)
+        if args.reg_shape is not None:
+            _cs.tune("reg_shape", args.reg_shape)
     BARRIER = args.barrier
     SYNC_CTAS = args.sync_ctas
     if args.bn_no_pdl:
